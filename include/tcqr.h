@@ -1,0 +1,173 @@
+/*
+ * tcqr.h -- C ABI of libtcqr.so: TensorCore mixed-precision recursive Gram-Schmidt QR and
+ * R-preconditioned CGLS least squares on NVIDIA B200 (sm_100a).  arXiv 1912.05508.
+ *
+ * Method:
+ *   - Alg. 2 "Recursive Modified Gram-Schmidt QR" (Eq. (5) :313-318): split the
+ *     columns, recurse left, R12 = Q1'*A2 (line 8), recurse on A2 - Q1*R12 (line 9). Both products
+ *     run as FP16-input / FP32-accumulate tcgen05 tensor-core GEMMs ("We use TensorCore to
+ *     accelerate these matrix-matrix multiplications") at split nodes wider than
+ *     the cutoff (128, Alg. 2 line 3); below it in FP32.
+ *   - panelQR: the communication-avoiding MGS panel of Eq. (6) built from
+ *     Alg. 4 "256x32 Modified Gram-Schmidt QR" blocks.
+ *   - Alg. 5 "CGLS with RMGSQR as Preconditioner", corrected as in
+ *     DESIGN.md reading R-A10, with the stop/restart rule R-A11/R-A12.
+ *
+ * Conventions (all entry points):
+ *   - Matrices are COLUMN-MAJOR: element (i, j) of an m x n matrix X with leading dimension ldx
+ *     lives at X[i + j*ldx].  A is FP32 problem data (reading R-A14); b and x are FP64.
+ *   - Every pointer argument is a DEVICE pointer on the context device, owned by the caller; the
+ *     library never frees or retains it after the call returns.  Exception: tcqr_lls_solve_host /
+ *     tcqr_factor_host take HOST pointers (end-to-end entry points that include the copies).
+ *   - Base pointers must be 16-byte aligned and lda*4 a multiple of 16 bytes (TMA requirement).
+ *   - All calls enqueue on the context stream (tcqr_init) and synchronize on it once at the end
+ *     to read the device status, so outputs are ready when the call returns.
+ *   - Multi-GPU (row partition, one process per GPU): every rank calls with ITS OWN row block
+ *     (m = local rows, contiguous in rank order, each >= 32) and identical n, config, tol, maxit.
+ *     R and x are replicated bitwise on all ranks.
+ *
+ * Return codes (LAPACK style; identical on all ranks):
+ *     0      success (a CGLS solve that stops at maxit also returns 0 with info->converged = 0,
+ *            SPEC.md:324-325 "converged=false (not an error)")
+ *    -i      argument i is invalid (1-based position in the C signature)
+ *    +k      numerical breakdown at global column k (1-based): zero or non-finite column norm
+ *            after orthogonalization, or a non-finite entry in input column k
+ *    TCQR_ERR_CUDA / _NCCL / _OOM / _NOT_INIT  (below)
+ */
+#ifndef TCQR_H_
+#define TCQR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCQR_ERR_CUDA (-1001)
+#define TCQR_ERR_NCCL (-1002)
+#define TCQR_ERR_OOM (-1003)
+#define TCQR_ERR_NOT_INIT (-1004)
+#define TCQR_ERR_UNSUPPORTED (-1005)
+
+/* Library configuration.  All ranks must pass identical values. */
+typedef struct tcqr_config {
+  int cutoff;        /* recursion cutoff c: split nodes wider than c use FP16 tensor cores
+                        (Alg. 2 line 3; default 128; multiple of 32, >= 32)     */
+  int panel_rows;    /* CAQR block rows br (256; default 256; 64..512)      */
+  int col_scaling;   /* 1: per-column power-of-two FP16 range guard (reading R-A4; default 1) */
+  int restart;       /* 1: FP64 target, one CGLS restart from the true residual (R-A12)        */
+  double tol2;       /* restart-pass tolerance (default 1e-6, R-A12)                           */
+  int stag_window;   /* stagnation window W (default 10, R-A11)                                */
+  double stag_floor; /* stagnation floor relative to pass 1's ||s0|| (default 1e-11, R-A11)    */
+  int use_graphs;    /* 1: capture the factorization into a CUDA graph and replay (default 1)  */
+} tcqr_config_t;
+
+/* Per-solve report (SPEC.md:296-299 CglsReport). */
+typedef struct tcqr_lls_info {
+  int iterations;        /* total CGLS iterations over all passes                      */
+  int iterations_pass1;  /* iterations of pass 1                                       */
+  int outer_passes;      /* 1 or 2                                                     */
+  int converged;         /* 1 if the last pass stopped by tolerance or stagnation      */
+  int stop_reason;       /* 0 tol, 1 stagnation, 2 maxit, 3 zero right-hand side       */
+  double s0;             /* ||s_0|| of pass 1                                          */
+  double final_rel;      /* last pass: best ||s_k|| / ||s_0||                          */
+  double qr_ms;          /* device time of the factorization (CUDA events)             */
+  double cgls_ms;        /* device time of the CGLS passes                             */
+} tcqr_lls_info_t;
+
+/* Create the per-process context on `device`, enqueueing on `cuda_stream` (a cudaStream_t;
+ * NULL = legacy default stream).  nccl_unique_id: NULL for one GPU, else a pointer to the
+ * 128-byte ncclUniqueId that rank 0 created with tcqr_nccl_unique_id() and broadcast; rank /
+ * nranks as in ncclCommInitRank.  Re-initialization finalizes the previous context first. */
+int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int rank, int nranks);
+
+/* Write a fresh ncclUniqueId (128 bytes) into `out`.  Returns 0 or TCQR_ERR_NCCL. */
+int tcqr_nccl_unique_id(void* out);
+
+/* Destroy the context: frees library-owned workspace, destroys the NCCL communicator. */
+int tcqr_finalize(void);
+
+/* Default configuration. */
+void tcqr_default_config(tcqr_config_t* cfg);
+/* Set the configuration (validated; returns -1 on an invalid field). */
+int tcqr_set_config(const tcqr_config_t* cfg);
+
+/* Workspace: op = 0 factor, 1 lls_solve.  bytes receives the device workspace the call needs
+ * for an m x n problem (m = local rows).  tcqr_set_workspace hands the library caller-owned
+ * device memory (e.g. a torch tensor); when none is set (or it is too small) the library
+ * allocates its own with cudaMalloc and keeps it until tcqr_finalize. */
+int tcqr_workspace_size(int64_t m, int64_t n, int op, size_t* bytes);
+int tcqr_set_workspace(void* dptr, size_t bytes);
+
+/*
+ * tcqr_factor -- A = Q R by Alg. 2 / Eq. (6) / Alg. 4 with FP16 tensor-core trailing updates.
+ *   m, n  : rows (this rank's rows at P > 1) and columns; need sum_r m_r >= n >= 1, m >= 1.
+ *   A     : FP32 m x n column-major, leading dimension lda >= m; read only.
+ *   Q     : FP32 m x n output, leading dimension m (row-partitioned like A).  Q == A is allowed
+ *           when lda == m (the factorization then runs in place).
+ *   R     : FP32 n x n output, leading dimension n: upper triangular, diag(R) > 0, strictly lower
+ *           triangle zeroed, replicated on all ranks.
+ * Errors: -1 m, -2 n, -3 A, -4 lda, -5 Q, -6 R; +k breakdown at column k.
+ */
+int tcqr_factor(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, float* R);
+
+/*
+ * tcqr_lls_solve -- min_x ||A x - b||_2 (Eq. (1)) by tcqr_factor's R and the
+ * corrected Alg. 5.  A is not modified (the factorization runs on a workspace copy; Q is not
+ * produced, reading R-A25).
+ *   b     : FP64, m entries (this rank's rows);  x : FP64, n entries (replicated output).
+ *   tol   : pass-1 threshold on ||s_k|| / ||s_0|| (> 0);  maxit : iteration cap per pass (>= 1).
+ *   info  : optional report (may be NULL).
+ * Errors: -1 m, -2 n, -3 A, -4 lda, -5 b, -6 x, -7 tol, -8 maxit; +k breakdown in the QR.
+ */
+int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const double* b, double* x,
+                   double tol, int maxit, tcqr_lls_info_t* info);
+
+/* Host-pointer variants (end-to-end: the H2D copy of A, b and the D2H copy of the result happen
+ * inside the call; A, b, Q, R, x are HOST pointers; pinned memory is used if the caller's is). */
+int tcqr_factor_host(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, float* R);
+int tcqr_lls_solve_host(int64_t m, int64_t n, const float* A, int64_t lda, const double* b,
+                        double* x, double tol, int maxit, tcqr_lls_info_t* info);
+
+/* ---------------------------------------------------------------------------------------------
+ * Component entry points (the individual hot-path kernels, for parity tests of each §8(a) step).
+ * All pointers are device pointers; all enqueue on the context stream and synchronize.
+ * ------------------------------------------------------------------------------------------- */
+
+/* K1 (§8a a1, reading R-A4): Xh = fl16(X diag(s)), s_j = 2^-floor(log2 max_i |X_ij|) (s_j = 1 if
+ * scaling is 0 or the column is zero); inv_s[j] = 1/s_j.  X FP32 m x w (ldx), Xh FP16 bits
+ * (uint16) m x w (ldh).  Returns +j (1-based) for the first column holding a non-finite entry. */
+int tcqr_cast_scale(int64_t m, int64_t w, const float* X, int64_t ldx, uint16_t* Xh, int64_t ldh,
+                    float* inv_s, int scaling);
+
+/* K3 (§8a a4, Alg. 2 line 8): C (h x w2, ldc, FP32) = A1h' * A2h * diag(col_mult), tcgen05
+ * kind::f16 with FP32 accumulation in TMEM, deterministic split-K over the m rows.
+ * A1h: FP16 m x h (lda1), A2h: FP16 m x w2 (lda2); col_mult may be NULL (= 1). */
+int tcqr_gemm_tn(int64_t m, int64_t h, int64_t w2, const uint16_t* A1h, int64_t lda1,
+                 const uint16_t* A2h, int64_t lda2, float* C, int64_t ldc, const float* col_mult);
+
+/* K4 (§8a a5, Alg. 2 line 9 argument): C (m x w2, ldc, FP32) -= (Qh * Bh) * diag(col_mult),
+ * Qh FP16 m x h (ldq, MN-major operand), Bh FP16 h x w2 (ldb, K-major operand). */
+int tcqr_gemm_nn_update(int64_t m, int64_t h, int64_t w2, const uint16_t* Qh, int64_t ldq,
+                        const uint16_t* Bh, int64_t ldb, float* C, int64_t ldc,
+                        const float* col_mult);
+
+/* K2 (§8a a3): CAQR-MGS panel (Eq. (6) with Alg. 4 blocks of br rows), w <= 32 columns, in
+ * place on X (m x w, ldx); R (w x w, ldr) upper triangular output. */
+int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t ldr, int br);
+
+/* K6 helper (Alg. 5 lines 12/18): Minv (n x n FP64, ldm) = R^-1 for upper-triangular FP32 R. */
+int tcqr_trinv(int64_t n, const float* R, int64_t ldr, double* Minv, int64_t ldm);
+
+/* K5 (Alg. 5 lines 12/18): y = A v (trans = 0, A m x n) or y = A' v (trans = 1); A FP32, v/y FP64. */
+int tcqr_gemv(int trans, int64_t m, int64_t n, const float* A, int64_t lda, const double* v,
+              double* y);
+
+/* Library build/version string. */
+const char* tcqr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCQR_H_ */

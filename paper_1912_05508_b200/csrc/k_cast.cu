@@ -1,0 +1,165 @@
+// k_cast.cu -- K1: FP16 range guard and cast (reading R-A4), the R12
+// finalize step (unscale, write R, scaled FP16 copy for K4), input validation and small copies.
+//
+// The paper is silent on FP16 range (PAPER.md:127-141 only notes FP16's "significantly
+// constrained range"); reading R-A4 guards it with a per-column power-of-two scale
+// s_j = 2^-floor(log2 max_i |X_ij|), exact to apply and undo.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tcqr {
+
+constexpr int kCastThreads = 256;
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float r = red[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i) r = fmaxf(r, red[i]);
+  return r;
+}
+
+// One CTA per column: pass 1 max|x| (and non-finite detection), pass 2 scaled RNE cast.
+__global__ void __launch_bounds__(kCastThreads) cast_scale_kernel(
+    int m, const float* __restrict__ X, long long ldx, __half* __restrict__ Xh, long long ldh,
+    float* __restrict__ inv_s, int scaling, int* status, int col_base) {
+  __shared__ float red[32];
+  const int j = blockIdx.x;
+  const float* x = X + (long long)j * ldx;
+  __half* xh = Xh + (long long)j * ldh;
+  const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
+                   ((ldh & 3) == 0) && ((reinterpret_cast<uintptr_t>(Xh) & 7) == 0);
+  const int m4 = vec ? (m & ~3) : 0;
+  float mx = 0.f;
+  bool bad = false;
+  for (int i = threadIdx.x * 4; i < m4; i += kCastThreads * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+  }
+  for (int i = m4 + threadIdx.x; i < m; i += kCastThreads) {
+    const float v = x[i];
+    mx = fmaxf(mx, fabsf(v));
+    bad |= !isfinite(v);
+  }
+  if (bad && status) atomicMin(status, col_base + j + 1);
+  float s = 1.f;
+  if (scaling) {
+    mx = block_max(mx, red);
+    s = pow2_scale_for(mx);
+  }
+  if (threadIdx.x == 0 && inv_s) inv_s[j] = 1.f / s;
+  for (int i = threadIdx.x * 4; i < m4; i += kCastThreads * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    __half2 lo = __floats2half2_rn(v.x * s, v.y * s);
+    __half2 hi = __floats2half2_rn(v.z * s, v.w * s);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(xh + i) = pk;
+  }
+  for (int i = m4 + threadIdx.x; i < m; i += kCastThreads) xh[i] = __float2half_rn(x[i] * s);
+}
+
+cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
+                       float* inv_s, int scaling, int* status, int col_base, cudaStream_t st) {
+  if (m <= 0 || w <= 0) return cudaSuccess;
+  cast_scale_kernel<<<w, kCastThreads, 0, st>>>(m, X, ldx, Xh, ldh, inv_s, scaling, status,
+                                                 col_base);
+  return cudaGetLastError();
+}
+
+// One CTA per column j of R12: R block <- T (already unscaled), s'_j from the column max, R12h.
+__global__ void __launch_bounds__(kCastThreads) r12_finalize_kernel(
+    int h, const float* __restrict__ T, long long ldt, float* __restrict__ Rblk, long long ldr,
+    __half* __restrict__ R12h, long long ldh2, float* __restrict__ inv_s2, int scaling) {
+  __shared__ float red[32];
+  const int j = blockIdx.x;
+  const float* t = T + (long long)j * ldt;
+  float* r = Rblk + (long long)j * ldr;
+  float mx = 0.f;
+  for (int i = threadIdx.x; i < h; i += kCastThreads) {
+    const float v = t[i];
+    if (r != t) r[i] = v;
+    mx = fmaxf(mx, fabsf(v));
+  }
+  float s = 1.f;
+  if (scaling) {
+    mx = block_max(mx, red);
+    s = pow2_scale_for(mx);
+  }
+  if (threadIdx.x == 0) inv_s2[j] = 1.f / s;
+  if (R12h) {
+    __half* o = R12h + (long long)j * ldh2;
+    for (int i = threadIdx.x; i < h; i += kCastThreads) o[i] = __float2half_rn(t[i] * s);
+  }
+}
+
+cudaError_t r12_finalize(int h, int w2, const float* T, long long ldt, float* Rblk, long long ldr,
+                         __half* R12h, long long ldh2, float* inv_s2, int scaling,
+                         cudaStream_t st) {
+  if (h <= 0 || w2 <= 0) return cudaSuccess;
+  r12_finalize_kernel<<<w2, kCastThreads, 0, st>>>(h, T, ldt, Rblk, ldr, R12h, ldh2, inv_s2,
+                                                    scaling);
+  return cudaGetLastError();
+}
+
+__global__ void copy_validate_kernel(int m, const float* __restrict__ A, long long lda,
+                                     float* __restrict__ Q, long long ldq, int* status) {
+  const int j = blockIdx.y;
+  const float* a = A + (long long)j * lda;
+  float* q = Q + (long long)j * ldq;
+  bool bad = false;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const float v = a[i];
+    bad |= !isfinite(v);
+    if (q != a) q[i] = v;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMin(status, j + 1);
+}
+
+cudaError_t copy_validate(int m, int n, const float* A, long long lda, float* Q, long long ldq,
+                          int* status, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  int gx = (m + 1023) / 1024;
+  if (gx > 64) gx = 64;
+  dim3 grid(gx, n);
+  copy_validate_kernel<<<grid, 256, 0, st>>>(m, A, lda, Q, ldq, status);
+  return cudaGetLastError();
+}
+
+__global__ void copy_block_kernel(int h, int w, const float* __restrict__ S, long long lds,
+                                  float* __restrict__ D, long long ldd) {
+  const long long total = (long long)h * w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % h), j = (int)(e / h);
+    D[i + j * ldd] = S[i + j * lds];
+  }
+}
+
+cudaError_t copy_block(int h, int w, const float* S, long long lds, float* D, long long ldd,
+                       cudaStream_t st) {
+  if (h <= 0 || w <= 0) return cudaSuccess;
+  long long total = (long long)h * w;
+  int grid = (int)((total + 255) / 256);
+  if (grid > 1184) grid = 1184;
+  copy_block_kernel<<<grid, 256, 0, st>>>(h, w, S, lds, D, ldd);
+  return cudaGetLastError();
+}
+
+__global__ void zero_lower_kernel(int n, float* R, long long ldr) {
+  const int j = blockIdx.x;
+  for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) R[i + (long long)j * ldr] = 0.f;
+}
+
+cudaError_t zero_lower(int n, float* R, long long ldr, cudaStream_t st) {
+  if (n <= 1) return cudaSuccess;
+  zero_lower_kernel<<<n, 256, 0, st>>>(n, R, ldr);
+  return cudaGetLastError();
+}
+
+}  // namespace tcqr

@@ -1,0 +1,528 @@
+// k_cgls.cu -- K5/K6/K7: the R-preconditioned CGLS of Alg. 5, corrected per
+// DESIGN.md reading R-A10, all vector arithmetic in FP64 (reading R-A13), A read as FP32 data
+// (reading R-A14).
+//
+//   K5  q = A t and v = A' r: FP32 A streamed once per product, FP64 accumulation, deterministic
+//       (fixed-order partial sums; one warp per column for A').
+//   K6  inv(R)*p and inv(R')*v (Alg. 5 lines 12, 18): R is applied through its explicit inverse
+//       M = inv(R), computed once in FP64 (block recursion X12 = -X11 R12 X22) and stored FP64;
+//       per iteration t = M p and s = M' v are fully parallel triangular GEMVs (reading R-A13:
+//       R is a fixed preconditioner, any consistent application is valid; Alg. 5 itself writes
+//       inv(R)).
+//   K7  scalar recurrences, stop/restart bookkeeping and the best-iterate copy, on the device, so
+//       the host only polls a done flag.
+#include "common.cuh"
+#include "kernels.h"
+#include "cgls_state.h"
+
+namespace tcqr {
+
+// ------------------------------------------------------------------------------------------
+// Explicit inverse of an upper-triangular FP32 R, in FP64.
+// ------------------------------------------------------------------------------------------
+constexpr int kInvBlk = 32;
+
+// One CTA per diagonal block: M_dd = inv(R_dd) by column-wise back substitution in FP64.
+__global__ void __launch_bounds__(kInvBlk) trinv_diag_kernel(int n, const float* __restrict__ R,
+                                                             long long ldr, double* __restrict__ M,
+                                                             long long ldm) {
+  __shared__ double Rs[kInvBlk][kInvBlk + 1];
+  __shared__ double Xs[kInvBlk][kInvBlk + 1];
+  const int d0 = blockIdx.x * kInvBlk;
+  const int bs = min(kInvBlk, n - d0);
+  for (int e = threadIdx.x; e < kInvBlk * kInvBlk; e += blockDim.x) {
+    const int i = e % kInvBlk, j = e / kInvBlk;
+    Rs[i][j] = (i < bs && j < bs && i <= j) ? (double)R[(d0 + i) + (long long)(d0 + j) * ldr] : 0.0;
+  }
+  __syncthreads();
+  const int j = threadIdx.x;  // column of the inverse
+  if (j < bs) {
+    for (int i = kInvBlk - 1; i >= 0; --i) {
+      double acc = (i == j) ? 1.0 : 0.0;
+      if (i <= j) {
+        for (int k = i + 1; k <= j; ++k) acc -= Rs[i][k] * Xs[k][j];
+        Xs[i][j] = acc / Rs[i][i];
+      } else {
+        Xs[i][j] = 0.0;
+      }
+    }
+    for (int i = 0; i <= j; ++i) M[(d0 + i) + (long long)(d0 + j) * ldm] = Xs[i][j];
+  }
+}
+
+// Batched FP64 GEMM for the inverse recursion: for pair p (rows i0 = p*2b):
+//   mode 0: W_p (b1 x b2) = R[i0:i0+b1, i0+b1:i0+b1+b2] * M[i0+b1:.., i0+b1:..]   (R12 * X22)
+//   mode 1: M[i0:i0+b1, i0+b1:..] = -M[i0:i0+b1, i0:i0+b1] * W_p                    (-X11 * W)
+// 64x64 output tile per CTA, 256 threads x (4x4), K-chunks of 16.
+__global__ void __launch_bounds__(256) trinv_pair_gemm_kernel(int n, int b, int mode,
+                                                              const float* __restrict__ R,
+                                                              long long ldr, double* __restrict__ M,
+                                                              long long ldm,
+                                                              double* __restrict__ W) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int p = blockIdx.z;
+  const int i0 = p * 2 * b;
+  const int b1 = b;
+  const int b2 = min(b, n - (i0 + b));
+  if (b2 <= 0) return;
+  const int tm = blockIdx.x * 64, tn = blockIdx.y * 64;
+  if (tm >= b1 || tn >= b2) return;
+  const int K = (mode == 0) ? b2 : b1;
+  double* Wp = W + (long long)p * b * b;  // ld = b
+  const int tid = threadIdx.x, ti = tid & 15, tj = tid >> 4;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    __syncthreads();
+    for (int e = tid; e < 16 * 64; e += 256) {
+      const int kk = e / 64, mm = e % 64;  // A element (row tm+mm, k k0+kk)
+      const int r = tm + mm, k = k0 + kk;
+      double av = 0.0;
+      if (r < b1 && k < K) {
+        if (mode == 0)
+          av = (double)R[(i0 + r) + (long long)(i0 + b1 + k) * ldr];
+        else
+          av = M[(i0 + r) + (long long)(i0 + k) * ldm];
+      }
+      As[kk][mm] = av;
+      const int c = tn + mm;  // B element (k k0+kk, col tn+mm)
+      double bv = 0.0;
+      if (c < b2 && k < K) {
+        if (mode == 0)
+          bv = M[(i0 + b1 + k) + (long long)(i0 + b1 + c) * ldm];
+        else
+          bv = Wp[k + (long long)c * b];
+      }
+      Bs[kk][mm] = bv;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], bb[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a[x] = As[kk][ti * 4 + x];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bb[y] = Bs[kk][tj * 4 + y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], bb[y], acc[x][y]);
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int r = tm + ti * 4 + x, c = tn + tj * 4 + y;
+      if (r < b1 && c < b2) {
+        if (mode == 0)
+          Wp[r + (long long)c * b] = acc[x][y];
+        else
+          M[(i0 + r) + (long long)(i0 + b1 + c) * ldm] = -acc[x][y];
+      }
+    }
+}
+
+cudaError_t trinv_f64(int n, const float* R, long long ldr, double* M, long long ldm, double* W,
+                      int num_sms, cudaStream_t st) {
+  (void)num_sms;
+  cudaError_t e = cudaMemsetAsync(M, 0, sizeof(double) * (size_t)ldm * n, st);
+  if (e != cudaSuccess) return e;
+  const int nblk = (n + kInvBlk - 1) / kInvBlk;
+  trinv_diag_kernel<<<nblk, kInvBlk, 0, st>>>(n, R, ldr, M, ldm);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  for (int b = kInvBlk; b < n; b *= 2) {
+    const int pairs = (n + 2 * b - 1) / (2 * b);
+    dim3 grid((b + 63) / 64, (b + 63) / 64, pairs);
+    trinv_pair_gemm_kernel<<<grid, 256, 0, st>>>(n, b, 0, R, ldr, M, ldm, W);
+    trinv_pair_gemm_kernel<<<grid, 256, 0, st>>>(n, b, 1, R, ldr, M, ldm, W);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------------------------------
+// Dense FP32 GEMVs with FP64 accumulation (K5)
+// ------------------------------------------------------------------------------------------
+constexpr int kGvRows = 256;  // rows per CTA (one per thread)
+constexpr int kGvCols = 128;  // columns per CTA chunk
+
+// part[cb][i] = sum_{j in chunk cb} A[i, j] v[j]    (grid: row blocks x column chunks)
+__global__ void __launch_bounds__(kGvRows) gemv_n_part_kernel(int m, int n,
+                                                              const float* __restrict__ A,
+                                                              long long lda,
+                                                              const double* __restrict__ v,
+                                                              double* __restrict__ part,
+                                                              const int* __restrict__ done) {
+  if (done && *done) return;
+  __shared__ double vs[kGvCols];
+  const int cb = blockIdx.y;
+  const int j0 = cb * kGvCols;
+  const int nc = min(kGvCols, n - j0);
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) vs[j] = v[j0 + j];
+  __syncthreads();
+  const long long i = (long long)blockIdx.x * kGvRows + threadIdx.x;
+  if (i >= m) return;
+  const float* a = A + i + (long long)j0 * lda;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  int j = 0;
+  for (; j + 4 <= nc; j += 4) {
+    const float a0 = a[(long long)(j + 0) * lda], a1 = a[(long long)(j + 1) * lda];
+    const float a2 = a[(long long)(j + 2) * lda], a3 = a[(long long)(j + 3) * lda];
+    acc0 = fma((double)a0, vs[j + 0], acc0);
+    acc1 = fma((double)a1, vs[j + 1], acc1);
+    acc2 = fma((double)a2, vs[j + 2], acc2);
+    acc3 = fma((double)a3, vs[j + 3], acc3);
+  }
+  for (; j < nc; ++j) acc0 = fma((double)a[(long long)j * lda], vs[j], acc0);
+  part[(long long)cb * m + i] = (acc0 + acc1) + (acc2 + acc3);
+}
+
+// y[i] = sum_cb part[cb][i] (fixed order); optional: dpart[block] = sum of y^2 over the block,
+// and y2[i] = base[i] - y[i] (residual form).
+__global__ void __launch_bounds__(256) gemv_n_reduce_kernel(int m, int nchunks,
+                                                            const double* __restrict__ part,
+                                                            double* __restrict__ y,
+                                                            double* __restrict__ dpart,
+                                                            const int* __restrict__ done) {
+  if (done && *done) return;
+  __shared__ double red[8];
+  const long long i = (long long)blockIdx.x * 256 + threadIdx.x;
+  double acc = 0.0;
+  if (i < m) {
+    for (int c = 0; c < nchunks; ++c) acc += part[(long long)c * m + i];
+    y[i] = acc;
+  }
+  if (dpart) {
+    double sq = warp_sum_d(acc * acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += red[w];
+      dpart[blockIdx.x] = t;
+    }
+  }
+}
+
+// y[j] = sum_i A[i, j] v[i]: one warp per column, float4 loads, FP64 accumulate, butterfly sum.
+__global__ void __launch_bounds__(256) gemv_t_kernel(int m, int n, const float* __restrict__ A,
+                                                     long long lda, const double* __restrict__ v,
+                                                     double* __restrict__ y,
+                                                     const int* __restrict__ done) {
+  if (done && *done) return;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const float* a = A + (long long)j * lda;
+  double acc0 = 0.0, acc1 = 0.0;
+  const bool vec = ((lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  int i = 0;
+  if (vec) {
+    const int m4 = m & ~127;
+    for (i = lane * 4; i < m4; i += 128) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(a + i));
+      const double2 v0 = *reinterpret_cast<const double2*>(v + i);
+      const double2 v1 = *reinterpret_cast<const double2*>(v + i + 2);
+      acc0 = fma((double)x.x, v0.x, acc0);
+      acc1 = fma((double)x.y, v0.y, acc1);
+      acc0 = fma((double)x.z, v1.x, acc0);
+      acc1 = fma((double)x.w, v1.y, acc1);
+    }
+    i = m4;
+  }
+  for (int ii = i + lane; ii < m; ii += 32) acc0 = fma((double)a[ii], v[ii], acc0);
+  const double s = warp_sum_d(acc0 + acc1);
+  if (lane == 0) y[j] = s;
+}
+
+cudaError_t gemv_f32_n(int m, int n, const float* A, long long lda, const double* v, double* y,
+                       double* part, long long part_cap, cudaStream_t st) {
+  const int nch = (n + kGvCols - 1) / kGvCols;
+  if ((long long)nch * m > part_cap) return cudaErrorInvalidValue;
+  dim3 g1((m + kGvRows - 1) / kGvRows, nch);
+  gemv_n_part_kernel<<<g1, kGvRows, 0, st>>>(m, n, A, lda, v, part, nullptr);
+  gemv_n_reduce_kernel<<<(m + 255) / 256, 256, 0, st>>>(m, nch, part, y, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t gemv_f32_t(int m, int n, const float* A, long long lda, const double* v, double* y,
+                       cudaStream_t st) {
+  gemv_t_kernel<<<(n + 7) / 8, 256, 0, st>>>(m, n, A, lda, v, y, nullptr);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Triangular (upper) FP64 GEMVs with the explicit inverse M (K6)
+// ------------------------------------------------------------------------------------------
+constexpr int kTriBlk = 256;
+
+// part[cb][i] = sum_{j in chunk cb, j >= i} M[i, j] p[j], only for chunks cb >= row block.
+__global__ void __launch_bounds__(kTriBlk) tri_n_part_kernel(int n, const double* __restrict__ M,
+                                                             long long ldm,
+                                                             const double* __restrict__ p,
+                                                             double* __restrict__ part,
+                                                             const int* __restrict__ done) {
+  if (done && *done) return;
+  const int rb = blockIdx.x, cb = blockIdx.y;
+  if (cb < rb) return;
+  __shared__ double ps[kTriBlk];
+  const int j0 = cb * kTriBlk;
+  const int nc = min(kTriBlk, n - j0);
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) ps[j] = p[j0 + j];
+  __syncthreads();
+  const int i = rb * kTriBlk + threadIdx.x;
+  if (i >= n) return;
+  const double* mm = M + i + (long long)j0 * ldm;
+  double a0 = 0.0, a1 = 0.0;
+  int j = 0;
+  for (; j + 2 <= nc; j += 2) {
+    a0 = fma(mm[(long long)j * ldm], ps[j], a0);
+    a1 = fma(mm[(long long)(j + 1) * ldm], ps[j + 1], a1);
+  }
+  if (j < nc) a0 = fma(mm[(long long)j * ldm], ps[j], a0);
+  part[(long long)cb * n + i] = a0 + a1;
+}
+
+__global__ void tri_n_reduce_kernel(int n, int nch, const double* __restrict__ part,
+                                    double* __restrict__ t, const int* __restrict__ done) {
+  if (done && *done) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int c = i / kTriBlk; c < nch; ++c) acc += part[(long long)c * n + i];
+  t[i] = acc;
+}
+
+// s[j] = sum_{i <= j} M[i, j] v[i]: one warp per column.
+__global__ void __launch_bounds__(256) tri_t_kernel(int n, const double* __restrict__ M,
+                                                    long long ldm, const double* __restrict__ v,
+                                                    double* __restrict__ s,
+                                                    const int* __restrict__ done) {
+  if (done && *done) return;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const double* mm = M + (long long)j * ldm;
+  double a0 = 0.0, a1 = 0.0;
+  int i = lane;
+  for (; i + 32 <= j; i += 64) {
+    a0 = fma(mm[i], v[i], a0);
+    a1 = fma(mm[i + 32], v[i + 32], a1);
+  }
+  for (; i <= j; i += 32) a0 = fma(mm[i], v[i], a0);
+  const double r = warp_sum_d(a0 + a1);
+  if (lane == 0) s[j] = r;
+}
+
+// ------------------------------------------------------------------------------------------
+// CGLS scalar / vector kernels (K7)
+// ------------------------------------------------------------------------------------------
+// Deterministic single-CTA sum of parts -> *out (FP64).
+__global__ void __launch_bounds__(1024) sum_parts_kernel(int np, const double* __restrict__ parts,
+                                                         double* __restrict__ out,
+                                                         const int* __restrict__ done) {
+  if (done && *done) return;
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += parts[i];
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
+}
+
+// alpha = gamma / delta; x += alpha t (n); r -= alpha q (m).   (Alg. 5 lines 15-17, R-A10)
+__global__ void cg_update_xr_kernel(int m, int n, CgState* __restrict__ st,
+                                    double* __restrict__ x, const double* __restrict__ t,
+                                    double* __restrict__ r, const double* __restrict__ q) {
+  if (st->done) return;
+  const double alpha = st->gamma / st->delta;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = fma(alpha, t[i], x[i]);
+  if (i < m) r[i] = fma(-alpha, q[i], r[i]);
+}
+
+// Pass set-up after s = R^-T A' r has been formed: gamma, s0, p = s, x = 0, best tracking.
+__global__ void __launch_bounds__(1024) cg_init_kernel(int n, CgState* __restrict__ st,
+                                                       const double* __restrict__ s,
+                                                       double* __restrict__ p,
+                                                       double* __restrict__ x,
+                                                       double* __restrict__ xbest) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = fma(s[i], s[i], acc);
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g = 0.0;
+    for (int w = 0; w < 32; ++w) g += red[w];
+    st->gamma = g;
+    st->s0 = sqrt(g);
+    if (st->sref <= 0.0) st->sref = st->s0;
+    st->best = st->s0;
+    st->since = 0;
+    st->k = 0;
+    st->reason = -1;
+    st->done = (g == 0.0) ? 1 : 0;
+    if (g == 0.0) st->reason = 3;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    p[i] = s[i];
+    x[i] = 0.0;
+    xbest[i] = 0.0;
+  }
+}
+
+// After s = R^-T A' r: gamma' = ||s||^2, history, best iterate, stop tests (R-A11), beta, p.
+__global__ void __launch_bounds__(1024) cg_finish_kernel(int n, CgState* __restrict__ st,
+                                                         const double* __restrict__ s,
+                                                         double* __restrict__ p,
+                                                         double* __restrict__ x,
+                                                         double* __restrict__ xbest,
+                                                         double* __restrict__ hist) {
+  if (st->done) return;
+  __shared__ double red[32];
+  __shared__ int action;  // 0 continue, 1 stop keep x, 2 stop use xbest
+  __shared__ int newbest;
+  __shared__ double beta_sh;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = fma(s[i], s[i], acc);
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g = 0.0;
+    for (int w = 0; w < 32; ++w) g += red[w];
+    const double ns = sqrt(g);
+    const int k = ++st->k;
+    if (hist && k <= st->hist_cap) hist[k - 1] = ns / st->s0;
+    newbest = 0;
+    if (ns < st->best) {
+      st->best = ns;
+      st->since = 0;
+      newbest = 1;
+    } else {
+      st->since += 1;
+    }
+    action = 0;
+    if (ns / st->s0 <= st->tol) {
+      action = 1;
+      st->reason = 0;
+    } else if (st->best < st->floor * st->sref && st->since >= st->window) {
+      action = 2;
+      st->reason = 1;
+    } else if (k >= st->maxit) {
+      action = 2;
+      st->reason = 2;
+    }
+    if (action) st->done = 1;
+    const double beta = g / st->gamma;
+    beta_sh = beta;
+    if (!action) st->gamma = g;
+  }
+  __syncthreads();
+  if (newbest || action == 2) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (newbest) xbest[i] = x[i];
+      else x[i] = xbest[i];  // action == 2 and this iterate is not the best
+    }
+  }
+  if (action == 0) {
+    const double beta = beta_sh;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = fma(beta, p[i], s[i]);
+  }
+}
+
+// r = b - q (restart residual); used with q = A x.
+__global__ void residual_kernel(int m, const double* __restrict__ b, const double* __restrict__ q,
+                                double* __restrict__ r) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) r[i] = b[i] - q[i];
+}
+
+__global__ void axpy_kernel(int n, double a, const double* __restrict__ xx,
+                            double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = fma(a, xx[i], y[i]);
+}
+
+// ------------------------------------------------------------------------------------------
+// Host launchers used by the driver (tcqr.cu)
+// ------------------------------------------------------------------------------------------
+int cg_gemv_n_chunks(int n) { return (n + kGvCols - 1) / kGvCols; }
+int cg_tri_chunks(int n) { return (n + kTriBlk - 1) / kTriBlk; }
+
+cudaError_t cg_launch_tri_n(int n, const double* M, long long ldm, const double* p, double* t,
+                            double* part, const int* done, cudaStream_t st) {
+  const int nch = cg_tri_chunks(n);
+  dim3 g(nch, nch);
+  tri_n_part_kernel<<<g, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
+  tri_n_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, nch, part, t, done);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_tri_t(int n, const double* M, long long ldm, const double* v, double* s,
+                            const int* done, cudaStream_t st) {
+  tri_t_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, M, ldm, v, s, done);
+  return cudaGetLastError();
+}
+
+// q = A t with delta partials (dpart sized (m+255)/256).
+cudaError_t cg_launch_a_n(int m, int n, const float* A, long long lda, const double* t, double* q,
+                          double* part, double* dpart, const int* done, cudaStream_t st) {
+  const int nch = (n + kGvCols - 1) / kGvCols;
+  dim3 g1((m + kGvRows - 1) / kGvRows, nch);
+  gemv_n_part_kernel<<<g1, kGvRows, 0, st>>>(m, n, A, lda, t, part, done);
+  gemv_n_reduce_kernel<<<(m + 255) / 256, 256, 0, st>>>(m, nch, part, q, dpart, done);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_a_t(int m, int n, const float* A, long long lda, const double* r, double* v,
+                          const int* done, cudaStream_t st) {
+  gemv_t_kernel<<<(n + 7) / 8, 256, 0, st>>>(m, n, A, lda, r, v, done);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_sum_parts(int np, const double* parts, double* out, const int* done,
+                                cudaStream_t st) {
+  sum_parts_kernel<<<1, 1024, 0, st>>>(np, parts, out, done);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_update_xr(int m, int n, CgState* s, double* x, const double* t, double* r,
+                                const double* q, cudaStream_t st) {
+  const int mx = m > n ? m : n;
+  cg_update_xr_kernel<<<(mx + 255) / 256, 256, 0, st>>>(m, n, s, x, t, r, q);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_init(int n, CgState* s, const double* sv, double* p, double* x,
+                           double* xbest, cudaStream_t st) {
+  cg_init_kernel<<<1, 1024, 0, st>>>(n, s, sv, p, x, xbest);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_finish(int n, CgState* s, const double* sv, double* p, double* x,
+                             double* xbest, double* hist, cudaStream_t st) {
+  cg_finish_kernel<<<1, 1024, 0, st>>>(n, s, sv, p, x, xbest, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_residual(int m, const double* b, const double* q, double* r,
+                               cudaStream_t st) {
+  residual_kernel<<<(m + 255) / 256, 256, 0, st>>>(m, b, q, r);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_axpy(int n, double a, const double* x, double* y, cudaStream_t st) {
+  axpy_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, a, x, y);
+  return cudaGetLastError();
+}
+
+}  // namespace tcqr

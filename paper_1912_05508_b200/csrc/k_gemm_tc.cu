@@ -1,0 +1,318 @@
+// k_gemm_tc.cu -- K3 / K4: FP16-input, FP32-accumulate tcgen05 GEMMs of Alg. 2 lines 8-9.
+//
+//   K3 (MODE_TN):  R12 = Q1' * A2          (Alg. 2 line 8)
+//       D (h x w2) = A' B, A = fl16(Q1) (m x h), B = fl16(A2 diag(s)) (m x w2): both operands are
+//       K-major (the contraction index m is contiguous in the column-major buffers).  Split-K over
+//       m is deterministic: each split writes its own FP32 partial, reduced in a fixed order.
+//   K4 (MODE_NN):  A2 <- A2 - Q1 * R12     (Alg. 2 line 9 argument)
+//       D (m x w2) = A B, A = fl16(Q1) is MN-major (m contiguous), B = fl16(R12 diag(s')) is
+//       K-major; the epilogue reads the FP32 A2 tile and writes A2 - D diag(1/s').
+//
+// Design (sm_100a): persistent warp-specialized CTA, 192 threads:
+//   warp 0      TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, mbarrier complete_tx)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (128 x BN x 16 per instruction)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> coalesced column-major stores
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap the MMAs of tile i+1.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tcqr {
+
+template <int BN, int MODE>
+struct TcCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int ST = (BN == 128) ? 6 : 4;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = ST * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(192, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int M, int N, int K, int splits, float* __restrict__ C, long long ldc,
+                   long long split_stride, const float* __restrict__ col_mult) {
+  using Cfg = TcCfg<BN, MODE>;
+  constexpr int BM = Cfg::BM, BK = Cfg::BK, ST = Cfg::ST, STAGE = Cfg::STAGE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * STAGE);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int nkb = (K + BK - 1) / BK;
+  const int total = tiles_m * tiles_n * splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n, s = w / (tiles_m * tiles_n);
+        const int kb0 = (int)((long long)s * nkb / splits), kb1 = (int)((long long)(s + 1) * nkb / splits);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE);
+          uint8_t* sa = smem + stage * STAGE;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          if (MODE == kModeTN) {
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, mb * BM);
+          } else {
+            tma_load_2d(sa, &tmA, &full[stage], mb * BM, kb * BK);
+            tma_load_2d(sa + 8192, &tmA, &full[stage], mb * BM + 64, kb * BK);
+          }
+          tma_load_2d(sb, &tmB, &full[stage], kb * BK, nb * BN);
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = make_idesc_f16(128, BN, MODE == kModeNN ? 1 : 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+        const int s = w / (tiles_m * tiles_n);
+        const int kb0 = (int)((long long)s * nkb / splits), kb1 = (int)((long long)(s + 1) * nkb / splits);
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tacc = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t base_a = smem_u32(smem + stage * STAGE);
+          const uint32_t base_b = base_a + Cfg::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            uint64_t da;
+            if (MODE == kModeTN)
+              da = make_sw128_desc(base_a + kk * 32, 16, 1024);
+            else
+              da = make_sw128_desc(base_a + kk * 2048, 8192, 1024);
+            const uint64_t db = make_sw128_desc(base_b + kk * 32, 16, 1024);
+            mma_f16_ss(tacc, da, db, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5 ----------------
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int it = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+      const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n, s = w / (tiles_m * tiles_n);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * BM + q * 32 + lane;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c, r);
+        tmem_ld_wait();
+        const int col0 = nb * BN + c;
+        if (row < M) {
+          if (MODE == kModeTN) {
+            float* out = C + (splits > 1 ? (long long)s * split_stride : 0LL) + row;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = col0 + j;
+              if (col < N) {
+                float v = __uint_as_float(r[j]);
+                if (splits == 1 && col_mult) v *= __ldg(col_mult + col);
+                out[(long long)col * ldc] = v;
+              }
+            }
+          } else {
+            float* out = C + row;
+            float cv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              cv[j] = (col0 + j < N) ? out[(long long)(col0 + j) * ldc] : 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = col0 + j;
+              if (col < N) {
+                const float mlt = col_mult ? __ldg(col_mult + col) : 1.f;
+                out[(long long)col * ldc] = cv[j] - __uint_as_float(r[j]) * mlt;
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  }
+}
+
+// Deterministic split-K reduction: C[i + j*ldc] = (sum_s P[s][i + j*ldp]) * col_mult[j].
+__global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, long long pstride,
+                                     int ldp, int M, int N, float* __restrict__ C, long long ldc,
+                                     const float* __restrict__ col_mult) {
+  const long long total = (long long)M * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % M), j = (int)(e / M);
+    const float* p = P + i + (long long)j * ldp;
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += p[(long long)s * pstride];
+    if (col_mult) acc *= col_mult[j];
+    C[i + (long long)j * ldc] = acc;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Host side
+// ------------------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2-D FP16 map: inner (contiguous) extent, outer extent, leading dimension (elements).
+static bool make_map_f16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                         uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int MODE>
+static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
+                             int splits, float* C, long long ldc, long long sstride,
+                             const float* mult, int num_sms, cudaStream_t st) {
+  using Cfg = TcCfg<BN, MODE>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = ((M + 127) / 128) * ((N + BN - 1) / BN) * splits;
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  tc_gemm_kernel<BN, MODE><<<grid, 192, Cfg::SMEM, st>>>(a, b, M, N, K, splits, C, ldc, sstride,
+                                                         mult);
+  return cudaGetLastError();
+}
+
+// D (h x w2) = A1h' A2h ; writes C (ldc) directly (splits == 1, scaled by col_mult) or the
+// partials P (splits > 1; P has room for splits * ldp * w2 floats) followed by the reduction.
+cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, const __half* A2h,
+                       long long lda2, float* C, long long ldc, const float* col_mult, float* P,
+                       long long p_cap, int num_sms, cudaStream_t st) {
+  if (m <= 0 || h <= 0 || w2 <= 0) return cudaSuccess;
+  CUtensorMap ma, mb;
+  const int BN = (w2 > 128) ? 256 : 128;
+  if (!make_map_f16(&ma, A1h, m, h, lda1, 64, 128)) return cudaErrorInvalidValue;
+  if (!make_map_f16(&mb, A2h, m, w2, lda2, 64, BN)) return cudaErrorInvalidValue;
+  const int tiles = ((h + 127) / 128) * ((w2 + BN - 1) / BN);
+  const int nkb = (m + 63) / 64;
+  int splits = 1;
+  if (tiles < num_sms) {
+    splits = num_sms / tiles;
+    if (splits > nkb) splits = nkb;
+    const long long per = (long long)h * w2;
+    if (P == nullptr || per * splits > p_cap) splits = P ? (int)(p_cap / per) : 1;
+    if (splits < 1) splits = 1;
+  }
+  cudaError_t e;
+  if (splits == 1) {
+    e = (BN == 256) ? launch_tc<256, kModeTN>(ma, mb, h, w2, m, 1, C, ldc, 0, col_mult, num_sms, st)
+                    : launch_tc<128, kModeTN>(ma, mb, h, w2, m, 1, C, ldc, 0, col_mult, num_sms, st);
+    return e;
+  }
+  const long long sstride = (long long)h * w2;
+  e = (BN == 256) ? launch_tc<256, kModeTN>(ma, mb, h, w2, m, splits, P, h, sstride, nullptr,
+                                            num_sms, st)
+                  : launch_tc<128, kModeTN>(ma, mb, h, w2, m, splits, P, h, sstride, nullptr,
+                                            num_sms, st);
+  if (e != cudaSuccess) return e;
+  const long long total = (long long)h * w2;
+  int grid = (int)((total + 255) / 256);
+  if (grid > 4 * num_sms) grid = 4 * num_sms;
+  splitk_reduce_kernel<<<grid, 256, 0, st>>>(P, splits, sstride, h, h, w2, C, ldc, col_mult);
+  return cudaGetLastError();
+}
+
+// C (m x w2) -= (Qh Bh) diag(col_mult);  Qh m x h (ldq), Bh h x w2 (ldb).
+cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long ldq,
+                              const __half* Bh, long long ldb, float* C, long long ldc,
+                              const float* col_mult, int num_sms, cudaStream_t st) {
+  if (m <= 0 || h <= 0 || w2 <= 0) return cudaSuccess;
+  CUtensorMap ma, mb;
+  const int BN = (w2 > 128) ? 256 : 128;
+  if (!make_map_f16(&ma, Qh, m, h, ldq, 64, 64)) return cudaErrorInvalidValue;
+  if (!make_map_f16(&mb, Bh, h, w2, ldb, 64, BN)) return cudaErrorInvalidValue;
+  return (BN == 256)
+             ? launch_tc<256, kModeNN>(ma, mb, m, w2, h, 1, C, ldc, 0, col_mult, num_sms, st)
+             : launch_tc<128, kModeNN>(ma, mb, m, w2, h, 1, C, ldc, 0, col_mult, num_sms, st);
+}
+
+}  // namespace tcqr

@@ -1,0 +1,65 @@
+// kernels.h -- internal host-side launch wrappers of the hot-path kernels (not part of the ABI).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tcqr {
+
+constexpr int kModeTN = 0;
+constexpr int kModeNN = 1;
+
+// ---- K3 / K4 (k_gemm_tc.cu) ----
+cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, const __half* A2h,
+                       long long lda2, float* C, long long ldc, const float* col_mult, float* P,
+                       long long p_cap, int num_sms, cudaStream_t st);
+cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long ldq,
+                              const __half* Bh, long long ldb, float* C, long long ldc,
+                              const float* col_mult, int num_sms, cudaStream_t st);
+
+// ---- K1 and friends (k_cast.cu) ----
+// Xh = fl16(X diag(s)); inv_s[j] = 1/s_j; status: atomicMin(1-based first non-finite column).
+cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
+                       float* inv_s, int scaling, int* status, int col_base, cudaStream_t st);
+// R12 finalize: T (h x w2, ldt) -> R block (ldr) and fl16(R12 diag(s')) (ldh2), inv_s2.
+cudaError_t r12_finalize(int h, int w2, const float* T, long long ldt, float* Rblk, long long ldr,
+                         __half* R12h, long long ldh2, float* inv_s2, int scaling, cudaStream_t st);
+// Copy A -> Q (ld m) and flag the first non-finite column in status.
+cudaError_t copy_validate(int m, int n, const float* A, long long lda, float* Q, long long ldq,
+                          int* status, cudaStream_t st);
+// Copy an h x w block (ld src / dst).
+cudaError_t copy_block(int h, int w, const float* S, long long lds, float* D, long long ldd,
+                       cudaStream_t st);
+// Zero the strictly lower triangle of an n x n matrix (ld).
+cudaError_t zero_lower(int n, float* R, long long ldr, cudaStream_t st);
+
+// ---- K2 panel (k_panel.cu) ----
+// One CAQR level: MGS on each br-row block of X (rows x w), local Q in place, R_b -> stack rows
+// [b*w, (b+1)*w) of S (lds), or (nb == 1) -> Rout (ldr).  top: zero norms are errors.
+cudaError_t panel_mgs_level(int rows, int w, float* X, long long ldx, int br, int nb, float* S,
+                            long long lds, float* Rout, long long ldr, int top, int* status,
+                            int col0, cudaStream_t st);
+// Step 4 of Eq. (6): X_b <- X_b * S[b*w:(b+1)*w, :].
+cudaError_t panel_apply(int rows, int w, float* X, long long ldx, int br, int nb, const float* S,
+                        long long lds, cudaStream_t st);
+int panel_num_blocks(int rows, int br, int w);
+
+// ---- K2b FP32 intra-leaf products (k_f32.cu) ----
+// T (h x w2, ld h) = Q1' A2 over m rows (deterministic split-K with partials in P).
+cudaError_t f32_tn(int m, int h, int w2, const float* Q1, long long ldq, const float* A2,
+                   long long lda, float* T, float* P, long long p_cap, int num_sms,
+                   cudaStream_t st);
+// A2 (m x w2) -= Q1 (m x h) T (h x w2, ld h).
+cudaError_t f32_nn_update(int m, int h, int w2, const float* Q1, long long ldq, const float* T,
+                          float* A2, long long lda, cudaStream_t st);
+
+// ---- CGLS (k_cgls.cu) ----
+struct CglsDev;  // device state, see k_cgls.cu
+cudaError_t trinv_f64(int n, const float* R, long long ldr, double* M, long long ldm, double* work,
+                      int num_sms, cudaStream_t st);
+cudaError_t gemv_f32_n(int m, int n, const float* A, long long lda, const double* v, double* y,
+                       double* part, long long part_cap, cudaStream_t st);
+cudaError_t gemv_f32_t(int m, int n, const float* A, long long lda, const double* v, double* y,
+                       cudaStream_t st);
+
+}  // namespace tcqr

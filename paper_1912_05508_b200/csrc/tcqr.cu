@@ -1,0 +1,870 @@
+// tcqr.cu -- the C ABI (include/tcqr.h): context, workspace, the Alg. 2 recursion driver, the
+// Eq. (6) panel tree (with TSQR across ranks), the Alg. 5 CGLS driver, CUDA-graph replay and the
+// NCCL communicator (loaded at run time only when nranks > 1).
+#include <dlfcn.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/tcqr.h"
+#include "cgls_state.h"
+#include "common.cuh"
+#include "kernels.h"
+
+// ---- minimal NCCL ABI (types from nccl.h; symbols resolved with dlsym) ----
+#include <nccl.h>
+
+namespace tcqr {
+
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  bool load() {
+    if (lib) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (lib) break;
+    }
+    if (!lib) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(lib, "ncclCommInitRank");
+    CommDestroy = (decltype(CommDestroy))dlsym(lib, "ncclCommDestroy");
+    AllReduce = (decltype(AllReduce))dlsym(lib, "ncclAllReduce");
+    AllGather = (decltype(AllGather))dlsym(lib, "ncclAllGather");
+    return GetUniqueId && CommInitRank && CommDestroy && AllReduce && AllGather;
+  }
+};
+static NcclApi g_nccl;
+
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+};
+
+struct Context {
+  bool inited = false;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  tcqr_config_t cfg;
+  // workspace
+  void* user_ws = nullptr;
+  size_t user_ws_bytes = 0;
+  void* own_ws = nullptr;
+  size_t own_ws_bytes = 0;
+  int* d_status = nullptr;  // [0] factor status, [1] scratch
+  int* h_status = nullptr;  // pinned
+  std::map<std::string, GraphEntry> graphs;
+};
+static Context g_ctx;
+static std::mutex g_mu;
+
+static int split_point(int w) { return 32 * ((w + 63) / 64); }
+static long long round_up(long long x, long long a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------------------------------------
+// Workspace layout
+// ------------------------------------------------------------------------------------------
+struct Arena {
+  char* base = nullptr;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = round_up(off, 256);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += sizeof(T) * count;
+    return p;
+  }
+};
+
+struct FactorWs {
+  __half* Qh = nullptr;  // fl16 shadow of the working matrix, ld ldh
+  long long ldh = 0;
+  float* inv_s = nullptr;   // n
+  float* inv_s2 = nullptr;  // n
+  float* T = nullptr;       // R12 staging (hmax * w2max)
+  __half* R12h = nullptr;   // ldh2 * w2max
+  float* P = nullptr;       // split-K partials
+  long long p_cap = 0;
+  float* stack = nullptr;  // CAQR stacks
+  long long stack_cap = 0;
+  float* gather = nullptr;  // TSQR allgather (nranks * 32 * 32)
+  float* rloc = nullptr;    // local panel R (32 * 32)
+};
+
+static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, FactorWs& w) {
+  w.ldh = round_up(std::max<long long>(m, 8), 8);
+  w.Qh = a.take<__half>((size_t)w.ldh * n);
+  w.inv_s = a.take<float>(n + 8);
+  w.inv_s2 = a.take<float>(n + 8);
+  const long long hmax = split_point((int)std::max<long long>(n, 64));
+  const long long w2max = std::max<long long>(n - split_point((int)n), 1);
+  w.T = a.take<float>((size_t)(hmax * std::max(w2max, hmax)) + 64);
+  w.R12h = a.take<__half>((size_t)round_up(hmax, 8) * std::max(w2max, hmax) + 64);
+  w.p_cap = std::max<long long>(8LL << 20, 64LL * 64 * 600);
+  w.P = a.take<float>((size_t)w.p_cap);
+  // stacks: sum over CAQR levels of nb*w*w <= 2 * ceil(m/64) * 32 * 32 (+ rank level)
+  w.stack_cap = 2 * ((m + 63) / 64 + 8 + nranks) * 32 * 32 + 4096;
+  w.stack = a.take<float>((size_t)w.stack_cap);
+  w.gather = a.take<float>((size_t)std::max(nranks, 1) * 32 * 32 + 64);
+  w.rloc = a.take<float>(32 * 32 + 64);
+}
+
+struct LlsWs {
+  float* Aw = nullptr;  // working copy of A (m x n, ld m)
+  float* R = nullptr;   // n x n
+  double* M = nullptr;  // inv(R), n x n
+  double* W = nullptr;  // trinv workspace
+  double *x, *xbest, *t, *s, *p, *v, *r, *q, *b2, *x1;
+  double* part = nullptr;
+  long long part_cap = 0;
+  double* dpart = nullptr;
+  double* hist = nullptr;
+  int hist_cap = 0;
+  CgState* st = nullptr;
+  FactorWs f;
+};
+
+static long long trinv_w_count(long long n) {
+  long long mx = 0;
+  for (long long b = 32; b < n; b *= 2) {
+    long long pairs = (n + 2 * b - 1) / (2 * b);
+    mx = std::max(mx, pairs * b * b);
+  }
+  return mx + 64;
+}
+
+static void plan_lls_ws(Arena& a, long long m, long long n, int nranks, int maxit, LlsWs& w) {
+  w.Aw = a.take<float>((size_t)m * n);
+  w.R = a.take<float>((size_t)n * n);
+  w.M = a.take<double>((size_t)n * n);
+  w.W = a.take<double>((size_t)trinv_w_count(n));
+  w.x = a.take<double>(n);
+  w.xbest = a.take<double>(n);
+  w.t = a.take<double>(n);
+  w.s = a.take<double>(n);
+  w.p = a.take<double>(n);
+  w.v = a.take<double>(n);
+  w.x1 = a.take<double>(n);
+  w.r = a.take<double>(m);
+  w.q = a.take<double>(m);
+  w.b2 = a.take<double>(m);
+  const long long nchA = cg_gemv_n_chunks((int)n) * m;
+  const long long nchT = (long long)cg_tri_chunks((int)n) * n;
+  w.part_cap = std::max(nchA, nchT);
+  w.part = a.take<double>((size_t)w.part_cap);
+  w.dpart = a.take<double>((size_t)((m + 255) / 256) + 8);
+  w.hist_cap = std::max(maxit, 1) * 2 + 8;
+  w.hist = a.take<double>((size_t)w.hist_cap);
+  w.st = a.take<CgState>(1);
+  plan_factor_ws(a, m, n, nranks, w.f);
+}
+
+static size_t ws_bytes(long long m, long long n, int op, int nranks, int maxit) {
+  Arena a;
+  if (op == 0) {
+    FactorWs f;
+    plan_factor_ws(a, m, n, nranks, f);
+  } else {
+    LlsWs l;
+    plan_lls_ws(a, m, n, nranks, maxit, l);
+  }
+  return a.off + 256;
+}
+
+static char* get_ws(size_t bytes) {
+  Context& c = g_ctx;
+  if (c.user_ws && c.user_ws_bytes >= bytes) return static_cast<char*>(c.user_ws);
+  if (c.own_ws_bytes < bytes) {
+    if (c.own_ws) {
+      cudaStreamSynchronize(c.stream);
+      cudaFree(c.own_ws);
+      c.own_ws = nullptr;
+      c.own_ws_bytes = 0;
+      for (auto& kv : c.graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      c.graphs.clear();
+    }
+    if (cudaMalloc(&c.own_ws, bytes) != cudaSuccess) {
+      c.own_ws = nullptr;
+      return nullptr;
+    }
+    c.own_ws_bytes = bytes;
+  }
+  return static_cast<char*>(c.own_ws);
+}
+
+// ------------------------------------------------------------------------------------------
+// Collectives (no-ops at nranks == 1)
+// ------------------------------------------------------------------------------------------
+static int allreduce_f32(float* buf, size_t count) {
+  Context& c = g_ctx;
+  if (c.nranks <= 1) return 0;
+  return g_nccl.AllReduce(buf, buf, count, ncclFloat32, ncclSum, c.comm, c.stream) == ncclSuccess
+             ? 0
+             : TCQR_ERR_NCCL;
+}
+static int allreduce_f64(double* buf, size_t count) {
+  Context& c = g_ctx;
+  if (c.nranks <= 1) return 0;
+  return g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, c.comm, c.stream) == ncclSuccess
+             ? 0
+             : TCQR_ERR_NCCL;
+}
+static int allreduce_max_i32(int* buf) {
+  Context& c = g_ctx;
+  if (c.nranks <= 1) return 0;
+  return g_nccl.AllReduce(buf, buf, 1, ncclInt32, ncclMin, c.comm, c.stream) == ncclSuccess
+             ? 0
+             : TCQR_ERR_NCCL;
+}
+
+#define CK(x)                                \
+  do {                                       \
+    cudaError_t _e = (x);                    \
+    if (_e != cudaSuccess) {                 \
+      fprintf(stderr, "tcqr: CUDA error %s at %s:%d\n", cudaGetErrorString(_e), __FILE__, \
+              __LINE__);                     \
+      return TCQR_ERR_CUDA;                  \
+    }                                        \
+  } while (0)
+#define CKR(x)              \
+  do {                      \
+    int _r = (x);           \
+    if (_r != 0) return _r; \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// Panel: Eq. (6) tree on X (rows x w, ldx); top-level R -> Rout (ldr).
+// stack_off: running offset into ws.stack (each tree level takes nb*w*w floats).
+// ------------------------------------------------------------------------------------------
+static int caqr_rec(FactorWs& ws, long long& stack_off, int rows, int w, float* X, long long ldx,
+                    float* Rout, long long ldr, bool top, int col0) {
+  Context& c = g_ctx;
+  const int br = c.cfg.panel_rows;
+  const int nb = panel_num_blocks(rows, br, w);
+  if (nb == 1) {
+    CK(panel_mgs_level(rows, w, X, ldx, br, 1, nullptr, 0, Rout, ldr, top ? 1 : 0, c.d_status,
+                       col0, c.stream));
+    return 0;
+  }
+  const long long need = (long long)nb * w * w;
+  if (stack_off + need > ws.stack_cap) return TCQR_ERR_OOM;
+  float* S = ws.stack + stack_off;
+  stack_off += need;
+  const long long lds = (long long)nb * w;
+  CK(panel_mgs_level(rows, w, X, ldx, br, nb, S, lds, nullptr, 0, 0, c.d_status, col0, c.stream));
+  CKR(caqr_rec(ws, stack_off, nb * w, w, S, lds, Rout, ldr, top, col0));
+  CK(panel_apply(rows, w, X, ldx, br, nb, S, lds, c.stream));
+  return 0;
+}
+
+static int panel(FactorWs& ws, int m, int w, float* X, long long ldx, float* Rout, long long ldr,
+                 int col0) {
+  Context& c = g_ctx;
+  long long off = 0;
+  if (c.nranks <= 1) return caqr_rec(ws, off, m, w, X, ldx, Rout, ldr, true, col0);
+  // TSQR (reading R-A26): local tree -> allgather of the P local R's -> redundant factorization of
+  // the stack on every rank -> this rank's slice applied to the local Q.
+  CKR(caqr_rec(ws, off, m, w, X, ldx, ws.rloc, w, false, col0));
+  if (g_nccl.AllGather(ws.rloc, ws.gather, (size_t)w * w, ncclFloat32, c.comm, c.stream) !=
+      ncclSuccess)
+    return TCQR_ERR_NCCL;
+  // gather holds P column-major w x w blocks; restack them as a (P*w) x w matrix.
+  const int P = c.nranks;
+  float* S = ws.stack + off;
+  const long long lds = (long long)P * w;
+  off += lds * w;
+  for (int r = 0; r < P; ++r) CK(copy_block(w, w, ws.gather + (long long)r * w * w, w, S + r * w, lds, c.stream));
+  CKR(caqr_rec(ws, off, P * w, w, S, lds, Rout, ldr, true, col0));
+  // X <- X * S[rank*w:(rank+1)*w, :]  (one block of all m rows)
+  CK(panel_apply(m, w, X, ldx, m, 1, S + (long long)c.rank * w, lds, c.stream));
+  return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// Alg. 2 recursion on columns [c0, c0+w) of the working matrix Q (m x n, ldq), R (ldr).
+// ------------------------------------------------------------------------------------------
+struct FactorJob {
+  int m, n;
+  float* Q;
+  long long ldq;
+  float* R;
+  long long ldr;
+  FactorWs* ws;
+};
+
+static int rgs(FactorJob& J, int c0, int w, bool need_h) {
+  Context& c = g_ctx;
+  FactorWs& ws = *J.ws;
+  const int m = J.m;
+  float* Qc = J.Q + (long long)c0 * J.ldq;
+  if (w <= 32) {
+    CKR(panel(ws, m, w, Qc, J.ldq, J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0));
+  } else {
+    const int h = split_point(w), w2 = w - h;
+    const bool tc = w > c.cfg.cutoff;
+    CKR(rgs(J, c0, h, tc || need_h));  // Alg. 2 line 7
+    float* A2 = J.Q + (long long)(c0 + h) * J.ldq;
+    float* Rblk = J.R + c0 + (long long)(c0 + h) * J.ldr;
+    if (tc) {
+      // Alg. 2 line 8 on tensor cores: K1 cast of A2, K3 split-K TN, [allreduce], finalize.
+      __half* A1h = ws.Qh + (long long)c0 * ws.ldh;
+      __half* A2h = ws.Qh + (long long)(c0 + h) * ws.ldh;
+      CK(cast_scale(m, w2, A2, J.ldq, A2h, ws.ldh, ws.inv_s + c0 + h, c.cfg.col_scaling,
+                    c.d_status, c0 + h, c.stream));
+      CK(tc_gemm_tn(m, h, w2, A1h, ws.ldh, A2h, ws.ldh, ws.T, h, ws.inv_s + c0 + h, ws.P,
+                    ws.p_cap, c.num_sms, c.stream));
+      CKR(allreduce_f32(ws.T, (size_t)h * w2));
+      const long long ldh2 = round_up(h, 8);
+      CK(r12_finalize(h, w2, ws.T, h, Rblk, J.ldr, ws.R12h, ldh2, ws.inv_s2 + c0 + h,
+                      c.cfg.col_scaling, c.stream));
+      // Alg. 2 line 9 argument on tensor cores: K4.
+      CK(tc_gemm_nn_update(m, h, w2, A1h, ws.ldh, ws.R12h, ldh2, A2, J.ldq, ws.inv_s2 + c0 + h,
+                           c.num_sms, c.stream));
+    } else {
+      CK(f32_tn(m, h, w2, Qc, J.ldq, A2, J.ldq, ws.T, ws.P, ws.p_cap, c.num_sms, c.stream));
+      CKR(allreduce_f32(ws.T, (size_t)h * w2));
+      CK(copy_block(h, w2, ws.T, h, Rblk, J.ldr, c.stream));
+      CK(f32_nn_update(m, h, w2, Qc, J.ldq, ws.T, A2, J.ldq, c.stream));
+    }
+    CKR(rgs(J, c0 + h, w2, need_h));  // Alg. 2 line 9
+    return 0;
+  }
+  if (need_h) {
+    // Q columns of this panel are final: emit their FP16 shadow for the GEMMs above.
+    CK(cast_scale(m, w, Qc, J.ldq, ws.Qh + (long long)c0 * ws.ldh, ws.ldh, nullptr, 0, nullptr, 0,
+                  c.stream));
+  }
+  return 0;
+}
+
+// Enqueue the whole factorization (no host synchronization inside: graph-capturable).
+static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q, float* R,
+                          FactorWs& ws) {
+  Context& c = g_ctx;
+  CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));  // INT_MAX-ish = OK
+  CK(cudaMemsetAsync(R, 0, sizeof(float) * (size_t)n * n, c.stream));
+  CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream));
+  FactorJob J{m, n, Q, (long long)m, R, (long long)n, &ws};
+  const bool need_h = n > c.cfg.cutoff;
+  CKR(rgs(J, 0, n, need_h));
+  CK(zero_lower(n, R, n, c.stream));
+  CKR(allreduce_max_i32(c.d_status));
+  return 0;
+}
+
+static int read_status() {
+  Context& c = g_ctx;
+  CK(cudaMemcpyAsync(c.h_status, c.d_status, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  const int s = *c.h_status;
+  return (s == 0x7f7f7f7f) ? 0 : s;
+}
+
+static std::string graph_key(const char* tag, std::initializer_list<long long> v) {
+  std::string k(tag);
+  char buf[32];
+  for (long long x : v) {
+    snprintf(buf, sizeof buf, ":%llx", (unsigned long long)x);
+    k += buf;
+  }
+  const tcqr_config_t& f = g_ctx.cfg;
+  snprintf(buf, sizeof buf, "|%d,%d,%d", f.cutoff, f.panel_rows, f.col_scaling);
+  k += buf;
+  return k;
+}
+
+static int run_factor(int m, int n, const float* A, long long lda, float* Q, float* R,
+                      FactorWs& ws, const void* ws_base) {
+  Context& c = g_ctx;
+  if (!c.cfg.use_graphs) return enqueue_factor(m, n, A, lda, Q, R, ws);
+  const std::string key =
+      graph_key("f", {m, n, lda, (long long)A, (long long)Q, (long long)R, (long long)ws_base});
+  auto it = c.graphs.find(key);
+  if (it == c.graphs.end()) {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_factor(m, n, A, lda, Q, R, ws);
+    cudaError_t e = cudaStreamEndCapture(c.stream, &g);
+    if (rc != 0) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    CK(e);
+    GraphEntry ge;
+    e = cudaGraphInstantiate(&ge.exec, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    it = c.graphs.emplace(key, ge).first;
+  }
+  CK(cudaGraphLaunch(it->second.exec, c.stream));
+  return 0;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static int check_common(long long m, long long n, const void* A, long long lda) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (m < 1 || m > (1LL << 31) - 1) return -1;
+  if (n < 1 || n > 65536) return -2;
+  if (g_ctx.nranks == 1 && m < n) return -1;
+  if (g_ctx.nranks > 1 && m < 32) return -1;
+  if (!A || !aligned16(A)) return -3;
+  if (lda < m || (lda * 4) % 16) return -4;
+  return 0;
+}
+
+}  // namespace tcqr
+
+using namespace tcqr;
+
+// ==========================================================================================
+// C ABI
+// ==========================================================================================
+extern "C" {
+
+const char* tcqr_version(void) { return "tcqr 0.1 (sm_100a tcgen05; arXiv 1912.05508)"; }
+
+void tcqr_default_config(tcqr_config_t* c) {
+  if (!c) return;
+  c->cutoff = 128;
+  c->panel_rows = 256;
+  c->col_scaling = 1;
+  c->restart = 1;
+  c->tol2 = 1e-6;
+  c->stag_window = 10;
+  c->stag_floor = 1e-11;
+  c->use_graphs = 1;
+}
+
+int tcqr_set_config(const tcqr_config_t* cfg) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!cfg) return -1;
+  if (cfg->cutoff < 32 || cfg->cutoff > 128 || cfg->cutoff % 32) return -1;
+  if (cfg->panel_rows < 64 || cfg->panel_rows > 480 || cfg->panel_rows % 32) return -1;
+  if (cfg->tol2 <= 0 || cfg->stag_window < 1 || cfg->stag_floor < 0) return -1;
+  g_ctx.cfg = *cfg;
+  return 0;
+}
+
+int tcqr_nccl_unique_id(void* out) {
+  if (!out) return -1;
+  if (!g_nccl.load()) return TCQR_ERR_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return TCQR_ERR_NCCL;
+  memcpy(out, &id, sizeof(id));
+  return 0;
+}
+
+int tcqr_finalize(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Context& c = g_ctx;
+  if (!c.inited) return 0;
+  cudaSetDevice(c.device);
+  cudaStreamSynchronize(c.stream);
+  for (auto& kv : c.graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  c.graphs.clear();
+  if (c.own_ws) cudaFree(c.own_ws);
+  c.own_ws = nullptr;
+  c.own_ws_bytes = 0;
+  if (c.d_status) cudaFree(c.d_status);
+  if (c.h_status) cudaFreeHost(c.h_status);
+  c.d_status = nullptr;
+  c.h_status = nullptr;
+  if (c.comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c.comm);
+  c.comm = nullptr;
+  c.user_ws = nullptr;
+  c.user_ws_bytes = 0;
+  c.inited = false;
+  return 0;
+}
+
+int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int rank, int nranks) {
+  if (g_ctx.inited) tcqr_finalize();
+  std::lock_guard<std::mutex> lk(g_mu);
+  Context& c = g_ctx;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return -4;
+  if (nranks > 1 && !nccl_unique_id) return -3;
+  if (cudaSetDevice(device) != cudaSuccess) return -1;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return TCQR_ERR_CUDA;
+  if (prop.major != 10) {
+    fprintf(stderr, "tcqr: device %d is sm_%d%d; this library is built for sm_100a only\n", device,
+            prop.major, prop.minor);
+    return TCQR_ERR_UNSUPPORTED;
+  }
+  c.device = device;
+  c.stream = static_cast<cudaStream_t>(cuda_stream);
+  c.num_sms = prop.multiProcessorCount;
+  c.rank = rank;
+  c.nranks = nranks;
+  tcqr_default_config(&c.cfg);
+  if (cudaMalloc(&c.d_status, 64) != cudaSuccess) return TCQR_ERR_OOM;
+  if (cudaMallocHost(&c.h_status, 64) != cudaSuccess) return TCQR_ERR_OOM;
+  if (nranks > 1) {
+    if (!g_nccl.load()) return TCQR_ERR_NCCL;
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    if (g_nccl.CommInitRank(&c.comm, nranks, id, rank) != ncclSuccess) return TCQR_ERR_NCCL;
+  }
+  c.inited = true;
+  return 0;
+}
+
+int tcqr_workspace_size(int64_t m, int64_t n, int op, size_t* bytes) {
+  if (!bytes || m < 1 || n < 1 || (op != 0 && op != 1)) return -1;
+  *bytes = ws_bytes(m, n, op, g_ctx.inited ? g_ctx.nranks : 1, 2000);
+  return 0;
+}
+
+int tcqr_set_workspace(void* dptr, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (dptr && !aligned16(dptr)) return -1;
+  g_ctx.user_ws = dptr;
+  g_ctx.user_ws_bytes = dptr ? bytes : 0;
+  return 0;
+}
+
+int tcqr_factor(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, float* R) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc = check_common(m, n, A, lda);
+  if (rc) return rc;
+  if (!Q || !aligned16(Q)) return -5;
+  if (!R || !aligned16(R)) return -6;
+  if (Q == A && lda != m) return -5;
+  Context& c = g_ctx;
+  cudaSetDevice(c.device);
+  const size_t need = ws_bytes(m, n, 0, c.nranks, 0);
+  char* base = get_ws(need);
+  if (!base) return TCQR_ERR_OOM;
+  Arena a{base, 0};
+  FactorWs ws;
+  plan_factor_ws(a, m, n, c.nranks, ws);
+  CKR(run_factor((int)m, (int)n, A, lda, Q, R, ws, base));
+  return read_status();
+}
+
+static int lls_pass(LlsWs& w, int m, int n, const float* A, long long lda, double tol, int maxit,
+                    double sref, int* iters, int* reason, double* s0, double* final_rel) {
+  Context& c = g_ctx;
+  CgState hs;
+  memset(&hs, 0, sizeof hs);
+  hs.tol = tol;
+  hs.floor = c.cfg.stag_floor;
+  hs.window = c.cfg.stag_window;
+  hs.maxit = maxit;
+  hs.sref = sref;
+  hs.hist_cap = w.hist_cap;
+  CK(cudaMemcpyAsync(w.st, &hs, sizeof hs, cudaMemcpyHostToDevice, c.stream));
+  const int* done = &w.st->done;
+  // set-up: s = R^-T (A' r)   (Alg. 5 line 7, R-A10 ii)
+  CK(cg_launch_a_t(m, n, A, lda, w.r, w.v, nullptr, c.stream));
+  CKR(allreduce_f64(w.v, n));
+  CK(cg_launch_tri_t(n, w.M, n, w.v, w.s, nullptr, c.stream));
+  CK(cg_launch_init(n, w.st, w.s, w.p, w.x, w.xbest, c.stream));
+  const int ndp = (m + 255) / 256;
+  int launched = 0;
+  while (true) {
+    const int chunk = 8;
+    for (int i = 0; i < chunk; ++i) {
+      CK(cg_launch_tri_n(n, w.M, n, w.p, w.t, w.part, done, c.stream));               // t = inv(R) p
+      CK(cg_launch_a_n(m, n, A, lda, w.t, w.q, w.part, w.dpart, done, c.stream));      // q = A t
+      CK(cg_launch_sum_parts(ndp, w.dpart, &w.st->delta, done, c.stream));             // delta
+      CKR(allreduce_f64(&w.st->delta, 1));
+      CK(cg_launch_update_xr(m, n, w.st, w.x, w.t, w.r, w.q, c.stream));               // x, r
+      CK(cg_launch_a_t(m, n, A, lda, w.r, w.v, done, c.stream));                       // A' r
+      CKR(allreduce_f64(w.v, n));
+      CK(cg_launch_tri_t(n, w.M, n, w.v, w.s, done, c.stream));                        // s
+      CK(cg_launch_finish(n, w.st, w.s, w.p, w.x, w.xbest, w.hist, c.stream));          // beta, p
+    }
+    launched += chunk;
+    CK(cudaMemcpyAsync(&hs, w.st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    if (hs.done || launched >= maxit + chunk) break;
+  }
+  *iters = hs.k;
+  *reason = hs.reason;
+  *s0 = hs.s0;
+  *final_rel = hs.s0 > 0 ? hs.best / hs.s0 : 0.0;
+  if (hs.reason == 0 && hs.s0 > 0) {
+    // tolerance stop keeps the last iterate; report its ratio
+    *final_rel = hs.best / hs.s0;
+  }
+  return 0;
+}
+
+int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const double* b, double* x,
+                   double tol, int maxit, tcqr_lls_info_t* info) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc = check_common(m, n, A, lda);
+  if (rc) return rc;
+  if (!b) return -5;
+  if (!x) return -6;
+  if (!(tol > 0)) return -7;
+  if (maxit < 1) return -8;
+  Context& c = g_ctx;
+  cudaSetDevice(c.device);
+  const size_t need = ws_bytes(m, n, 1, c.nranks, maxit);
+  char* base = get_ws(need);
+  if (!base) return TCQR_ERR_OOM;
+  Arena a{base, 0};
+  LlsWs w;
+  plan_lls_ws(a, m, n, c.nranks, maxit, w);
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaEventRecord(e0, c.stream);
+  // QR of a working copy (A is problem data and stays untouched; Q is not an output, R-A25).
+  rc = run_factor((int)m, (int)n, A, lda, w.Aw, w.R, w.f, base);
+  if (rc == 0) rc = read_status();
+  if (rc != 0) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    return rc;
+  }
+  cudaEventRecord(e1, c.stream);
+  // K6 set-up: M = inv(R) in FP64 (reading R-A13).
+  CK(trinv_f64((int)n, w.R, n, w.M, n, w.W, c.num_sms, c.stream));
+  // pass 1: r = b, x = 0
+  CK(cudaMemcpyAsync(w.r, b, sizeof(double) * m, cudaMemcpyDeviceToDevice, c.stream));
+  int it1 = 0, reason1 = 0, it2 = 0, reason2 = -1;
+  double s01 = 0, fr1 = 0, s02 = 0, fr2 = 0;
+  CKR(lls_pass(w, (int)m, (int)n, A, lda, tol, maxit, 0.0, &it1, &reason1, &s01, &fr1));
+  int passes = 1;
+  CK(cudaMemcpyAsync(x, w.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  if (c.cfg.restart && reason1 != 3) {
+    // pass 2 (reading R-A12): restart from the true FP64 residual r = b - A x1, tol2, floor
+    // relative to pass 1's ||s0||.
+    CK(gemv_f32_n((int)m, (int)n, A, lda, x, w.q, w.part, w.part_cap, c.stream));
+    CK(cg_launch_residual((int)m, b, w.q, w.r, c.stream));
+    CKR(lls_pass(w, (int)m, (int)n, A, lda, c.cfg.tol2, maxit, s01, &it2, &reason2, &s02, &fr2));
+    CK(cg_launch_axpy((int)n, 1.0, w.x, x, c.stream));
+    passes = 2;
+  }
+  cudaEventRecord(e2, c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  float qr_ms = 0, cg_ms = 0;
+  cudaEventElapsedTime(&qr_ms, e0, e1);
+  cudaEventElapsedTime(&cg_ms, e1, e2);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  if (info) {
+    info->iterations = it1 + it2;
+    info->iterations_pass1 = it1;
+    info->outer_passes = passes;
+    const int last_reason = passes == 2 ? reason2 : reason1;
+    info->stop_reason = last_reason;
+    info->converged = (last_reason == 0 || last_reason == 1 || last_reason == 3) ? 1 : 0;
+    info->s0 = s01;
+    info->final_rel = passes == 2 ? fr2 : fr1;
+    info->qr_ms = qr_ms;
+    info->cgls_ms = cg_ms;
+  }
+  return 0;
+}
+
+int tcqr_factor_host(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, float* R) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  if (!A) return -3;
+  if (lda < m) return -4;
+  if (!Q) return -5;
+  if (!R) return -6;
+  Context& c = g_ctx;
+  cudaSetDevice(c.device);
+  float *dQ = nullptr, *dR = nullptr;
+  if (cudaMallocAsync(&dQ, sizeof(float) * m * n, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
+  if (cudaMallocAsync(&dR, sizeof(float) * n * n, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
+  CK(cudaMemcpy2DAsync(dQ, sizeof(float) * m, A, sizeof(float) * lda, sizeof(float) * m, n,
+                       cudaMemcpyHostToDevice, c.stream));
+  int rc = tcqr_factor(m, n, dQ, m, dQ, dR);
+  if (rc == 0) {
+    CK(cudaMemcpyAsync(Q, dQ, sizeof(float) * m * n, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(R, dR, sizeof(float) * n * n, cudaMemcpyDeviceToHost, c.stream));
+  }
+  cudaFreeAsync(dQ, c.stream);
+  cudaFreeAsync(dR, c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  return rc;
+}
+
+int tcqr_lls_solve_host(int64_t m, int64_t n, const float* A, int64_t lda, const double* b,
+                        double* x, double tol, int maxit, tcqr_lls_info_t* info) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  if (!A) return -3;
+  if (lda < m) return -4;
+  if (!b) return -5;
+  if (!x) return -6;
+  Context& c = g_ctx;
+  cudaSetDevice(c.device);
+  float* dA = nullptr;
+  double *db = nullptr, *dx = nullptr;
+  if (cudaMallocAsync(&dA, sizeof(float) * m * n, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
+  if (cudaMallocAsync(&db, sizeof(double) * m, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
+  if (cudaMallocAsync(&dx, sizeof(double) * n, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
+  CK(cudaMemcpy2DAsync(dA, sizeof(float) * m, A, sizeof(float) * lda, sizeof(float) * m, n,
+                       cudaMemcpyHostToDevice, c.stream));
+  CK(cudaMemcpyAsync(db, b, sizeof(double) * m, cudaMemcpyHostToDevice, c.stream));
+  int rc = tcqr_lls_solve(m, n, dA, m, db, dx, tol, maxit, info);
+  if (rc == 0) CK(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+  cudaFreeAsync(dA, c.stream);
+  cudaFreeAsync(db, c.stream);
+  cudaFreeAsync(dx, c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  return rc;
+}
+
+// ---- component entry points ----
+int tcqr_cast_scale(int64_t m, int64_t w, const float* X, int64_t ldx, uint16_t* Xh, int64_t ldh,
+                    float* inv_s, int scaling) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (m < 1) return -1;
+  if (w < 1) return -2;
+  if (!X) return -3;
+  if (ldx < m) return -4;
+  if (!Xh) return -5;
+  if (ldh < m) return -6;
+  Context& c = g_ctx;
+  CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));
+  CK(cast_scale((int)m, (int)w, X, ldx, reinterpret_cast<__half*>(Xh), ldh, inv_s, scaling,
+                c.d_status, 0, c.stream));
+  return read_status();
+}
+
+int tcqr_gemm_tn(int64_t m, int64_t h, int64_t w2, const uint16_t* A1h, int64_t lda1,
+                 const uint16_t* A2h, int64_t lda2, float* C, int64_t ldc, const float* col_mult) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (m < 1) return -1;
+  if (h < 1) return -2;
+  if (w2 < 1) return -3;
+  if (!A1h || !aligned16(A1h)) return -4;
+  if (lda1 < m || lda1 % 8) return -5;
+  if (!A2h || !aligned16(A2h)) return -6;
+  if (lda2 < m || lda2 % 8) return -7;
+  if (!C) return -8;
+  if (ldc < h) return -9;
+  Context& c = g_ctx;
+  const size_t need = ws_bytes(64, 64, 0, 1, 0);
+  char* base = get_ws(need);
+  if (!base) return TCQR_ERR_OOM;
+  Arena a{base, 0};
+  FactorWs ws;
+  plan_factor_ws(a, 64, 64, 1, ws);
+  CK(tc_gemm_tn((int)m, (int)h, (int)w2, reinterpret_cast<const __half*>(A1h), lda1,
+                reinterpret_cast<const __half*>(A2h), lda2, C, ldc, col_mult, ws.P, ws.p_cap,
+                c.num_sms, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  return 0;
+}
+
+int tcqr_gemm_nn_update(int64_t m, int64_t h, int64_t w2, const uint16_t* Qh, int64_t ldq,
+                        const uint16_t* Bh, int64_t ldb, float* C, int64_t ldc,
+                        const float* col_mult) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (m < 1) return -1;
+  if (h < 1) return -2;
+  if (w2 < 1) return -3;
+  if (!Qh || !aligned16(Qh)) return -4;
+  if (ldq < m || ldq % 8) return -5;
+  if (!Bh || !aligned16(Bh)) return -6;
+  if (ldb < h || ldb % 8) return -7;
+  if (!C) return -8;
+  if (ldc < m) return -9;
+  Context& c = g_ctx;
+  CK(tc_gemm_nn_update((int)m, (int)h, (int)w2, reinterpret_cast<const __half*>(Qh), ldq,
+                       reinterpret_cast<const __half*>(Bh), ldb, C, ldc, col_mult, c.num_sms,
+                       c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  return 0;
+}
+
+int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t ldr, int br) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (m < 1) return -1;
+  if (w < 1 || w > 32) return -2;
+  if (!X) return -3;
+  if (ldx < m) return -4;
+  if (!R) return -5;
+  if (ldr < w) return -6;
+  if (br < 64 || br > 480 || br % 32) return -7;
+  Context& c = g_ctx;
+  const int saved = c.cfg.panel_rows;
+  c.cfg.panel_rows = br;
+  const size_t need = ws_bytes(m, 32, 0, 1, 0);
+  char* base = get_ws(need);
+  if (!base) return TCQR_ERR_OOM;
+  Arena a{base, 0};
+  FactorWs ws;
+  plan_factor_ws(a, m, 32, 1, ws);
+  CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));
+  long long off = 0;
+  int rc = caqr_rec(ws, off, (int)m, (int)w, X, ldx, R, ldr, true, 0);
+  c.cfg.panel_rows = saved;
+  if (rc) return rc;
+  return read_status();
+}
+
+int tcqr_trinv(int64_t n, const float* R, int64_t ldr, double* Minv, int64_t ldm) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (n < 1) return -1;
+  if (!R) return -2;
+  if (ldr < n) return -3;
+  if (!Minv) return -4;
+  if (ldm < n) return -5;
+  Context& c = g_ctx;
+  double* W = nullptr;
+  CK(cudaMallocAsync(&W, sizeof(double) * trinv_w_count(n), c.stream));
+  CK(trinv_f64((int)n, R, ldr, Minv, ldm, W, c.num_sms, c.stream));
+  cudaFreeAsync(W, c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  return 0;
+}
+
+int tcqr_gemv(int trans, int64_t m, int64_t n, const float* A, int64_t lda, const double* v,
+              double* y) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (trans != 0 && trans != 1) return -1;
+  if (m < 1) return -2;
+  if (n < 1) return -3;
+  if (!A) return -4;
+  if (lda < m) return -5;
+  if (!v) return -6;
+  if (!y) return -7;
+  Context& c = g_ctx;
+  if (trans == 0) {
+    double* part = nullptr;
+    const long long cap = (long long)cg_gemv_n_chunks((int)n) * m;
+    CK(cudaMallocAsync(&part, sizeof(double) * cap, c.stream));
+    CK(gemv_f32_n((int)m, (int)n, A, lda, v, y, part, cap, c.stream));
+    cudaFreeAsync(part, c.stream);
+  } else {
+    CK(gemv_f32_t((int)m, (int)n, A, lda, v, y, c.stream));
+  }
+  CK(cudaStreamSynchronize(c.stream));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,145 @@
+"""GPU parity of the individual hot-path kernels through the C ABI.
+
+Each kernel is compared element by element with a plain float64 reference built from the SAME
+rounded inputs (oracle.fp16 for the FP16 rounding), at sizes spanning several tiles and ragged
+edges. Tolerances: FP16 cast bitwise; tensor-core GEMMs within the FP32-accumulation envelope
+|gpu - ref| <= k 2^-22 ||row|| ||col||; FP32 panel within 1e-5 of the FP64 oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import workloads as W  # noqa: E402
+from oracle.fp16 import fl16, pow2_colscale  # noqa: E402
+from oracle.metrics import orthogonality_f, r_rel_error  # noqa: E402
+from oracle.qr import caqr, mgs  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def tq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1912_05508_b200 as tq
+    tq.init(0)
+    return tq
+
+
+def _h2np(xh):
+    return xh.float().cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("m,w", [(1000, 7), (4096, 33), (37, 3)])
+def test_cast_scale_bitwise(tq, m, w):
+    rng = np.random.default_rng(m)
+    x = (rng.standard_normal((m, w)) * np.exp2(rng.integers(-30, 20, w))).astype(np.float32)
+    x[:, 1] = 0.0
+    X = tq.to_device_colmajor(x)
+    Xh, inv_s = tq.cast_scale(X, scaling=True)
+    s = pow2_colscale(x.astype(np.float64))
+    ref = fl16(x.astype(np.float64) * s)
+    assert np.array_equal(_h2np(Xh), ref)
+    assert np.array_equal(inv_s.cpu().numpy().astype(np.float64), 1.0 / s)
+    Xh2, _ = tq.cast_scale(X, scaling=False)
+    with np.errstate(over="ignore"):
+        assert np.array_equal(_h2np(Xh2), fl16(x.astype(np.float64)))
+
+
+def test_cast_flags_nonfinite(tq):
+    x = np.ones((300, 5), np.float32)
+    x[17, 3] = np.nan
+    X = tq.to_device_colmajor(x)
+    with pytest.raises(tq.TcqrError) as e:
+        tq.cast_scale(X)
+    assert e.value.code == 4
+
+
+def _fp16_operand(rng, m, k, scale=1.0):
+    return fl16(rng.standard_normal((m, k)) * scale)
+
+
+@pytest.mark.parametrize("m,h,w2", [(64, 128, 128), (1000, 96, 200), (4160, 128, 384),
+                                    (8192, 300, 130), (262144, 128, 128)])
+def test_gemm_tn_envelope(tq, m, h, w2):
+    rng = np.random.default_rng(h + w2)
+    a1 = _fp16_operand(rng, m, h)
+    a2 = _fp16_operand(rng, m, w2)
+    mult = np.exp2(rng.integers(-3, 3, w2)).astype(np.float32)
+    A1 = tq.to_device_colmajor(a1, dtype=torch.float16)
+    A2 = tq.to_device_colmajor(a2, dtype=torch.float16)
+    C = tq.gemm_tn(A1, A2, torch.from_numpy(mult).cuda()).cpu().numpy().astype(np.float64)
+    ref = (a1.T @ a2) * mult
+    env = 8 * 2.0 ** -22 * np.outer(np.linalg.norm(a1, axis=0), np.linalg.norm(a2, axis=0)) * mult
+    err = np.abs(C - ref)
+    assert np.all(err <= env + 1e-30), float(np.max(err / env))
+
+
+@pytest.mark.parametrize("m,h,w2", [(128, 64, 128), (1000, 96, 200), (4160, 256, 384),
+                                    (3000, 512, 64)])
+def test_gemm_nn_update_envelope(tq, m, h, w2):
+    rng = np.random.default_rng(m + h)
+    qh = _fp16_operand(rng, m, h, 0.05)
+    bh = _fp16_operand(rng, h, w2)
+    c = rng.standard_normal((m, w2)).astype(np.float32)
+    mult = np.exp2(rng.integers(-3, 3, w2)).astype(np.float32)
+    Q = tq.to_device_colmajor(qh, dtype=torch.float16)
+    B = tq.to_device_colmajor(bh, dtype=torch.float16)
+    C = tq.to_device_colmajor(c)
+    tq.gemm_nn_update(C, Q, B, torch.from_numpy(mult).cuda())
+    got = C.cpu().numpy().astype(np.float64)
+    ref = c.astype(np.float64) - (qh @ bh) * mult
+    env = 8 * 2.0 ** -22 * np.outer(np.linalg.norm(qh, axis=1), np.linalg.norm(bh, axis=0)) * mult \
+        + 2.0 ** -23 * np.abs(ref) * 2
+    assert np.all(np.abs(got - ref) <= env + 1e-30), float(np.max(np.abs(got - ref) / env))
+
+
+def test_gemm_exact_small_integers(tq):
+    # FP16 small integers: products and sums exact in FP32 -> bitwise (SPEC.md:58 analogue).
+    rng = np.random.default_rng(5)
+    a1 = rng.integers(-3, 4, (512, 128)).astype(np.float64)
+    a2 = rng.integers(-3, 4, (512, 256)).astype(np.float64)
+    A1 = tq.to_device_colmajor(a1, dtype=torch.float16)
+    A2 = tq.to_device_colmajor(a2, dtype=torch.float16)
+    C = tq.gemm_tn(A1, A2).cpu().numpy().astype(np.float64)
+    assert np.array_equal(C, a1.T @ a2)
+
+
+@pytest.mark.parametrize("m,w,br", [(256, 32, 256), (300, 32, 256), (1024, 32, 256),
+                                    (4096, 32, 256), (70000, 32, 256), (5000, 17, 128),
+                                    (33, 32, 64)])
+def test_panel_vs_oracle(tq, m, w, br):
+    a = W.gaussian(m, w, seed=m + w)
+    X = tq.to_device_colmajor(a)
+    Xq, R = tq.panel_qr(X, br=br)
+    q, r = Xq.cpu().numpy().astype(np.float64), R.cpu().numpy().astype(np.float64)
+    _, r_o = mgs(a.astype(np.float64))
+    assert np.array_equal(r, np.triu(r)) and np.all(np.diag(r) > 0)
+    assert r_rel_error(r, r_o) < 1e-5
+    assert orthogonality_f(q) < 1e-5
+    assert np.linalg.norm(a - q @ r) / np.linalg.norm(a) < 1e-6
+
+
+def test_panel_planted_hadamard_bitwise(tq):
+    a, qt, r0 = W.planted_hadamard(1024, 32, seed=201)
+    X = tq.to_device_colmajor(a)
+    Xq, R = tq.panel_qr(X, br=256)
+    assert np.array_equal(R.cpu().numpy().astype(np.float64), r0)
+    assert np.array_equal(Xq.cpu().numpy().astype(np.float64), qt)
+
+
+def test_trinv_and_gemv(tq):
+    rng = np.random.default_rng(9)
+    n = 300
+    r = np.triu(rng.standard_normal((n, n))) + np.diag(3 + rng.random(n))
+    r = r.astype(np.float32)
+    M = tq.trinv(tq.to_device_colmajor(r)).cpu().numpy()
+    res = np.linalg.norm(r.astype(np.float64) @ M - np.eye(n)) / np.sqrt(n)
+    assert res < 1e-12
+    a = rng.standard_normal((1000, n)).astype(np.float32)
+    A = tq.to_device_colmajor(a)
+    v = rng.standard_normal(n)
+    y = tq.gemv(A, torch.from_numpy(v).cuda()).cpu().numpy()
+    assert np.allclose(y, a.astype(np.float64) @ v, rtol=1e-12, atol=1e-10)
+    u = rng.standard_normal(1000)
+    z = tq.gemv(A, torch.from_numpy(u).cuda(), trans=True).cpu().numpy()
+    assert np.allclose(z, a.astype(np.float64).T @ u, rtol=1e-12, atol=1e-10)

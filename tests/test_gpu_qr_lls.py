@@ -1,0 +1,179 @@
+"""GPU parity of the whole hot path through the C ABI: tcqr_factor and tcqr_lls_solve against the CPU
+FP64 oracle (north_star tolerances: ||A-QR||_F/||A||_F <= 5e-3, ||Q'Q-I||_F/sqrt(n) <= 5e-2,
+||R-R_o||_F/||R_o||_F <= 1e-2 for kappa <= 1e3; x within 1e-10 of the oracle for the FP64 target),
+plus the closed-form pins: planted Hadamard bitwise (P2), power-of-two scale equivariance bitwise
+(P3), breakdown / non-finite status codes, degenerate right-hand sides."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import workloads as W  # noqa: E402
+from oracle.cgls import oracle_lls  # noqa: E402
+from oracle.metrics import (backward_error_f, orthogonality_f, r_rel_error,  # noqa: E402
+                            x_rel_error, lls_optimality)
+from oracle.qr import rgs  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def tq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1912_05508_b200 as tq
+    tq.init(0)
+    yield tq
+    tq.set_config()
+
+
+def _factor(tq, a, **cfg):
+    tq.set_config(**cfg)
+    A = tq.to_device_colmajor(a)
+    Q, R = tq.factor(A)
+    torch.cuda.synchronize()
+    return Q.cpu().numpy().astype(np.float64), R.cpu().numpy().astype(np.float64)
+
+
+def _gates(a, q, r, r_o, orth_gate=5e-2):
+    be = backward_error_f(a, q, r)
+    orth = orthogonality_f(q)
+    re = r_rel_error(r, r_o)
+    assert np.array_equal(r, np.triu(r)) and np.all(np.diag(r) > 0)
+    assert be <= 5e-3, be
+    assert orth <= orth_gate, orth
+    assert re <= 1e-2, re
+    return be, orth, re
+
+
+@pytest.mark.parametrize("m,n,cutoff", [(1024, 128, 128), (1024, 128, 64), (1024, 128, 32),
+                                        (1000, 100, 32), (777, 96, 64), (2048, 512, 128),
+                                        (4100, 300, 64), (300, 300, 128)])
+def test_factor_gaussian_gates(tq, m, n, cutoff):
+    a = W.gaussian(m, n, seed=m * 7 + n)
+    q, r = _factor(tq, a, cutoff=cutoff)
+    _, r_o = rgs(a.astype(np.float64))
+    be, orth, re = _gates(a, q, r, r_o)
+    if n <= cutoff:   # no FP16 anywhere: FP32 accuracy
+        assert be < 1e-5 and re < 1e-4
+
+
+@pytest.mark.parametrize("kind,cond", [("geometric", 1e2), ("arithmetic", 1e3)])
+def test_factor_spectrum_gates(tq, kind, cond):
+    a = W.spectrum_matrix(4096, 1024, kind, cond, seed=3)
+    q, r = _factor(tq, a)
+    _, r_o = rgs(a.astype(np.float64))
+    _gates(a, q, r, r_o)
+
+
+@pytest.mark.parametrize("n,cutoff", [(128, 32), (128, 128), (256, 32), (256, 64)])
+def test_factor_planted_hadamard_bitwise(tq, n, cutoff):
+    a, qt, r0 = W.planted_hadamard(1024, n, seed=201)
+    q, r = _factor(tq, a, cutoff=cutoff, panel_rows=256)
+    assert np.array_equal(r, r0)
+    assert np.array_equal(q, qt)
+
+
+def test_factor_scale_equivariance_bitwise(tq):
+    a = W.gaussian(2048, 384, seed=11)
+    q, r = _factor(tq, a, cutoff=64)
+    for e in (-30, -9, 7, 20):
+        qe, re_ = _factor(tq, np.ldexp(a, e).astype(np.float32), cutoff=64)
+        assert np.array_equal(qe, q), e
+        assert np.array_equal(re_, np.ldexp(r, e)), e
+
+
+def test_factor_deterministic(tq):
+    a = W.gaussian(3000, 640, seed=5)
+    q1, r1 = _factor(tq, a)
+    q2, r2 = _factor(tq, a)
+    assert np.array_equal(q1, q2) and np.array_equal(r1, r2)
+
+
+def test_factor_breakdown_and_nonfinite(tq):
+    tq.set_config()
+    a = W.gaussian(512, 200, seed=2)
+    a[:, 150] = 0.0
+    with pytest.raises(tq.TcqrError) as e:
+        tq.factor(tq.to_device_colmajor(a))
+    assert e.value.code == 151
+    a = W.gaussian(512, 200, seed=2)
+    a[7, 42] = np.inf
+    with pytest.raises(tq.TcqrError) as e:
+        tq.factor(tq.to_device_colmajor(a))
+    assert e.value.code == 43
+
+
+def test_factor_argument_errors(tq):
+    A = tq.to_device_colmajor(W.gaussian(64, 32, seed=1))
+    import ctypes
+    lib = tq.lib()
+    p = ctypes.c_void_p(A.data_ptr())
+    assert lib.tcqr_factor(0, 32, p, 64, p, p) == -1
+    assert lib.tcqr_factor(64, 0, p, 64, p, p) == -2
+    assert lib.tcqr_factor(64, 32, None, 64, p, p) == -3
+    assert lib.tcqr_factor(64, 32, p, 63, p, p) == -4
+    assert lib.tcqr_factor(64, 32, p, 64, p, None) == -6
+    assert lib.tcqr_factor(16, 32, p, 64, p, p) == -1     # m < n
+
+
+def test_factor_host_entry_point(tq):
+    tq.set_config()
+    a = W.gaussian(1500, 200, seed=8)
+    q, r = tq.factor_host(a)
+    _, r_o = rgs(a.astype(np.float64))
+    _gates(a, q.astype(np.float64), r.astype(np.float64), r_o)
+
+
+@pytest.mark.parametrize("m,n,kind,cond", [(1024, 128, "gaussian", 1), (2048, 512, "arithmetic", 1e6),
+                                           (2048, 256, "cluster", 1e6), (2000, 300, "geometric", 1e3)])
+def test_lls_fp64_target(tq, m, n, kind, cond):
+    tq.set_config()
+    a = W.make_matrix(kind, m, n, seed=m + n, cond=cond)
+    b, x_true = W.consistent_rhs(a, seed=n)
+    x, info = tq.lls_solve(tq.to_device_colmajor(a), torch.from_numpy(b).cuda(), tol=1e-10,
+                           maxit=2000)
+    x = x.cpu().numpy()
+    x_o, _ = oracle_lls(a.astype(np.float64), b)
+    assert info["converged"] == 1, info
+    assert x_rel_error(x, x_o) <= 1e-10, (x_rel_error(x, x_o), info)
+
+
+def test_lls_large_residual_optimality(tq):
+    tq.set_config()
+    a = W.gaussian(3000, 400, seed=4)
+    b = W.random_rhs(3000, seed=5)
+    x, info = tq.lls_solve(tq.to_device_colmajor(a), torch.from_numpy(b).cuda())
+    x = x.cpu().numpy()
+    x_o, _ = oracle_lls(a.astype(np.float64), b)
+    assert x_rel_error(x, x_o) <= 1e-10
+    assert lls_optimality(a, x, b) <= 1e-9 * np.linalg.norm(a.astype(np.float64).T @ b)
+
+
+def test_lls_zero_projection_rhs(tq):
+    tq.set_config()
+    rng = np.random.default_rng(2)
+    a = W.gaussian(500, 50, seed=9)
+    qf, _ = np.linalg.qr(a.astype(np.float64), mode="complete")
+    b = qf[:, 100].copy()
+    x, info = tq.lls_solve(tq.to_device_colmajor(a), torch.from_numpy(b).cuda())
+    assert np.linalg.norm(x.cpu().numpy()) < 1e-10
+    assert info["converged"] == 1
+
+
+def test_lls_host_entry_point(tq):
+    tq.set_config()
+    a = W.gaussian(1024, 128, seed=1)
+    b, _ = W.consistent_rhs(a, seed=101)
+    x, info = tq.lls_solve_host(a, b)
+    x_o, _ = oracle_lls(a.astype(np.float64), b)
+    assert x_rel_error(x, x_o) <= 1e-10
+
+
+def test_lls_maxit_reports_not_converged(tq):
+    # SPEC.md:324-325 / :343: hitting the cap is data, not an error.
+    tq.set_config()
+    a = W.spectrum_matrix(2048, 256, "geometric", 1e6, seed=7)
+    b, _ = W.consistent_rhs(a, seed=8)
+    x, info = tq.lls_solve(tq.to_device_colmajor(a), torch.from_numpy(b).cuda(), maxit=5)
+    assert info["converged"] == 0 and info["stop_reason"] == 2
+    assert np.all(np.isfinite(x.cpu().numpy()))
