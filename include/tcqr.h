@@ -19,7 +19,8 @@
  *   - Every pointer argument is a DEVICE pointer on the context device, owned by the caller; the
  *     library never frees or retains it after the call returns.  Exception: tcqr_lls_solve_host /
  *     tcqr_factor_host take HOST pointers (end-to-end entry points that include the copies).
- *   - Base pointers must be 16-byte aligned and lda*4 a multiple of 16 bytes (TMA requirement).
+ *   - Base pointers must be 16-byte aligned (the FP16 shadows the TMA reads are library-owned,
+ *     so any lda >= m is accepted; the component GEMM entry points need FP16 lds % 8 == 0).
  *   - All calls enqueue on the context stream (tcqr_init) and synchronize on it once at the end
  *     to read the device status, so outputs are ready when the call returns.
  *   - Multi-GPU (row partition, one process per GPU): every rank calls with ITS OWN row block

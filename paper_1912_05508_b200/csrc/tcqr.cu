@@ -56,7 +56,9 @@ struct GraphEntry {
 struct Context {
   bool inited = false;
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;       // internal non-blocking stream (capturable)
+  cudaStream_t user_stream = nullptr;  // the caller's stream (may be the legacy NULL stream)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   int num_sms = 148;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
@@ -72,6 +74,16 @@ struct Context {
 };
 static Context g_ctx;
 static std::mutex g_mu;
+
+// Order the call after the caller's pending work, and the caller's stream after the call.
+static void begin_call() {
+  cudaEventRecord(g_ctx.ev_in, g_ctx.user_stream);
+  cudaStreamWaitEvent(g_ctx.stream, g_ctx.ev_in, 0);
+}
+static void end_call() {
+  cudaEventRecord(g_ctx.ev_out, g_ctx.stream);
+  cudaStreamWaitEvent(g_ctx.user_stream, g_ctx.ev_out, 0);
+}
 
 static int split_point(int w) { return 32 * ((w + 63) / 64); }
 static long long round_up(long long x, long long a) { return (x + a - 1) / a * a; }
@@ -370,6 +382,7 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
 
 static int read_status() {
   Context& c = g_ctx;
+  end_call();
   CK(cudaMemcpyAsync(c.h_status, c.d_status, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));
   const int s = *c.h_status;
@@ -425,7 +438,7 @@ static int check_common(long long m, long long n, const void* A, long long lda) 
   if (g_ctx.nranks == 1 && m < n) return -1;
   if (g_ctx.nranks > 1 && m < 32) return -1;
   if (!A || !aligned16(A)) return -3;
-  if (lda < m || (lda * 4) % 16) return -4;
+  if (lda < m) return -4;
   return 0;
 }
 
@@ -489,6 +502,11 @@ int tcqr_finalize(void) {
   c.h_status = nullptr;
   if (c.comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c.comm);
   c.comm = nullptr;
+  if (c.ev_in) cudaEventDestroy(c.ev_in);
+  if (c.ev_out) cudaEventDestroy(c.ev_out);
+  if (c.stream) cudaStreamDestroy(c.stream);
+  c.ev_in = c.ev_out = nullptr;
+  c.stream = nullptr;
   c.user_ws = nullptr;
   c.user_ws_bytes = 0;
   c.inited = false;
@@ -510,7 +528,11 @@ int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int ran
     return TCQR_ERR_UNSUPPORTED;
   }
   c.device = device;
-  c.stream = static_cast<cudaStream_t>(cuda_stream);
+  c.user_stream = static_cast<cudaStream_t>(cuda_stream);
+  if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess)
+    return TCQR_ERR_CUDA;
+  cudaEventCreateWithFlags(&c.ev_in, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c.ev_out, cudaEventDisableTiming);
   c.num_sms = prop.multiProcessorCount;
   c.rank = rank;
   c.nranks = nranks;
@@ -550,6 +572,7 @@ int tcqr_factor(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, flo
   if (!R || !aligned16(R)) return -6;
   if (Q == A && lda != m) return -5;
   Context& c = g_ctx;
+  begin_call();
   cudaSetDevice(c.device);
   const size_t need = ws_bytes(m, n, 0, c.nranks, 0);
   char* base = get_ws(need);
@@ -620,6 +643,7 @@ int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const doub
   if (!(tol > 0)) return -7;
   if (maxit < 1) return -8;
   Context& c = g_ctx;
+  begin_call();
   cudaSetDevice(c.device);
   const size_t need = ws_bytes(m, n, 1, c.nranks, maxit);
   char* base = get_ws(need);
@@ -692,6 +716,7 @@ int tcqr_factor_host(int64_t m, int64_t n, const float* A, int64_t lda, float* Q
   if (!Q) return -5;
   if (!R) return -6;
   Context& c = g_ctx;
+  begin_call();
   cudaSetDevice(c.device);
   float *dQ = nullptr, *dR = nullptr;
   if (cudaMallocAsync(&dQ, sizeof(float) * m * n, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
@@ -719,6 +744,7 @@ int tcqr_lls_solve_host(int64_t m, int64_t n, const float* A, int64_t lda, const
   if (!b) return -5;
   if (!x) return -6;
   Context& c = g_ctx;
+  begin_call();
   cudaSetDevice(c.device);
   float* dA = nullptr;
   double *db = nullptr, *dx = nullptr;
@@ -748,6 +774,7 @@ int tcqr_cast_scale(int64_t m, int64_t w, const float* X, int64_t ldx, uint16_t*
   if (!Xh) return -5;
   if (ldh < m) return -6;
   Context& c = g_ctx;
+  begin_call();
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));
   CK(cast_scale((int)m, (int)w, X, ldx, reinterpret_cast<__half*>(Xh), ldh, inv_s, scaling,
                 c.d_status, 0, c.stream));
@@ -767,6 +794,7 @@ int tcqr_gemm_tn(int64_t m, int64_t h, int64_t w2, const uint16_t* A1h, int64_t 
   if (!C) return -8;
   if (ldc < h) return -9;
   Context& c = g_ctx;
+  begin_call();
   const size_t need = ws_bytes(64, 64, 0, 1, 0);
   char* base = get_ws(need);
   if (!base) return TCQR_ERR_OOM;
@@ -794,6 +822,7 @@ int tcqr_gemm_nn_update(int64_t m, int64_t h, int64_t w2, const uint16_t* Qh, in
   if (!C) return -8;
   if (ldc < m) return -9;
   Context& c = g_ctx;
+  begin_call();
   CK(tc_gemm_nn_update((int)m, (int)h, (int)w2, reinterpret_cast<const __half*>(Qh), ldq,
                        reinterpret_cast<const __half*>(Bh), ldb, C, ldc, col_mult, c.num_sms,
                        c.stream));
@@ -811,6 +840,7 @@ int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t
   if (ldr < w) return -6;
   if (br < 64 || br > 480 || br % 32) return -7;
   Context& c = g_ctx;
+  begin_call();
   const int saved = c.cfg.panel_rows;
   c.cfg.panel_rows = br;
   const size_t need = ws_bytes(m, 32, 0, 1, 0);
@@ -835,6 +865,7 @@ int tcqr_trinv(int64_t n, const float* R, int64_t ldr, double* Minv, int64_t ldm
   if (!Minv) return -4;
   if (ldm < n) return -5;
   Context& c = g_ctx;
+  begin_call();
   double* W = nullptr;
   CK(cudaMallocAsync(&W, sizeof(double) * trinv_w_count(n), c.stream));
   CK(trinv_f64((int)n, R, ldr, Minv, ldm, W, c.num_sms, c.stream));
@@ -854,6 +885,7 @@ int tcqr_gemv(int trans, int64_t m, int64_t n, const float* A, int64_t lda, cons
   if (!v) return -6;
   if (!y) return -7;
   Context& c = g_ctx;
+  begin_call();
   if (trans == 0) {
     double* part = nullptr;
     const long long cap = (long long)cg_gemv_n_chunks((int)n) * m;

