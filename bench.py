@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py -- QR TFLOP/s of the RGSQRF hot path at 32768x16384 (BASELINE.json configs[2]) on N
+B200s, plus LLS time-to-FP64 accuracy (configs[3]) as an extra key.
+
+One "step" = one tcqr_factor of the whole matrix (all SURVEY.md §8(a) QR rows: copy/validate, the
+Alg. 2 recursion with K1 casts, K3/K4 tcgen05 GEMMs, FP32 products below the cutoff, the Eq. (6)
+panel), inputs resident in HBM. value = (2 M n^2 - 2/3 n^3) / time (the north_star convention),
+summed over the whole job (N > 1: row-partitioned single factorization, strong scaling).
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under torchrun (one rank per
+GPU, NCCL). --impl reference times the CPU oracle (the base contract's reference arm for this tier).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QR TFLOP/s at 32768x16384; LLS time-to-FP64 accuracy; 1/2/4/8 GPUs"
+WORKLOADS = {
+    "cfg3": dict(m=32768, n=16384, kind="gaussian", seed=4,
+                 name="QR of 32768x16384 Gaussian (BASELINE configs[2])"),
+    "cfg2": dict(m=16384, n=4096, kind="gaussian", seed=2,
+                 name="QR of 16384x4096 Gaussian (BASELINE configs[1])"),
+    "cfg5": dict(m=262144, n=2048, kind="gaussian", seed=8,
+                 name="QR of 262144x2048 Gaussian (BASELINE configs[4])"),
+    "cfg1": dict(m=1024, n=128, kind="gaussian", seed=1,
+                 name="QR of 1024x128 Gaussian (BASELINE configs[0])"),
+}
+
+
+def conv_flops(m, n):
+    return 2.0 * m * n * n - 2.0 / 3.0 * n ** 3
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], tc=d["bf16_tflops"], tc_sustained=d["bf16_tflops_sustained"],
+                    src="MEASURED_PEAKS.json (measured)")
+    return dict(hbm=6650.0, tc=1590.0, tc_sustained=1400.0, src="B200_PROFILING.md fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_sample(a_cols_np, reps=1):
+    """Time the oracle (as it stands) on host cores: oracle.qr.rgs on an m x n_s sample."""
+    from oracle.qr import rgs
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        rgs(a_cols_np.astype(np.float64))
+    dt = (time.perf_counter() - t0) / reps
+    return dt
+
+
+def run_reference(args, wl):
+    """--impl reference: the CPU FP64 oracle timed on this box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import workloads as W
+    m, n_s = wl["m"], min(wl["n"], args.cpu_sample_cols)
+    a = W.gaussian(m, n_s, seed=wl["seed"])
+    cores = len(os.sched_getaffinity(0))
+    for _ in range(args.warmup):
+        cpu_oracle_sample(a)
+    ts = [cpu_oracle_sample(a) for _ in range(args.steps)]
+    t = sum(ts) / len(ts)
+    v = conv_flops(m, n_s) / t / 1e12
+    sample = f"oracle.qr.rgs (FP64 numpy) on the first {n_s} columns of the {m}x{wl['n']} workload"
+    line = {
+        "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": wl["name"] + f" [CPU sample {m}x{n_s}]", "m": m, "n": n_s},
+        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-sample-cols", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-lls", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--cutoff", type=int, default=128)
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1912_05508_b200 as tq
+    import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        tq.init_distributed()
+    else:
+        tq.init(local)
+    tq.set_config(cutoff=args.cutoff)
+    dev = torch.device("cuda", local)
+    M, n = wl["m"], wl["n"]
+    rows = np.array_split(np.arange(M), world)[rank]
+    r0, r1 = int(rows[0]), int(rows[-1]) + 1
+    m = r1 - r0
+    Afull = W.gaussian_cuda(M, n, wl["seed"], device=dev)           # same A on every rank
+    A = torch.empty((n, m), dtype=torch.float32, device=dev).t()
+    A.copy_(Afull[r0:r1])
+    del Afull
+    torch.cuda.empty_cache()
+    Q = tq.colmajor_empty(m, n, device=dev)
+    R = tq.colmajor_empty(n, n, device=dev)
+    tq.reserve_workspace(m, n, op=0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        tq.factor(A, Q, R)
+    torch.cuda.synchronize()
+    launches_per_step = tq.last_launch_count()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            tq.factor(A, Q, R)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = conv_flops(M, n) / (ms * 1e-3) / 1e12
+
+    # ---- sampled parity at full size (oracle on the leading 256 columns: R11 of A = QR) ----
+    parity = None
+    if rank == 0 and world == 1:
+        from oracle.qr import rgs
+        from oracle.metrics import r_rel_error
+        k = 256
+        a_lead = A[:, :k].cpu().numpy().astype(np.float64)
+        _, r_o = rgs(a_lead)
+        r_lead = R[:k, :k].cpu().numpy().astype(np.float64)
+        q_lead = Q[:, :k].cpu().numpy().astype(np.float64)
+        parity = {"R_lead256_rel_err_vs_oracle": r_rel_error(r_lead, r_o),
+                  "Q_lead256_orthogonality_f": float(np.linalg.norm(q_lead.T @ q_lead - np.eye(k))
+                                                     / np.sqrt(k))}
+        # full-size invariants on the device in FP64 (harness arithmetic, not the method)
+        Rd = R.to(torch.float64)
+        res = 0.0
+        nrm = 0.0
+        for c0 in range(0, n, 2048):
+            c1 = min(n, c0 + 2048)   # R is upper triangular: only Q[:, :c1] contributes
+            blk = A[:, c0:c1].to(torch.float64) - Q[:, :c1].to(torch.float64) @ Rd[:c1, c0:c1]
+            res += float(torch.linalg.norm(blk) ** 2)
+            nrm += float(torch.linalg.norm(A[:, c0:c1].to(torch.float64)) ** 2)
+            del blk
+        parity["backward_error_f"] = (res / nrm) ** 0.5
+        Qd = Q.to(torch.float64)
+        parity["orthogonality_f"] = float(torch.linalg.norm(Qd.T @ Qd - torch.eye(n, device=dev,
+                                          dtype=torch.float64)) / n ** 0.5)
+        del Qd, Rd
+        torch.cuda.empty_cache()
+
+    # ---- per-kernel-class profile pass (CUDA events around every launch, same stream) ----
+    peaks = load_peaks()
+    roofline, classes = None, None
+    if not args.no_profile:
+        tq.profile_enable(True)
+        tq.factor(A, Q, R)
+        classes = tq.profile_read()
+        tq.profile_enable(False)
+        tot = sum(c["ms"] for c in classes.values()) or 1.0
+        dom = max(classes, key=lambda k: classes[k]["ms"])
+        c = classes[dom]
+        per_launch_ms = c["ms"] / max(c["launches"], 1)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
+        if dom in ("k3_tn", "k4_nn"):
+            ach = c["flops"] / (c["ms"] * 1e-3) / 1e12
+            roofline = {"bound": "tensor", "achieved": ach, "peak": peaks["tc_sustained"],
+                        "unit": "TFLOP/s", "frac": ach / peaks["tc_sustained"], "traffic": traffic}
+        else:
+            ach = c["bytes"] / (c["ms"] * 1e-3) / 1e9
+            roofline = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s",
+                        "frac": ach / peaks["hbm"], "traffic": traffic}
+        roofline.update({"kernel": dom, "share_of_step": c["ms"] / tot,
+                         "launches_per_step": c["launches"], "ms_per_launch": per_launch_ms,
+                         "peak_source": peaks["src"] + (" bf16 sustained (fp16 dense = bf16 rate)"
+                                                        if dom in ("k3_tn", "k4_nn") else " hbm_gbs")})
+        classes = {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
+                       "share": round(v["ms"] / tot, 4),
+                       "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 2),
+                       "gbs": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)}
+                   for k, v in classes.items() if v["launches"]}
+
+    # ---- e2e: the same factorization through the host-pointer C ABI (H2D A, D2H Q and R) ----
+    e2e = None
+    if not args.no_e2e:
+        a_host = torch.empty((n, m), dtype=torch.float32, pin_memory=True)
+        a_host.copy_(A.t())
+        a_np = a_host.numpy().T           # column-major view of the pinned buffer
+        q_host = torch.empty((n, m), dtype=torch.float32, pin_memory=True).numpy().T
+        r_host = torch.empty((n, n), dtype=torch.float32, pin_memory=True).numpy().T
+        import ctypes
+        L = tq.lib()
+        P = ctypes.c_void_p
+        steps_e2e = max(1, min(args.steps, 3))
+        rc = L.tcqr_factor_host(m, n, a_np.ctypes.data_as(P), m, q_host.ctypes.data_as(P),
+                                r_host.ctypes.data_as(P))
+        assert rc == 0, rc
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(steps_e2e):
+            rc = L.tcqr_factor_host(m, n, a_np.ctypes.data_as(P), m, q_host.ctypes.data_as(P),
+                                    r_host.ctypes.data_as(P))
+            assert rc == 0, rc
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1) / steps_e2e
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ems = float(te.item())
+        e2e = {"value": conv_flops(M, n) / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": ems, "h2d_bytes_per_step": 4 * m * n,
+               "d2h_bytes_per_step": 4 * m * n + 4 * n * n,
+               "api": "tcqr_factor_host (pinned host A, Q, R)"}
+        del a_host
+
+    # ---- LLS time-to-FP64 accuracy (configs[3]: 32768x8192 geometric kappa=1e4) ----
+    lls = None
+    if not args.no_lls and args.workload == "cfg3":
+        del Q, R
+        torch.cuda.empty_cache()
+        Ml, nl = 32768, 8192
+        Al_full = W.spectrum_cuda(Ml, nl, "geometric", 1e4, W.CONFIG_SEEDS["cfg4_k1e4"], device=dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(W.CONFIG_SEEDS["cfg4_x_k1e4"])
+        x_true = torch.randn(nl, generator=g, device=dev, dtype=torch.float64)
+        b_full = Al_full.to(torch.float64) @ x_true
+        lrows = np.array_split(np.arange(Ml), world)[rank]
+        l0, l1 = int(lrows[0]), int(lrows[-1]) + 1
+        Al = torch.empty((nl, l1 - l0), dtype=torch.float32, device=dev).t()
+        Al.copy_(Al_full[l0:l1])
+        bl = b_full[l0:l1].contiguous()
+        del Al_full, b_full
+        torch.cuda.empty_cache()
+        barrier()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        x, info = tq.lls_solve(Al, bl, tol=1e-10, maxit=4000)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        lms = h0.elapsed_time(h1)
+        xe = float(torch.linalg.norm(x - x_true) / torch.linalg.norm(x_true))
+        lls = {"workload": "LLS 32768x8192 geometric kappa=1e4, b = A x_true (BASELINE configs[3])",
+               "time_to_solution_ms": lms, "qr_ms": info["qr_ms"], "cgls_ms": info["cgls_ms"],
+               "iterations": info["iterations"], "iterations_pass1": info["iterations_pass1"],
+               "converged": bool(info["converged"]), "x_rel_err_vs_x_true": xe,
+               "fp64_accuracy_reached": bool(xe <= 1e-10)}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_s = min(n, args.cpu_sample_cols)
+        a_s = W.gaussian(M, n_s, seed=wl["seed"])   # same distribution, host generator
+        dt = cpu_oracle_sample(a_s)
+        cpu = {"value": conv_flops(M, n_s) / dt / 1e12, "unit": "TFLOP/s",
+               "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+               "sample": f"oracle.qr.rgs (FP64 numpy/OpenBLAS) on a {M}x{n_s} Gaussian "
+                         f"(first {n_s} columns of the workload shape), {dt:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f16xf32", "data": "synthetic",
+            "config": {"workload": wl["name"], "M": M, "n": n, "local_rows": m,
+                       "cutoff": args.cutoff, "panel_rows": 256,
+                       "flops_convention": "2Mn^2-2/3n^3",
+                       "l2": "inputs larger than L2 (A 2 GiB fp32 per step; no flush needed)",
+                       "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU",
+                       "timing": "CUDA events on the caller stream around K tcqr_factor calls "
+                                 "(graph replay), max over ranks"},
+            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches_per_step": launches_per_step,
+            "clocks": clk.summary(),
+            "roofline": roofline,
+            "kernel_classes": classes,
+            "parity": parity,
+            "e2e": e2e,
+            "lls": lls,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,33 @@ int tcqr_trinv(int64_t n, const float* R, int64_t ldr, double* Minv, int64_t ldm
 int tcqr_gemv(int trans, int64_t m, int64_t n, const float* A, int64_t lda, const double* v,
               double* y);
 
+/* ---------------------------------------------------------------------------------------------
+ * Profiling: per-kernel-class device time (CUDA events recorded on the launching stream around
+ * every launch group) with the ALGORITHMIC flops and bytes of each launch.
+ * While enabled, CUDA-graph replay is bypassed.  tcqr_profile_enable clears the accumulators;
+ * tcqr_profile_read synchronizes and returns the totals for one class.
+ * ------------------------------------------------------------------------------------------- */
+enum {
+  TCQR_COPY = 0,        /* input validation + copy A -> working Q                 */
+  TCQR_K1_CAST = 1,     /* K1 FP16 range guard + cast (A2 and final Q columns)    */
+  TCQR_K3_TN = 2,       /* K3 tcgen05 R12 = Q1' A2 (split-K + reduction)          */
+  TCQR_K3_FINALIZE = 3, /* R12 -> R, scaled FP16 copy of R12                       */
+  TCQR_K4_NN = 4,       /* K4 tcgen05 A2 -= Q1 R12                                 */
+  TCQR_K2_MGS = 5,      /* K2 CAQR level: Alg. 4 MGS on every row block            */
+  TCQR_K2_APPLY = 6,    /* K2 Eq. (6) step 4: Q_b <- Q_b Q_red[b]                  */
+  TCQR_K2B_TN = 7,      /* FP32 R12 below the cutoff                               */
+  TCQR_K2B_NN = 8,      /* FP32 update below the cutoff                            */
+  TCQR_K5_GEMV = 9,     /* CGLS A t and A' r                                       */
+  TCQR_K6_TRI = 10,     /* CGLS inv(R) p and inv(R') v                             */
+  TCQR_K7_SCALAR = 11,  /* CGLS scalar / vector recurrences                        */
+  TCQR_TRINV = 12,      /* one-time explicit inverse of R                          */
+  TCQR_NUM_CLASSES = 13
+};
+int tcqr_profile_enable(int on);
+int tcqr_profile_read(int cls, double* ms, double* flops, double* bytes, int* launches);
+/* Kernels launched by the most recent graph-replayed tcqr_factor (kernel nodes of its graph). */
+int tcqr_last_launch_count(void);
+
 /* Library build/version string. */
 const char* tcqr_version(void);
 

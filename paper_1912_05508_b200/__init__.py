@@ -69,7 +69,15 @@ _SIGS = {
     "tcqr_trinv": (ctypes.c_int, [_I64, _P, _I64, _P, _I64]),
     "tcqr_gemv": (ctypes.c_int, [ctypes.c_int, _I64, _I64, _P, _I64, _P, _P]),
     "tcqr_version": (ctypes.c_char_p, []),
+    "tcqr_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "tcqr_profile_read": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_int)]),
+    "tcqr_last_launch_count": (ctypes.c_int, []),
 }
+PROFILE_CLASSES = ["copy", "k1_cast", "k3_tn", "k3_finalize", "k4_nn", "k2_mgs", "k2_apply",
+                   "k2b_tn", "k2b_nn", "k5_gemv", "k6_tri", "k7_scalar", "trinv"]
 EXPORTS = tuple(_SIGS)
 
 
@@ -331,6 +339,26 @@ def gemv(A, v, trans=False):
     y = torch.empty(n if trans else m, dtype=torch.float64, device=A.device)
     _check("tcqr_gemv", lib().tcqr_gemv(int(trans), m, n, _ptr(A), _ld(A), _ptr(v), _ptr(y)))
     return y
+
+
+def profile_enable(on=True):
+    _ensure()
+    _check("tcqr_profile_enable", lib().tcqr_profile_enable(int(on)))
+
+
+def profile_read():
+    """{class: {ms, flops, bytes, launches}} accumulated since profile_enable()."""
+    out = {}
+    for i, name in enumerate(PROFILE_CLASSES):
+        ms, fl, by, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        _check("tcqr_profile_read", lib().tcqr_profile_read(
+            i, ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(by), ctypes.byref(n)))
+        out[name] = {"ms": ms.value, "flops": fl.value, "bytes": by.value, "launches": n.value}
+    return out
+
+
+def last_launch_count():
+    return lib().tcqr_last_launch_count()
 
 
 def version():

@@ -51,6 +51,7 @@ static NcclApi g_nccl;
 
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
+  int kernels = 0;  // kernel nodes captured (= kernels launched per replay)
 };
 
 struct Context {
@@ -261,6 +262,65 @@ static int allreduce_max_i32(int* buf) {
   } while (0)
 
 // ------------------------------------------------------------------------------------------
+// Per-kernel-class profiling: CUDA events around every launch group on the launching stream,
+// with the algorithmic flops / bytes of that launch.  Graph replay is bypassed
+// while profiling is on.
+// ------------------------------------------------------------------------------------------
+struct ProfAcc {
+  double ms = 0, flops = 0, bytes = 0;
+  int launches = 0;
+};
+struct PendingEv {
+  int cls;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+static bool g_prof = false;
+static ProfAcc g_acc[TCQR_NUM_CLASSES];
+static std::vector<PendingEv> g_pend;
+static std::vector<cudaEvent_t> g_evpool;
+static int g_last_launches = 0;
+
+static cudaEvent_t prof_ev() {
+  if (!g_evpool.empty()) {
+    cudaEvent_t e = g_evpool.back();
+    g_evpool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+static void prof_drain() {
+  if (g_pend.empty()) return;
+  cudaStreamSynchronize(g_ctx.stream);
+  for (auto& p : g_pend) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    ProfAcc& a = g_acc[p.cls];
+    a.ms += ms;
+    a.flops += p.flops;
+    a.bytes += p.bytes;
+    a.launches += 1;
+    g_evpool.push_back(p.a);
+    g_evpool.push_back(p.b);
+  }
+  g_pend.clear();
+}
+#define PROF(cls, fl, by, stmt)                                      \
+  do {                                                               \
+    if (g_prof) {                                                    \
+      cudaEvent_t _a = prof_ev(), _b = prof_ev();                    \
+      cudaEventRecord(_a, c.stream);                                 \
+      stmt;                                                          \
+      cudaEventRecord(_b, c.stream);                                 \
+      g_pend.push_back({(cls), _a, _b, (double)(fl), (double)(by)}); \
+    } else {                                                         \
+      stmt;                                                          \
+    }                                                                \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
 // Panel: Eq. (6) tree on X (rows x w, ldx); top-level R -> Rout (ldr).
 // stack_off: running offset into ws.stack (each tree level takes nb*w*w floats).
 // ------------------------------------------------------------------------------------------
@@ -270,8 +330,9 @@ static int caqr_rec(FactorWs& ws, long long& stack_off, int rows, int w, float* 
   const int br = c.cfg.panel_rows;
   const int nb = panel_num_blocks(rows, br, w);
   if (nb == 1) {
-    CK(panel_mgs_level(rows, w, X, ldx, br, 1, nullptr, 0, Rout, ldr, top ? 1 : 0, c.d_status,
-                       col0, c.stream));
+    PROF(TCQR_K2_MGS, 2.0 * rows * w * w, 8.0 * rows * w,
+         CK(panel_mgs_level(rows, w, X, ldx, br, 1, nullptr, 0, Rout, ldr, top ? 1 : 0,
+                            c.d_status, col0, c.stream)));
     return 0;
   }
   const long long need = (long long)nb * w * w;
@@ -279,9 +340,12 @@ static int caqr_rec(FactorWs& ws, long long& stack_off, int rows, int w, float* 
   float* S = ws.stack + stack_off;
   stack_off += need;
   const long long lds = (long long)nb * w;
-  CK(panel_mgs_level(rows, w, X, ldx, br, nb, S, lds, nullptr, 0, 0, c.d_status, col0, c.stream));
+  PROF(TCQR_K2_MGS, 2.0 * rows * w * w, 8.0 * rows * w,
+       CK(panel_mgs_level(rows, w, X, ldx, br, nb, S, lds, nullptr, 0, 0, c.d_status, col0,
+                          c.stream)));
   CKR(caqr_rec(ws, stack_off, nb * w, w, S, lds, Rout, ldr, top, col0));
-  CK(panel_apply(rows, w, X, ldx, br, nb, S, lds, c.stream));
+  PROF(TCQR_K2_APPLY, 2.0 * rows * w * w, 8.0 * rows * w,
+       CK(panel_apply(rows, w, X, ldx, br, nb, S, lds, c.stream)));
   return 0;
 }
 
@@ -337,30 +401,38 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
       // Alg. 2 line 8 on tensor cores: K1 cast of A2, K3 split-K TN, [allreduce], finalize.
       __half* A1h = ws.Qh + (long long)c0 * ws.ldh;
       __half* A2h = ws.Qh + (long long)(c0 + h) * ws.ldh;
-      CK(cast_scale(m, w2, A2, J.ldq, A2h, ws.ldh, ws.inv_s + c0 + h, c.cfg.col_scaling,
-                    c.d_status, c0 + h, c.stream));
-      CK(tc_gemm_tn(m, h, w2, A1h, ws.ldh, A2h, ws.ldh, ws.T, h, ws.inv_s + c0 + h, ws.P,
-                    ws.p_cap, c.num_sms, c.stream));
+      PROF(TCQR_K1_CAST, 0, 6.0 * m * w2,
+           CK(cast_scale(m, w2, A2, J.ldq, A2h, ws.ldh, ws.inv_s + c0 + h, c.cfg.col_scaling,
+                         c.d_status, c0 + h, c.stream)));
+      PROF(TCQR_K3_TN, 2.0 * m * h * w2, 2.0 * m * (h + w2) + 4.0 * h * w2,
+           CK(tc_gemm_tn(m, h, w2, A1h, ws.ldh, A2h, ws.ldh, ws.T, h, ws.inv_s + c0 + h, ws.P,
+                         ws.p_cap, c.num_sms, c.stream)));
       CKR(allreduce_f32(ws.T, (size_t)h * w2));
       const long long ldh2 = round_up(h, 8);
-      CK(r12_finalize(h, w2, ws.T, h, Rblk, J.ldr, ws.R12h, ldh2, ws.inv_s2 + c0 + h,
-                      c.cfg.col_scaling, c.stream));
+      PROF(TCQR_K3_FINALIZE, 0, 10.0 * h * w2,
+           CK(r12_finalize(h, w2, ws.T, h, Rblk, J.ldr, ws.R12h, ldh2, ws.inv_s2 + c0 + h,
+                           c.cfg.col_scaling, c.stream)));
       // Alg. 2 line 9 argument on tensor cores: K4.
-      CK(tc_gemm_nn_update(m, h, w2, A1h, ws.ldh, ws.R12h, ldh2, A2, J.ldq, ws.inv_s2 + c0 + h,
-                           c.num_sms, c.stream));
+      PROF(TCQR_K4_NN, 2.0 * m * h * w2, 2.0 * m * h + 2.0 * h * w2 + 8.0 * m * w2,
+           CK(tc_gemm_nn_update(m, h, w2, A1h, ws.ldh, ws.R12h, ldh2, A2, J.ldq,
+                                ws.inv_s2 + c0 + h, c.num_sms, c.stream)));
     } else {
-      CK(f32_tn(m, h, w2, Qc, J.ldq, A2, J.ldq, ws.T, ws.P, ws.p_cap, c.num_sms, c.stream));
+      PROF(TCQR_K2B_TN, 2.0 * m * h * w2, 4.0 * m * (h + w2),
+           CK(f32_tn(m, h, w2, Qc, J.ldq, A2, J.ldq, ws.T, ws.P, ws.p_cap, c.num_sms,
+                     c.stream)));
       CKR(allreduce_f32(ws.T, (size_t)h * w2));
-      CK(copy_block(h, w2, ws.T, h, Rblk, J.ldr, c.stream));
-      CK(f32_nn_update(m, h, w2, Qc, J.ldq, ws.T, A2, J.ldq, c.stream));
+      PROF(TCQR_K3_FINALIZE, 0, 8.0 * h * w2, CK(copy_block(h, w2, ws.T, h, Rblk, J.ldr, c.stream)));
+      PROF(TCQR_K2B_NN, 2.0 * m * h * w2, 4.0 * m * h + 8.0 * m * w2,
+           CK(f32_nn_update(m, h, w2, Qc, J.ldq, ws.T, A2, J.ldq, c.stream)));
     }
     CKR(rgs(J, c0 + h, w2, need_h));  // Alg. 2 line 9
     return 0;
   }
   if (need_h) {
     // Q columns of this panel are final: emit their FP16 shadow for the GEMMs above.
-    CK(cast_scale(m, w, Qc, J.ldq, ws.Qh + (long long)c0 * ws.ldh, ws.ldh, nullptr, 0, nullptr, 0,
-                  c.stream));
+    PROF(TCQR_K1_CAST, 0, 6.0 * m * w,
+         CK(cast_scale(m, w, Qc, J.ldq, ws.Qh + (long long)c0 * ws.ldh, ws.ldh, nullptr, 0,
+                       nullptr, 0, c.stream)));
   }
   return 0;
 }
@@ -371,7 +443,7 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
   Context& c = g_ctx;
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));  // INT_MAX-ish = OK
   CK(cudaMemsetAsync(R, 0, sizeof(float) * (size_t)n * n, c.stream));
-  CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream));
+  PROF(TCQR_COPY, 0, 8.0 * m * n, CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream)));
   FactorJob J{m, n, Q, (long long)m, R, (long long)n, &ws};
   const bool need_h = n > c.cfg.cutoff;
   CKR(rgs(J, 0, n, need_h));
@@ -405,7 +477,7 @@ static std::string graph_key(const char* tag, std::initializer_list<long long> v
 static int run_factor(int m, int n, const float* A, long long lda, float* Q, float* R,
                       FactorWs& ws, const void* ws_base) {
   Context& c = g_ctx;
-  if (!c.cfg.use_graphs) return enqueue_factor(m, n, A, lda, Q, R, ws);
+  if (!c.cfg.use_graphs || g_prof) return enqueue_factor(m, n, A, lda, Q, R, ws);
   const std::string key =
       graph_key("f", {m, n, lda, (long long)A, (long long)Q, (long long)R, (long long)ws_base});
   auto it = c.graphs.find(key);
@@ -420,12 +492,22 @@ static int run_factor(int m, int n, const float* A, long long lda, float* Q, flo
     }
     CK(e);
     GraphEntry ge;
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+    ge.kernels = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++ge.kernels;
+    }
     e = cudaGraphInstantiate(&ge.exec, g, 0);
     cudaGraphDestroy(g);
     CK(e);
     it = c.graphs.emplace(key, ge).first;
   }
   CK(cudaGraphLaunch(it->second.exec, c.stream));
+  g_last_launches = it->second.kernels;
   return 0;
 }
 
@@ -607,15 +689,22 @@ static int lls_pass(LlsWs& w, int m, int n, const float* A, long long lda, doubl
   while (true) {
     const int chunk = 8;
     for (int i = 0; i < chunk; ++i) {
-      CK(cg_launch_tri_n(n, w.M, n, w.p, w.t, w.part, done, c.stream));               // t = inv(R) p
-      CK(cg_launch_a_n(m, n, A, lda, w.t, w.q, w.part, w.dpart, done, c.stream));      // q = A t
-      CK(cg_launch_sum_parts(ndp, w.dpart, &w.st->delta, done, c.stream));             // delta
+      const double tri = 4.0 * (double)n * (n + 1);  // FP64 upper triangle, one pass
+      PROF(TCQR_K6_TRI, (double)n * n, tri,
+           CK(cg_launch_tri_n(n, w.M, n, w.p, w.t, w.part, done, c.stream)));   // t = inv(R) p
+      PROF(TCQR_K5_GEMV, 2.0 * m * n, 4.0 * m * n + 8.0 * m,
+           CK(cg_launch_a_n(m, n, A, lda, w.t, w.q, w.part, w.dpart, done, c.stream)));  // q = A t
+      PROF(TCQR_K7_SCALAR, 0, 0, CK(cg_launch_sum_parts(ndp, w.dpart, &w.st->delta, done, c.stream)));
       CKR(allreduce_f64(&w.st->delta, 1));
-      CK(cg_launch_update_xr(m, n, w.st, w.x, w.t, w.r, w.q, c.stream));               // x, r
-      CK(cg_launch_a_t(m, n, A, lda, w.r, w.v, done, c.stream));                       // A' r
+      PROF(TCQR_K7_SCALAR, 2.0 * (m + n), 24.0 * (m + n),
+           CK(cg_launch_update_xr(m, n, w.st, w.x, w.t, w.r, w.q, c.stream)));  // x, r
+      PROF(TCQR_K5_GEMV, 2.0 * m * n, 4.0 * m * n + 8.0 * m,
+           CK(cg_launch_a_t(m, n, A, lda, w.r, w.v, done, c.stream)));          // A' r
       CKR(allreduce_f64(w.v, n));
-      CK(cg_launch_tri_t(n, w.M, n, w.v, w.s, done, c.stream));                        // s
-      CK(cg_launch_finish(n, w.st, w.s, w.p, w.x, w.xbest, w.hist, c.stream));          // beta, p
+      PROF(TCQR_K6_TRI, (double)n * n, tri,
+           CK(cg_launch_tri_t(n, w.M, n, w.v, w.s, done, c.stream)));           // s
+      PROF(TCQR_K7_SCALAR, 4.0 * n, 40.0 * n,
+           CK(cg_launch_finish(n, w.st, w.s, w.p, w.x, w.xbest, w.hist, c.stream)));  // beta, p
     }
     launched += chunk;
     CK(cudaMemcpyAsync(&hs, w.st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
@@ -667,7 +756,8 @@ int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const doub
   }
   cudaEventRecord(e1, c.stream);
   // K6 set-up: M = inv(R) in FP64 (reading R-A13).
-  CK(trinv_f64((int)n, w.R, n, w.M, n, w.W, c.num_sms, c.stream));
+  PROF(TCQR_TRINV, (double)n * n * n / 3.0, 12.0 * n * n,
+       CK(trinv_f64((int)n, w.R, n, w.M, n, w.W, c.num_sms, c.stream)));
   // pass 1: r = b, x = 0
   CK(cudaMemcpyAsync(w.r, b, sizeof(double) * m, cudaMemcpyDeviceToDevice, c.stream));
   int it1 = 0, reason1 = 0, it2 = 0, reason2 = -1;
@@ -873,6 +963,30 @@ int tcqr_trinv(int64_t n, const float* R, int64_t ldr, double* Minv, int64_t ldm
   CK(cudaStreamSynchronize(c.stream));
   return 0;
 }
+
+int tcqr_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  prof_drain();
+  for (auto& a : g_acc) a = ProfAcc();
+  g_prof = on != 0;
+  return 0;
+}
+
+int tcqr_profile_read(int cls, double* ms, double* flops, double* bytes, int* launches) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (cls < 0 || cls >= TCQR_NUM_CLASSES) return -1;
+  prof_drain();
+  const ProfAcc& a = g_acc[cls];
+  if (ms) *ms = a.ms;
+  if (flops) *flops = a.flops;
+  if (bytes) *bytes = a.bytes;
+  if (launches) *launches = a.launches;
+  return 0;
+}
+
+int tcqr_last_launch_count(void) { return g_last_launches; }
 
 int tcqr_gemv(int trans, int64_t m, int64_t n, const float* A, int64_t lda, const double* v,
               double* y) {

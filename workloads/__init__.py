@@ -152,3 +152,35 @@ def make_matrix(kind: str, m: int, n: int, seed: int, cond: float = 1.0) -> np.n
     if kind == "uniform_sym":
         return uniform_sym(m, n, seed)
     return spectrum_matrix(m, n, kind, cond, seed)
+
+
+# ------------------------------------------------------------------------------------------
+# Device-side generators for the full-size bench workloads (same distributions; torch's Philox
+# generator seeded per call; torch.linalg is a library primitive of the GENERATOR only).
+# ------------------------------------------------------------------------------------------
+def gaussian_cuda(m: int, n: int, seed: int, device="cuda"):
+    """i.i.d. N(0,1) float32, column-major (shape (m, n), stride (1, m)), on `device`."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return torch.randn((n, m), generator=g, device=device, dtype=torch.float32).t()
+
+
+def spectrum_cuda(m: int, n: int, kind: str, cond: float, seed: int, device="cuda"):
+    """A = U diag(sigma) V^T (float32, column-major) with Haar U, V drawn on the device."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    u = torch.randn((m, n), generator=g, device=device, dtype=torch.float64)
+    u, ru = torch.linalg.qr(u)
+    u *= torch.sign(torch.diagonal(ru))
+    del ru
+    v = torch.randn((n, n), generator=g, device=device, dtype=torch.float64)
+    v, rv = torch.linalg.qr(v)
+    v *= torch.sign(torch.diagonal(rv))
+    s = torch.from_numpy(spectrum_values(n, kind, cond)).to(device)
+    a = (u * s) @ v.T
+    del u, v
+    out = torch.empty((n, m), device=device, dtype=torch.float32).t()
+    out.copy_(a)
+    return out
