@@ -6,54 +6,69 @@
 
 namespace tcqr {
 
-constexpr int kF32Chunk = 32;
+constexpr int kTnRows = 64;   // rows per shared-memory chunk
+constexpr int kTnPad = 68;    // row stride (floats) of the staged tiles, 16-byte aligned
 
 // P_s (h x w2, ld h) = sum over rows [r0_s, r1_s) of Q1(r, :)' A2(r, :).  h, w2 <= 64.
+// 256 threads = 4 row groups x (8 x 8 threads) each owning an 8 x 8 output micro-tile.
 __global__ void __launch_bounds__(256) f32_tn_kernel(int m, int h, int w2,
                                                      const float* __restrict__ Q1, long long ldq,
                                                      const float* __restrict__ A2, long long lda,
                                                      float* __restrict__ P, int splits) {
-  __shared__ float Qs[kF32Chunk][65];
-  __shared__ float As[kF32Chunk][65];
+  __shared__ __align__(16) float Qs[kTnRows][kTnPad];
+  __shared__ __align__(16) float As[kTnRows][kTnPad];
   const int s = blockIdx.x;
   const long long r0 = (long long)s * m / splits, r1 = (long long)(s + 1) * m / splits;
-  const int tid = threadIdx.x, ti = tid & 15, tj = tid >> 4;
-  float acc[4][4];
+  const int tid = threadIdx.x, grp = tid >> 6, t = tid & 63, ti = t & 7, tj = t >> 3;
+  float acc[8][8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-  for (long long c0 = r0; c0 < r1; c0 += kF32Chunk) {
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+  for (long long c0 = r0; c0 < r1; c0 += kTnRows) {
     __syncthreads();
-    for (int e = tid; e < kF32Chunk * 64; e += 256) {
-      const int rr = e & (kF32Chunk - 1), cc = e / kF32Chunk;
+    for (int e = tid; e < kTnRows * 64; e += 256) {
+      const int rr = e & (kTnRows - 1), cc = e / kTnRows;
       const long long row = c0 + rr;
       const bool rok = row < r1;
       Qs[rr][cc] = (rok && cc < h) ? Q1[row + cc * ldq] : 0.f;
       As[rr][cc] = (rok && cc < w2) ? A2[row + cc * lda] : 0.f;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int rr = 0; rr < kF32Chunk; ++rr) {
-      float qv[4], av[4];
+#pragma unroll 4
+    for (int rr = grp; rr < kTnRows; rr += 4) {
+      const float4 q0 = *reinterpret_cast<const float4*>(&Qs[rr][ti * 8]);
+      const float4 q1 = *reinterpret_cast<const float4*>(&Qs[rr][ti * 8 + 4]);
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[rr][tj * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[rr][tj * 8 + 4]);
+      const float qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
-      for (int a = 0; a < 4; ++a) qv[a] = Qs[rr][ti * 4 + a];
+      for (int a = 0; a < 8; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) av[b] = As[rr][tj * 4 + b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(qv[a], av[b], acc[a][b]);
+        for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(qv[a], av[b], acc[a][b]);
     }
   }
-  float* out = P + (long long)s * h * w2;
+  // combine the 4 row groups in a fixed order (deterministic)
+  __syncthreads();
+  float* red = &Qs[0][0];  // 64 x 64 floats fit in Qs (64 x 68)
+  for (int g = 0; g < 4; ++g) {
+    if (grp == g) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = ti * 4 + a, j = tj * 4 + b;
-      if (i < h && j < w2) out[i + (long long)j * h] = acc[a][b];
+        for (int b = 0; b < 8; ++b) {
+          float* p = red + (ti * 8 + a) * kTnPad + tj * 8 + b;
+          *p = (g == 0) ? acc[a][b] : *p + acc[a][b];
+        }
     }
+    __syncthreads();
+  }
+  float* out = P + (long long)s * h * w2;
+  for (int e = tid; e < h * w2; e += 256) {
+    const int i = e % h, j = e / h;
+    out[i + (long long)j * h] = red[i * kTnPad + j];
+  }
 }
 
 __global__ void f32_reduce_kernel(const float* __restrict__ P, int splits, int hw,
@@ -71,7 +86,7 @@ cudaError_t f32_tn(int m, int h, int w2, const float* Q1, long long ldq, const f
   if (h > 64 || w2 > 64) return cudaErrorInvalidValue;
   const int hw = h * w2;
   int splits = (m + 255) / 256;
-  if (splits > 2 * num_sms) splits = 2 * num_sms;
+  if (splits > num_sms) splits = num_sms;
   if ((long long)splits * hw > p_cap) splits = (int)(p_cap / hw);
   if (splits < 1) splits = 1;
   if (splits == 1) {
@@ -85,41 +100,50 @@ cudaError_t f32_tn(int m, int h, int w2, const float* Q1, long long ldq, const f
   return cudaGetLastError();
 }
 
-// A2 (m x w2) -= Q1 (m x h) T (h x w2, ld h).  grid (row blocks of 256, column groups of 16).
-__global__ void __launch_bounds__(256) f32_nn_kernel(int m, int h, int w2,
+// A2 (m x w2) -= Q1 (m x h) T (h x w2, ld h).  One thread per row, all w2 <= 64 columns.
+template <int W2>
+__global__ void __launch_bounds__(128) f32_nn_kernel(int m, int h, int w2,
                                                      const float* __restrict__ Q1, long long ldq,
                                                      const float* __restrict__ T,
                                                      float* __restrict__ A2, long long lda) {
-  __shared__ float Ts[64][16];
-  const int j0 = blockIdx.y * 16;
-  for (int e = threadIdx.x; e < h * 16; e += 256) {
-    const int i = e / 16, jj = e % 16;
-    Ts[i][jj] = (j0 + jj < w2) ? T[i + (long long)(j0 + jj) * h] : 0.f;
+  __shared__ __align__(16) float Ts[64][W2];
+  for (int e = threadIdx.x; e < h * W2; e += blockDim.x) {
+    const int i = e / W2, j = e % W2;
+    Ts[i][j] = (j < w2) ? T[i + (long long)j * h] : 0.f;
   }
   __syncthreads();
-  const long long row = (long long)blockIdx.x * 256 + threadIdx.x;
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= m) return;
-  float acc[16];
+  float acc[W2];
 #pragma unroll
-  for (int jj = 0; jj < 16; ++jj) acc[jj] = 0.f;
+  for (int j = 0; j < W2; ++j) acc[j] = 0.f;
   for (int i = 0; i < h; ++i) {
     const float q = Q1[row + (long long)i * ldq];
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj) acc[jj] = fmaf(q, Ts[i][jj], acc[jj]);
+    for (int j = 0; j < W2; j += 4) {
+      const float4 tv = *reinterpret_cast<const float4*>(&Ts[i][j]);
+      acc[j] = fmaf(q, tv.x, acc[j]);
+      acc[j + 1] = fmaf(q, tv.y, acc[j + 1]);
+      acc[j + 2] = fmaf(q, tv.z, acc[j + 2]);
+      acc[j + 3] = fmaf(q, tv.w, acc[j + 3]);
+    }
   }
 #pragma unroll
-  for (int jj = 0; jj < 16; ++jj)
-    if (j0 + jj < w2) {
-      float* p = A2 + row + (long long)(j0 + jj) * lda;
-      *p = *p - acc[jj];
+  for (int j = 0; j < W2; ++j)
+    if (j < w2) {
+      float* p = A2 + row + (long long)j * lda;
+      *p = *p - acc[j];
     }
 }
 
 cudaError_t f32_nn_update(int m, int h, int w2, const float* Q1, long long ldq, const float* T,
                           float* A2, long long lda, cudaStream_t st) {
-  if (h > 64) return cudaErrorInvalidValue;
-  dim3 grid((m + 255) / 256, (w2 + 15) / 16);
-  f32_nn_kernel<<<grid, 256, 0, st>>>(m, h, w2, Q1, ldq, T, A2, lda);
+  if (h > 64 || w2 > 64) return cudaErrorInvalidValue;
+  const int grid = (m + 127) / 128;
+  if (w2 <= 32)
+    f32_nn_kernel<32><<<grid, 128, 0, st>>>(m, h, w2, Q1, ldq, T, A2, lda);
+  else
+    f32_nn_kernel<64><<<grid, 128, 0, st>>>(m, h, w2, Q1, ldq, T, A2, lda);
   return cudaGetLastError();
 }
 

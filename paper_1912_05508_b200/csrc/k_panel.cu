@@ -1,24 +1,22 @@
 // k_panel.cu -- K2: the communication-avoiding MGS panel (Eq. (6), Alg. 4).
 //
-// One CAQR level = one launch of panel_mgs_kernel: CTA b owns row block b (br rows; the last
-// block absorbs a remainder shorter than w rows, reading R-A6), keeps it in registers (one or two
-// rows per thread, as the paper's "256 threads ... a single row" design) and
-// runs Alg. 4 on it:
+// Primary path: panel_fused_kernel (below) runs the whole Eq. (6) tree in ONE cooperative launch.
+// Fallback (tree wider than the co-resident grid): one launch of panel_mgs_kernel per level plus
+// panel_apply_kernel.  In both, CTA b owns row block b (br rows; the last block absorbs a
+// remainder shorter than w rows, reading R-A6), keeps it in registers (two rows per thread, the
+// paper's "each thread ... a single row" design) and runs Alg. 4 on it:
 //     for k: R(k,k) = ||q_k||; q_k /= R(k,k); R(k,k+1:) = q_k' Q(:,k+1:); Q(:,k+1:) -= q_k R(k,k+1:)
 // The norm and the w-k dot products of step k are ONE block reduction: each thread forms its
 // partial products, a 31-shuffle transpose-reduce leaves lane j with the warp sum of product j,
 // and a double-buffered shared array combines the warps in a fixed order (deterministic).
 // R(k,j) = (a_k' a_j) / R(k,k) equals q_k' a_j up to rounding order.
-// The stacked R's are factored by the same kernel (step 3); panel_apply_kernel is step 4
-// ("batched SGEMM" in the paper).
+// The stacked R's are factored by the same step (step 3); step 4 ("batched SGEMM" in the paper,
+// PAPER.md:453-455) multiplies each local Q by its slice of the stack's Q.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace tcqr {
 
-constexpr int kPanelThreads = 256;
-constexpr int kPanelWarps = kPanelThreads / 32;
-constexpr int kPanelRPT = 2;  // rows per thread -> up to 512 rows per block (br <= 480 + w)
 
 int panel_num_blocks(int rows, int br, int w) {
   int nb = (rows + br - 1) / br;
@@ -44,95 +42,7 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
   return v[0];
 }
 
-__global__ void __launch_bounds__(kPanelThreads) panel_mgs_kernel(
-    int rows, int w, float* __restrict__ X, long long ldx, int br, int nb, float* __restrict__ S,
-    long long lds, float* __restrict__ Rout, long long ldr, int top, int* status, int col0) {
-  __shared__ float red[2][kPanelWarps][32];
-  const int b = blockIdx.x;
-  const int row0 = b * br;
-  const int nrows = (b == nb - 1) ? rows - row0 : br;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  float x[kPanelRPT][32];
-#pragma unroll
-  for (int r = 0; r < kPanelRPT; ++r) {
-    const int i = tid + r * kPanelThreads;
-    const bool ok = i < nrows;
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      x[r][j] = (ok && j < w) ? X[(long long)(row0 + i) + (long long)j * ldx] : 0.f;
-  }
-  float* Rdst = (nb == 1) ? Rout : S + (long long)b * w;
-  const long long ldR = (nb == 1) ? ldr : lds;
-
-  int buf = 0;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    if (k < w) {
-      float p[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        float acc = 0.f;
-        if (j >= k) {
-#pragma unroll
-          for (int r = 0; r < kPanelRPT; ++r) acc = fmaf(x[r][k], x[r][j], acc);
-        }
-        p[j] = acc;
-      }
-      const float part = transpose_reduce32(p);  // lane j: warp sum of a_k' a_j
-      red[buf][warp][lane] = part;
-      __syncthreads();
-      float tot = 0.f;
-#pragma unroll
-      for (int v = 0; v < kPanelWarps; ++v) tot += red[buf][v][lane];
-      buf ^= 1;
-      const float nrm2 = __shfl_sync(0xffffffffu, tot, k);
-      const float rkk = sqrtf(nrm2);
-      const bool zero = !(rkk > 0.f) || !isfinite(rkk);
-      if (top && zero && tid == 0 && status) atomicMin(status, col0 + k + 1);
-      float rkj = zero ? 0.f : tot / rkk;  // lane j > k: R(k, j)
-      if (lane == k) rkj = zero ? 0.f : rkk;
-      if (lane < k) rkj = 0.f;
-      if (warp == 0 && lane < w) Rdst[k + (long long)lane * ldR] = rkj;
-      float qk[kPanelRPT];
-#pragma unroll
-      for (int r = 0; r < kPanelRPT; ++r) {
-        qk[r] = zero ? 0.f : x[r][k] / rkk;
-        x[r][k] = qk[r];
-      }
-#pragma unroll
-      for (int j = k + 1; j < 32; ++j) {
-        const float rj = __shfl_sync(0xffffffffu, rkj, j);
-#pragma unroll
-        for (int r = 0; r < kPanelRPT; ++r) x[r][j] = fmaf(-qk[r], rj, x[r][j]);
-      }
-    } else if (warp == 0 && k < 32 && lane < w) {
-      // unreachable rows of R beyond w are not stored
-    }
-  }
-  // Zero the strictly-lower part of this R block (rows k > j) so the stack is a proper R.
-  if (warp == 0) {
-    for (int k = 1; k < w; ++k)
-      if (lane < k) Rdst[k + (long long)lane * ldR] = 0.f;
-  }
-#pragma unroll
-  for (int r = 0; r < kPanelRPT; ++r) {
-    const int i = tid + r * kPanelThreads;
-    if (i < nrows) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < w) X[(long long)(row0 + i) + (long long)j * ldx] = x[r][j];
-    }
-  }
-}
-
-cudaError_t panel_mgs_level(int rows, int w, float* X, long long ldx, int br, int nb, float* S,
-                            long long lds, float* Rout, long long ldr, int top, int* status,
-                            int col0, cudaStream_t st) {
-  panel_mgs_kernel<<<nb, kPanelThreads, 0, st>>>(rows, w, X, ldx, br, nb, S, lds, Rout, ldr, top,
-                                                 status, col0);
-  return cudaGetLastError();
-}
+// (panel_mgs_kernel is defined below, after the rotating MGS step it shares.)
 
 // X_b <- X_b * T_b with T_b = S[b*w:(b+1)*w, 0:w] (lds).  grid.x = row chunks of 256 rows.
 __global__ void __launch_bounds__(256) panel_apply_kernel(int rows, int w, float* __restrict__ X,
@@ -190,6 +100,378 @@ cudaError_t panel_apply(int rows, int w, float* X, long long ldx, int br, int nb
   const int grid = (rows + 255) / 256;
   panel_apply_kernel<<<grid, 256, 0, st>>>(rows, w, X, ldx, br, nb, S, lds);
   return cudaGetLastError();
+}
+
+
+// ==========================================================================================
+// Fused single-launch CAQR panel (Eq. (6) steps 1-5 in ONE cooperative kernel).
+//
+// CTA b runs Alg. 4 on row block b (step 1) with a rotating register window: at step k the pivot
+// column is always x[.][0] and the trailing update writes column j into slot j-1, so the loop
+// body has no data-dependent register indexing and is small enough for the instruction cache
+// (the fully unrolled v1 kernel spent 55% of its cycles in no_instructions stalls; ncu,
+// profiles/r01_ncu_panel_mgs_v1_details.csv).  The stacked R's (step 2) are factored (step 3) by
+// the LAST child CTA to finish each tree node (atomic arrival counter), level by level, so no
+// CTA ever waits for another until the root is done.  Then every CTA forms its composite
+// transform T_b = S1[b] S2[parent(b)] ... (step 4) from the stack Q slices and writes its final Q
+// rows (FP32 and the FP16 shadow used by the tensor-core GEMMs above), step 5.
+// Co-residency of all CTAs is guaranteed by the cooperative launch.
+// ==========================================================================================
+constexpr int kFusedThreads = 160;  // 5 warps
+constexpr int kFusedRPT = 2;        // 320 rows per CTA: br <= 288 (br + w - 1 <= 319)
+constexpr int kFusedCap = kFusedThreads * kFusedRPT;
+constexpr int kFusedWarps = kFusedThreads / 32;
+constexpr int kMaxLevels = 8;
+
+struct FusedPanelArgs {
+  float* X;
+  long long ldx;
+  __half* Xh;  // may be null
+  long long ldh;
+  int m, w, br, nb, F, L;       // L = tree levels above the row blocks (0 if nb == 1)
+  int nodes[kMaxLevels + 1];    // nodes[l] = nodes at level l (nodes[0] = nb, nodes[L] = 1)
+  float* Rbuf[kMaxLevels + 1];  // R of every node at level l: nodes[l] * w * w floats
+  float* Qst[kMaxLevels + 1];   // stack-Q slices for the children of level-l nodes (l >= 1)
+  int* cnt[kMaxLevels + 1];     // arrival counters of level-l nodes (l >= 1)
+  int* done;                    // [0] root done flag, [1] exit counter
+  float* Rout;                  // final R (w x w, ldr)
+  long long ldr;
+  int root_is_global;           // 1: a zero/non-finite norm at the root is a breakdown
+  int* status;
+  int col0;
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Alg. 4 on the rows held in x (thread t owns rows t, t + kFusedThreads).  Q columns go to
+// qs[row * 33 + k] (shared), R row k to Rdst[k + j * ldR] (zeros below the diagonal).
+__device__ __forceinline__ void mgs_rotating(float (&x)[kFusedRPT][32], int nrows, int w,
+                                             float* qs, float* Rdst, long long ldR, bool check,
+                                             int* status, int col0, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int buf = 0;
+  for (int k = 0; k < w; ++k) {
+    float p[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float acc = 0.f;
+#pragma unroll
+      for (int r = 0; r < kFusedRPT; ++r) acc = fmaf(x[r][0], x[r][j], acc);
+      p[j] = acc;
+    }
+    const float part = transpose_reduce32(p);  // lane j: warp sum of a_k' a_{k+j}
+    red[(buf * kFusedWarps + warp) * 32 + lane] = part;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int v = 0; v < kFusedWarps; ++v) tot += red[(buf * kFusedWarps + v) * 32 + lane];
+    buf ^= 1;
+    const float rkk = sqrtf(__shfl_sync(0xffffffffu, tot, 0));
+    const bool zero = !(rkk > 0.f) || !isfinite(rkk);
+    if (check && zero && threadIdx.x == 0 && status) atomicMin(status, col0 + k + 1);
+    const float rkj = zero ? 0.f : (lane == 0 ? rkk : tot / rkk);
+    if (warp == 0) {
+      if (lane < w - k) Rdst[k + (long long)(k + lane) * ldR] = rkj;
+      if (lane < k) Rdst[k + (long long)lane * ldR] = 0.f;
+    }
+    float q[kFusedRPT];
+#pragma unroll
+    for (int r = 0; r < kFusedRPT; ++r) {
+      q[r] = zero ? 0.f : x[r][0] / rkk;
+      const int row = threadIdx.x + r * kFusedThreads;
+      if (row < nrows) qs[row * 33 + k] = q[r];
+    }
+#pragma unroll
+    for (int j = 1; j < 32; ++j) {
+      const float rj = __shfl_sync(0xffffffffu, rkj, j);
+#pragma unroll
+      for (int r = 0; r < kFusedRPT; ++r) x[r][j - 1] = fmaf(-q[r], rj, x[r][j]);
+    }
+#pragma unroll
+    for (int r = 0; r < kFusedRPT; ++r) x[r][31] = 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelArgs a) {
+  extern __shared__ float fsm[];
+  float* qA = fsm;                      // level-1 Q_b   [kFusedCap][33]
+  float* qB = qA + kFusedCap * 33;      // stack-level Q [kFusedCap][33]
+  float* T = qB + kFusedCap * 33;       // [32][33]
+  float* T2 = T + 32 * 33;              // [32][33]
+  float* red = T2 + 32 * 33;            // [2][warps][32]
+  __shared__ int s_last;
+  const int b = blockIdx.x, w = a.w;
+  const int row0 = b * a.br;
+  const int nrows = (b == a.nb - 1) ? a.m - row0 : a.br;
+
+  // ---- step 1: Alg. 4 on this row block ----
+  float x[kFusedRPT][32];
+#pragma unroll
+  for (int r = 0; r < kFusedRPT; ++r) {
+    const int i = threadIdx.x + r * kFusedThreads;
+    const bool ok = i < nrows;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      x[r][j] = (ok && j < w) ? a.X[(long long)(row0 + i) + (long long)j * a.ldx] : 0.f;
+  }
+  const bool single = (a.L == 0);
+  float* Rb = single ? a.Rout : a.Rbuf[0] + (long long)b * w * w;
+  mgs_rotating(x, nrows, w, qA, Rb, single ? a.ldr : w, single && a.root_is_global, a.status,
+               a.col0, red);
+
+  // ---- steps 2-3: the last child to arrive factors each tree node ----
+  int node = b;
+  bool root = single;
+  for (int l = 1; l <= a.L; ++l) {
+    __threadfence();
+    __syncthreads();
+    const int parent = node / a.F;
+    const int first = parent * a.F;
+    const int nchild = min(a.F, a.nodes[l - 1] - first);
+    if (threadIdx.x == 0) s_last = (atomicAdd(a.cnt[l] + parent, 1) == nchild - 1);
+    __syncthreads();
+    if (!s_last) break;
+    __threadfence();
+    const int srows = nchild * w;
+    const float* Rc = a.Rbuf[l - 1] + (long long)first * w * w;
+#pragma unroll
+    for (int r = 0; r < kFusedRPT; ++r) {
+      const int s = threadIdx.x + r * kFusedThreads;
+      const bool ok = s < srows;
+      const int ci = ok ? s / w : 0, aa = ok ? s % w : 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        x[r][j] = (ok && j < w) ? __ldcg(Rc + (long long)ci * w * w + aa + (long long)j * w) : 0.f;
+    }
+    const bool top = (l == a.L);
+    float* Rn = top ? a.Rout : a.Rbuf[l] + (long long)parent * w * w;
+    mgs_rotating(x, srows, w, qB, Rn, top ? a.ldr : w, top && a.root_is_global, a.status, a.col0,
+                 red);
+    __syncthreads();
+    float* Qd = a.Qst[l] + (long long)first * w * w;  // slice of child ci at Qd + ci*w*w
+    for (int e = threadIdx.x; e < srows * w; e += kFusedThreads) {
+      const int s = e % srows, j = e / srows;
+      const int ci = s / w, aa = s % w;
+      Qd[(long long)ci * w * w + aa + (long long)j * w] = qB[s * 33 + j];
+    }
+    node = parent;
+    root = top;
+  }
+  if (root && !single) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(a.done, 1);
+  }
+
+  // ---- step 4: T_b = S1[b] S2[b/F] ... ; Q_b <- Q_b T_b ----
+  if (!single) {
+    if (threadIdx.x == 0)
+      while (ld_acquire(a.done) == 0) __nanosleep(64);
+    __syncthreads();
+    int idx = b;
+    for (int e = threadIdx.x; e < 32 * 32; e += kFusedThreads) {
+      const int l_ = e % 32, j = e / 32;
+      T[l_ * 33 + j] = (l_ < w && j < w) ? __ldcg(a.Qst[1] + (long long)idx * w * w + l_ + j * w)
+                                         : 0.f;
+    }
+    for (int l = 2; l <= a.L; ++l) {
+      idx /= a.F;
+      const float* S = a.Qst[l] + (long long)idx * w * w;
+      __syncthreads();
+      for (int e = threadIdx.x; e < 32 * 32; e += kFusedThreads) {
+        const int i = e % 32, j = e / 32;
+        float acc = 0.f;
+        if (i < w && j < w)
+          for (int t = 0; t < w; ++t) acc = fmaf(T[i * 33 + t], __ldcg(S + t + j * w), acc);
+        T2[i * 33 + j] = acc;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < 32 * 32; e += kFusedThreads) {
+        const int i = e % 32, j = e / 32;
+        T[i * 33 + j] = T2[i * 33 + j];
+      }
+    }
+    __syncthreads();
+  } else {
+    for (int e = threadIdx.x; e < 32 * 32; e += kFusedThreads) {
+      const int i = e % 32, j = e / 32;
+      T[i * 33 + j] = (i == j) ? 1.f : 0.f;
+    }
+    __syncthreads();
+  }
+  // ---- step 5: final Q rows (FP32 + FP16 shadow) ----
+  for (int r = 0; r < kFusedRPT; ++r) {
+    const int i = threadIdx.x + r * kFusedThreads;
+    if (i >= nrows) continue;
+    float y[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) y[j] = 0.f;
+    if (single) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) y[j] = qA[i * 33 + j];
+    } else {
+      for (int l_ = 0; l_ < w; ++l_) {
+        const float ql = qA[i * 33 + l_];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) y[j] = fmaf(ql, T[l_ * 33 + j], y[j]);
+      }
+    }
+    const long long gi = (long long)(row0 + i);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < w) {
+        a.X[gi + (long long)j * a.ldx] = y[j];
+        if (a.Xh) a.Xh[gi + (long long)j * a.ldh] = __float2half_rn(y[j]);
+      }
+    }
+  }
+  // ---- reset the arrival state for the next panel (last CTA out) ----
+  if (!single) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(a.done + 1, 1) == a.nb - 1) {
+        for (int l = 1; l <= a.L; ++l)
+          for (int g = 0; g < a.nodes[l]; ++g) a.cnt[l][g] = 0;
+        a.done[1] = 0;
+        __threadfence();
+        st_release(a.done, 0);
+      }
+    }
+  }
+}
+
+// One CAQR level as its own launch (used when the fused tree does not fit the co-resident grid):
+// MGS on every row block of X; local Q in place; R_b -> stack rows [b*w, (b+1)*w) of S or Rout.
+__global__ void __launch_bounds__(kFusedThreads) panel_mgs_kernel(
+    int rows, int w, float* __restrict__ X, long long ldx, int br, int nb, float* __restrict__ S,
+    long long lds, float* __restrict__ Rout, long long ldr, int top, int* status, int col0) {
+  extern __shared__ float fsm[];
+  float* qs = fsm;
+  float* red = qs + kFusedCap * 33;
+  const int b = blockIdx.x;
+  const int row0 = b * br;
+  const int nrows = (b == nb - 1) ? rows - row0 : br;
+  float x[kFusedRPT][32];
+#pragma unroll
+  for (int r = 0; r < kFusedRPT; ++r) {
+    const int i = threadIdx.x + r * kFusedThreads;
+    const bool ok = i < nrows;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      x[r][j] = (ok && j < w) ? X[(long long)(row0 + i) + (long long)j * ldx] : 0.f;
+  }
+  float* Rdst = (nb == 1) ? Rout : S + (long long)b * w;
+  const long long ldR = (nb == 1) ? ldr : lds;
+  mgs_rotating(x, nrows, w, qs, Rdst, ldR, top != 0, status, col0, red);
+  __syncthreads();
+  for (int r = 0; r < kFusedRPT; ++r) {
+    const int i = threadIdx.x + r * kFusedThreads;
+    if (i < nrows)
+      for (int j = 0; j < w; ++j) X[(long long)(row0 + i) + (long long)j * ldx] = qs[i * 33 + j];
+  }
+}
+
+cudaError_t panel_mgs_level(int rows, int w, float* X, long long ldx, int br, int nb, float* S,
+                            long long lds, float* Rout, long long ldr, int top, int* status,
+                            int col0, cudaStream_t st) {
+  if (br + w - 1 > kFusedCap && nb > 1) return cudaErrorInvalidValue;
+  if (nb == 1 && rows > kFusedCap) return cudaErrorInvalidValue;
+  const int smem = (int)sizeof(float) * (kFusedCap * 33 + 2 * kFusedWarps * 32);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(panel_mgs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  panel_mgs_kernel<<<nb, kFusedThreads, smem, st>>>(rows, w, X, ldx, br, nb, S, lds, Rout, ldr,
+                                                    top, status, col0);
+  return cudaGetLastError();
+}
+
+int fused_panel_capacity(int num_sms) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    const int smem = fused_panel_smem_bytes();
+    cudaFuncSetAttribute(panel_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_fused_kernel, kFusedThreads,
+                                                      smem) != cudaSuccess)
+      per_sm = 0;
+  }
+  return per_sm * num_sms;
+}
+
+int fused_panel_smem_bytes() {
+  return (int)sizeof(float) * (2 * kFusedCap * 33 + 2 * 32 * 33 + 2 * kFusedWarps * 32);
+}
+
+int fused_panel_max_rows() { return kFusedCap; }
+
+// Plan the tree and launch.  ws: float scratch (Rbuf/Qst), iws: zeroed int scratch (counters,
+// done flags) that the kernel leaves zeroed.  Returns cudaErrorNotSupported if the tree does not
+// fit the co-resident grid (the caller then uses the multi-launch path).
+cudaError_t panel_fused(int m, int w, float* X, long long ldx, __half* Xh, long long ldh, int br,
+                        float* Rout, long long ldr, int root_is_global, int* status, int col0,
+                        float* ws, long long ws_cap, int* iws, long long iws_cap, int num_sms,
+                        cudaStream_t st) {
+  if (w < 1 || w > 32 || br + w - 1 > kFusedCap) return cudaErrorNotSupported;
+  FusedPanelArgs a{};
+  a.X = X;
+  a.ldx = ldx;
+  a.Xh = Xh;
+  a.ldh = ldh;
+  a.m = m;
+  a.w = w;
+  a.br = br;
+  a.nb = panel_num_blocks(m, br, w);
+  if (a.nb > fused_panel_capacity(num_sms)) return cudaErrorNotSupported;
+  a.F = br / w;
+  if (a.F < 2) return cudaErrorNotSupported;
+  a.nodes[0] = a.nb;
+  int L = 0;
+  while (a.nodes[L] > 1) {
+    if (L + 1 > kMaxLevels) return cudaErrorNotSupported;
+    a.nodes[L + 1] = (a.nodes[L] + a.F - 1) / a.F;
+    ++L;
+  }
+  a.L = L;
+  long long off = 0, ioff = 0;
+  const long long ww = (long long)w * w;
+  for (int l = 0; l <= L; ++l) {
+    a.Rbuf[l] = ws + off;
+    off += a.nodes[l] * ww;
+    if (l >= 1) {
+      a.Qst[l] = ws + off;
+      off += a.nodes[l - 1] * ww;
+      a.cnt[l] = iws + ioff;
+      ioff += a.nodes[l];
+    }
+  }
+  a.done = iws + ioff;
+  ioff += 2;
+  if (off > ws_cap || ioff > iws_cap) return cudaErrorNotSupported;
+  a.Rout = Rout;
+  a.ldr = ldr;
+  a.root_is_global = root_is_global;
+  a.status = status;
+  a.col0 = col0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.nb);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = fused_panel_smem_bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = (a.L > 0) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, panel_fused_kernel, a);
 }
 
 }  // namespace tcqr

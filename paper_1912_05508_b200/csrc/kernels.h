@@ -43,6 +43,14 @@ cudaError_t panel_mgs_level(int rows, int w, float* X, long long ldx, int br, in
 cudaError_t panel_apply(int rows, int w, float* X, long long ldx, int br, int nb, const float* S,
                         long long lds, cudaStream_t st);
 int panel_num_blocks(int rows, int br, int w);
+// Fused single-launch Eq. (6) panel (cooperative); cudaErrorNotSupported -> use the levels above.
+cudaError_t panel_fused(int m, int w, float* X, long long ldx, __half* Xh, long long ldh, int br,
+                        float* Rout, long long ldr, int root_is_global, int* status, int col0,
+                        float* ws, long long ws_cap, int* iws, long long iws_cap, int num_sms,
+                        cudaStream_t st);
+int fused_panel_capacity(int num_sms);
+int fused_panel_smem_bytes();
+int fused_panel_max_rows();
 
 // ---- K2b FP32 intra-leaf products (k_f32.cu) ----
 // T (h x w2, ld h) = Q1' A2 over m rows (deterministic split-K with partials in P).

@@ -117,6 +117,10 @@ struct FactorWs {
   long long stack_cap = 0;
   float* gather = nullptr;  // TSQR allgather (nranks * 32 * 32)
   float* rloc = nullptr;    // local panel R (32 * 32)
+  float* pws = nullptr;     // fused panel tree scratch (node R's and stack-Q slices)
+  long long pws_cap = 0;
+  int* iws = nullptr;       // fused panel arrival counters / flags (zero between launches)
+  long long iws_cap = 0;
 };
 
 static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, FactorWs& w) {
@@ -135,6 +139,10 @@ static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, Facto
   w.stack = a.take<float>((size_t)w.stack_cap);
   w.gather = a.take<float>((size_t)std::max(nranks, 1) * 32 * 32 + 64);
   w.rloc = a.take<float>(32 * 32 + 64);
+  w.pws_cap = 4 * ((m + 31) / 32 + 64) * 32 * 32;
+  w.pws = a.take<float>((size_t)w.pws_cap);
+  w.iws_cap = 4096 + m / 16;
+  w.iws = a.take<int>((size_t)w.iws_cap);
 }
 
 struct LlsWs {
@@ -349,11 +357,25 @@ static int caqr_rec(FactorWs& ws, long long& stack_off, int rows, int w, float* 
   return 0;
 }
 
+// Returns 0 and sets *wrote_h when the FP16 shadow of the final Q was emitted by the panel.
 static int panel(FactorWs& ws, int m, int w, float* X, long long ldx, float* Rout, long long ldr,
-                 int col0) {
+                 int col0, __half* Xh, bool* wrote_h) {
   Context& c = g_ctx;
   long long off = 0;
-  if (c.nranks <= 1) return caqr_rec(ws, off, m, w, X, ldx, Rout, ldr, true, col0);
+  *wrote_h = false;
+  if (c.nranks <= 1) {
+    cudaError_t e = cudaErrorNotSupported;
+    PROF(TCQR_K2_MGS, 4.0 * m * w * w, 8.0 * m * w + (Xh ? 2.0 * m * w : 0.0),
+         e = panel_fused(m, w, X, ldx, Xh, ws.ldh, c.cfg.panel_rows, Rout, ldr, 1, c.d_status,
+                         col0, ws.pws, ws.pws_cap, ws.iws, ws.iws_cap, c.num_sms, c.stream));
+    if (e == cudaSuccess) {
+      *wrote_h = Xh != nullptr;
+      return 0;
+    }
+    if (e != cudaErrorNotSupported) CK(e);
+    cudaGetLastError();
+    return caqr_rec(ws, off, m, w, X, ldx, Rout, ldr, true, col0);
+  }
   // TSQR (reading R-A26): local tree -> allgather of the P local R's -> redundant factorization of
   // the stack on every rank -> this rank's slice applied to the local Q.
   CKR(caqr_rec(ws, off, m, w, X, ldx, ws.rloc, w, false, col0));
@@ -390,7 +412,10 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   const int m = J.m;
   float* Qc = J.Q + (long long)c0 * J.ldq;
   if (w <= 32) {
-    CKR(panel(ws, m, w, Qc, J.ldq, J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0));
+    bool wrote_h = false;
+    CKR(panel(ws, m, w, Qc, J.ldq, J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0,
+              need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, &wrote_h));
+    if (wrote_h) return 0;
   } else {
     const int h = split_point(w), w2 = w - h;
     const bool tc = w > c.cfg.cutoff;
@@ -443,6 +468,7 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
   Context& c = g_ctx;
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));  // INT_MAX-ish = OK
   CK(cudaMemsetAsync(R, 0, sizeof(float) * (size_t)n * n, c.stream));
+  CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
   PROF(TCQR_COPY, 0, 8.0 * m * n, CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream)));
   FactorJob J{m, n, Q, (long long)m, R, (long long)n, &ws};
   const bool need_h = n > c.cfg.cutoff;
@@ -551,7 +577,7 @@ int tcqr_set_config(const tcqr_config_t* cfg) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!cfg) return -1;
   if (cfg->cutoff < 32 || cfg->cutoff > 128 || cfg->cutoff % 32) return -1;
-  if (cfg->panel_rows < 64 || cfg->panel_rows > 480 || cfg->panel_rows % 32) return -1;
+  if (cfg->panel_rows < 64 || cfg->panel_rows > 288 || cfg->panel_rows % 32) return -1;
   if (cfg->tol2 <= 0 || cfg->stag_window < 1 || cfg->stag_floor < 0) return -1;
   g_ctx.cfg = *cfg;
   return 0;
@@ -928,7 +954,7 @@ int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t
   if (ldx < m) return -4;
   if (!R) return -5;
   if (ldr < w) return -6;
-  if (br < 64 || br > 480 || br % 32) return -7;
+  if (br < 64 || br > 288 || br % 32) return -7;
   Context& c = g_ctx;
   begin_call();
   const int saved = c.cfg.panel_rows;
@@ -940,8 +966,9 @@ int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t
   FactorWs ws;
   plan_factor_ws(a, m, 32, 1, ws);
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));
-  long long off = 0;
-  int rc = caqr_rec(ws, off, (int)m, (int)w, X, ldx, R, ldr, true, 0);
+  CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
+  bool wrote_h = false;
+  int rc = panel(ws, (int)m, (int)w, X, ldx, R, ldr, 0, nullptr, &wrote_h);
   c.cfg.panel_rows = saved;
   if (rc) return rc;
   return read_status();
