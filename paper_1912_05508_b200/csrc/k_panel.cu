@@ -139,7 +139,18 @@ struct FusedPanelArgs {
   int root_is_global;           // 1: a zero/non-finite norm at the root is a breakdown
   int* status;
   int col0;
+  unsigned long long* dbg;  // optional phase timestamps (globaltimer), 64 slots
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define DBG_T(slot)                                                   \
+  do {                                                                \
+    if (a.dbg && threadIdx.x == 0) a.dbg[(slot)] = gtimer();          \
+  } while (0)
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -212,6 +223,7 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
   const int nrows = (b == a.nb - 1) ? a.m - row0 : a.br;
 
   // ---- step 1: Alg. 4 on this row block ----
+  if (b == 0) DBG_T(0);
   float x[kFusedRPT][32];
 #pragma unroll
   for (int r = 0; r < kFusedRPT; ++r) {
@@ -223,8 +235,10 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
   }
   const bool single = (a.L == 0);
   float* Rb = single ? a.Rout : a.Rbuf[0] + (long long)b * w * w;
+  if (b == 0) DBG_T(1);
   mgs_rotating(x, nrows, w, qA, Rb, single ? a.ldr : w, single && a.root_is_global, a.status,
                a.col0, red);
+  if (b == 0) DBG_T(2);
 
   // ---- steps 2-3: the last child to arrive factors each tree node ----
   int node = b;
@@ -239,6 +253,7 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
     __syncthreads();
     if (!s_last) break;
     __threadfence();
+    DBG_T(8 + 4 * l);
     const int srows = nchild * w;
     const float* Rc = a.Rbuf[l - 1] + (long long)first * w * w;
 #pragma unroll
@@ -252,8 +267,10 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
     }
     const bool top = (l == a.L);
     float* Rn = top ? a.Rout : a.Rbuf[l] + (long long)parent * w * w;
+    DBG_T(9 + 4 * l);
     mgs_rotating(x, srows, w, qB, Rn, top ? a.ldr : w, top && a.root_is_global, a.status, a.col0,
                  red);
+    DBG_T(10 + 4 * l);
     __syncthreads();
     float* Qd = a.Qst[l] + (long long)first * w * w;  // slice of child ci at Qd + ci*w*w
     for (int e = threadIdx.x; e < srows * w; e += kFusedThreads) {
@@ -263,6 +280,7 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
     }
     node = parent;
     root = top;
+    DBG_T(11 + 4 * l);
   }
   if (root && !single) {
     __threadfence();
@@ -275,6 +293,7 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
     if (threadIdx.x == 0)
       while (ld_acquire(a.done) == 0) __nanosleep(64);
     __syncthreads();
+    if (b == 0) DBG_T(3);
     int idx = b;
     for (int e = threadIdx.x; e < 32 * 32; e += kFusedThreads) {
       const int l_ = e % 32, j = e / 32;
@@ -306,6 +325,7 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
     }
     __syncthreads();
   }
+  if (b == 0) DBG_T(4);
   // ---- step 5: final Q rows (FP32 + FP16 shadow) ----
   for (int r = 0; r < kFusedRPT; ++r) {
     const int i = threadIdx.x + r * kFusedThreads;
@@ -332,6 +352,7 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
       }
     }
   }
+  if (b == 0) DBG_T(5);
   // ---- reset the arrival state for the next panel (last CTA out) ----
   if (!single) {
     __syncthreads();
@@ -394,6 +415,8 @@ cudaError_t panel_mgs_level(int rows, int w, float* X, long long ldx, int br, in
                                                     top, status, col0);
   return cudaGetLastError();
 }
+
+unsigned long long* g_panel_dbg = nullptr;
 
 int fused_panel_capacity(int num_sms) {
   static int per_sm = -1;
@@ -461,6 +484,7 @@ cudaError_t panel_fused(int m, int w, float* X, long long ldx, __half* Xh, long 
   a.root_is_global = root_is_global;
   a.status = status;
   a.col0 = col0;
+  a.dbg = g_panel_dbg;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.nb);
   cfg.blockDim = dim3(kFusedThreads);

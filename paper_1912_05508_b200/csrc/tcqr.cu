@@ -1015,6 +1015,12 @@ int tcqr_profile_read(int cls, double* ms, double* flops, double* bytes, int* la
 
 int tcqr_last_launch_count(void) { return g_last_launches; }
 
+// Debug: pointer to 64 device uint64 slots receiving fused-panel phase timestamps (or NULL).
+int tcqr_debug_panel_timestamps(void* dptr) {
+  g_panel_dbg = static_cast<unsigned long long*>(dptr);
+  return 0;
+}
+
 int tcqr_gemv(int trans, int64_t m, int64_t n, const float* A, int64_t lda, const double* v,
               double* y) {
   if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
