@@ -55,7 +55,8 @@ extern "C" {
 typedef struct tcqr_config {
   int cutoff;        /* recursion cutoff c: split nodes wider than c use FP16 tensor cores
                         (Alg. 2 line 3; default 128; multiple of 32, >= 32)     */
-  int panel_rows;    /* CAQR block rows br (256; default 256; 64..288)      */
+  int panel_rows;    /* CAQR block rows br (PAPER.md:441-442 uses 256 on V100; default 1024 on
+                        B200, reading R-A6; 64..1024, multiple of 32)                        */
   int col_scaling;   /* 1: per-column power-of-two FP16 range guard (reading R-A4; default 1) */
   int restart;       /* 1: FP64 target, one CGLS restart from the true residual (R-A12)        */
   double tol2;       /* restart-pass tolerance (default 1e-6, R-A12)                           */
@@ -155,7 +156,7 @@ int tcqr_gemm_nn_update(int64_t m, int64_t h, int64_t w2, const uint16_t* Qh, in
                         const float* col_mult);
 
 /* K2 (§8a a3): CAQR-MGS panel (Eq. (6) with Alg. 4 blocks of br rows), w <= 32 columns, in
- * place on X (m x w, ldx); R (w x w, ldr) upper triangular output; br in [64, 288]. */
+ * place on X (m x w, ldx); R (w x w, ldr) upper triangular output; br in [64, 1024]. */
 int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t ldr, int br);
 
 /* K6 helper (Alg. 5 lines 12/18): Minv (n x n FP64, ldm) = R^-1 for upper-triangular FP32 R. */

@@ -26,22 +26,6 @@ int panel_num_blocks(int rows, int br, int w) {
   return nb;
 }
 
-// Transpose-reduce: on exit v[0] in lane l holds sum over the warp of the input v[l].
-__device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool upper = (lane & s) != 0;
-#pragma unroll
-    for (int i = 0; i < s; ++i) {
-      const float send = upper ? v[i] : v[i + s];
-      const float keep = upper ? v[i + s] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-    }
-  }
-  return v[0];
-}
-
 // (panel_mgs_kernel is defined below, after the rotating MGS step it shares.)
 
 // X_b <- X_b * T_b with T_b = S[b*w:(b+1)*w, 0:w] (lds).  grid.x = row chunks of 256 rows.
@@ -108,19 +92,17 @@ cudaError_t panel_apply(int rows, int w, float* X, long long ldx, int br, int nb
 //
 // CTA b runs Alg. 4 on row block b (step 1) with a rotating register window: at step k the pivot
 // column is always x[.][0] and the trailing update writes column j into slot j-1, so the loop
-// body has no data-dependent register indexing and is small enough for the instruction cache
-// (the fully unrolled v1 kernel spent 55% of its cycles in no_instructions stalls; ncu,
-// profiles/r01_ncu_panel_mgs_v1_details.csv).  The stacked R's (step 2) are factored (step 3) by
-// the LAST child CTA to finish each tree node (atomic arrival counter), level by level, so no
-// CTA ever waits for another until the root is done.  Then every CTA forms its composite
-// transform T_b = S1[b] S2[parent(b)] ... (step 4) from the stack Q slices and writes its final Q
-// rows (FP32 and the FP16 shadow used by the tensor-core GEMMs above), step 5.
-// Co-residency of all CTAs is guaranteed by the cooperative launch.
+// body has no data-dependent register indexing and stays small for the instruction cache (the
+// fully unrolled v1 kernel spent 55% of its cycles in no_instructions stalls; ncu,
+// profiles/r01_ncu_panel_mgs_v1_details.csv).  The reduction width follows the active column
+// count.  The stacked R's (step 2) are factored (step 3) by the LAST child CTA to finish each
+// tree node (atomic arrival counter), level by level, so no CTA waits for another until the root
+// is done.  Then every CTA forms its composite transform T_b = S1[b] S2[parent(b)] ... (step 4)
+// from the stack-Q slices and writes its final Q rows (FP32 and the FP16 shadow used by the
+// tensor-core GEMMs above), step 5.  Co-residency of all CTAs is guaranteed by the cooperative
+// launch.  Two shapes: 128 threads x 2 rows (256-row blocks, fan-in 8) and 256 threads x 4 rows
+// (1024-row blocks, fan-in 32: two tree levels up to m = 32768).
 // ==========================================================================================
-constexpr int kFusedThreads = 160;  // 5 warps
-constexpr int kFusedRPT = 2;        // 320 rows per CTA: br <= 288 (br + w - 1 <= 319)
-constexpr int kFusedCap = kFusedThreads * kFusedRPT;
-constexpr int kFusedWarps = kFusedThreads / 32;
 constexpr int kMaxLevels = 8;
 
 struct FusedPanelArgs {
@@ -139,7 +121,7 @@ struct FusedPanelArgs {
   int root_is_global;           // 1: a zero/non-finite norm at the root is a breakdown
   int* status;
   int col0;
-  unsigned long long* dbg;  // optional phase timestamps (globaltimer), 64 slots
+  unsigned long long* dbg;      // optional phase timestamps (globaltimer), 64 slots
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -147,87 +129,157 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-#define DBG_T(slot)                                                   \
-  do {                                                                \
-    if (a.dbg && threadIdx.x == 0) a.dbg[(slot)] = gtimer();          \
+#define DBG_T(slot)                                          \
+  do {                                                       \
+    if (a.dbg && threadIdx.x == 0) a.dbg[(slot)] = gtimer(); \
   } while (0)
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Alg. 4 on the rows held in x (thread t owns rows t, t + kFusedThreads).  Q columns go to
-// qs[row * 33 + k] (shared), R row k to Rdst[k + j * ldR] (zeros below the diagonal).
-__device__ __forceinline__ void mgs_rotating(float (&x)[kFusedRPT][32], int nrows, int w,
-                                             float* qs, float* Rdst, long long ldR, bool check,
-                                             int* status, int col0, float* red) {
+// Lane l ends with the warp sum of v[l % W] (all lanes sharing l % W hold the same value).
+template <int W>
+__device__ __forceinline__ float tr_reduce(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = W / 2; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const float send = upper ? v[i] : v[i + s];
+      const float keep = upper ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  float r = v[0];
+#pragma unroll
+  for (int s = W; s < 32; s <<= 1) r += __shfl_xor_sync(0xffffffffu, r, s);
+  return r;
+}
+
+// Where the Q columns of an MGS go: shared [row][33] (row blocks) or a global stack-Q slice
+// layout (children blocks of w x w, column-major): row s -> child s / w, row s % w.
+struct QSink {
+  float* sm;       // shared rows x 33, or null
+  float* g;        // global slices base, or null
+  int w;
+  __device__ __forceinline__ void put(int row, int k, float v) const {
+    if (sm)
+      sm[row * 33 + k] = v;
+    else
+      g[(long long)(row / w) * w * w + (row % w) + (long long)k * w] = v;
+  }
+};
+
+// One MGS step with reduction width W (>= active columns).  Columns >= W are zero.
+template <int NT, int RPT, int W>
+__device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, int k,
+                                         const QSink& qs, float* Rdst, long long ldR, bool check,
+                                         int* status, int col0, float* red, int& buf) {
+  constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float p[32];
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) acc = fmaf(x[r][0], x[r][j], acc);
+    p[j] = acc;
+  }
+  const float part = tr_reduce<W>(p);  // lane j: warp sum of a_k' a_{k+(j%W)}
+  red[(buf * NW + warp) * 32 + lane] = part;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int v = 0; v < NW; ++v) tot += red[(buf * NW + v) * 32 + lane];
+  buf ^= 1;
+  const float rkk = sqrtf(__shfl_sync(0xffffffffu, tot, 0));
+  const bool zero = !(rkk > 0.f) || !isfinite(rkk);
+  if (check && zero && threadIdx.x == 0 && status) atomicMin(status, col0 + k + 1);
+  const int jl = lane & (W - 1);
+  const float rkj = zero ? 0.f : (jl == 0 ? rkk : tot / rkk);
+  if (warp == 0) {
+    if (lane < w - k && lane < W) Rdst[k + (long long)(k + lane) * ldR] = rkj;
+    if (lane < k) Rdst[k + (long long)lane * ldR] = 0.f;
+  }
+  float q[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    q[r] = zero ? 0.f : x[r][0] / rkk;
+    const int row = threadIdx.x + r * NT;
+    if (row < nrows) qs.put(row, k, q[r]);
+  }
+#pragma unroll
+  for (int j = 1; j < W; ++j) {
+    const float rj = __shfl_sync(0xffffffffu, rkj, j);
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) x[r][j - 1] = fmaf(-q[r], rj, x[r][j]);
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) x[r][W - 1] = 0.f;
+}
+
+// Alg. 4 on the rows held in x (thread t owns rows t + r*NT): Q columns -> qs, R rows -> Rdst.
+template <int NT, int RPT>
+__device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int w,
+                                             const QSink& qs, float* Rdst, long long ldR,
+                                             bool check, int* status, int col0, float* red) {
   int buf = 0;
   for (int k = 0; k < w; ++k) {
-    float p[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      float acc = 0.f;
-#pragma unroll
-      for (int r = 0; r < kFusedRPT; ++r) acc = fmaf(x[r][0], x[r][j], acc);
-      p[j] = acc;
-    }
-    const float part = transpose_reduce32(p);  // lane j: warp sum of a_k' a_{k+j}
-    red[(buf * kFusedWarps + warp) * 32 + lane] = part;
-    __syncthreads();
-    float tot = 0.f;
-#pragma unroll
-    for (int v = 0; v < kFusedWarps; ++v) tot += red[(buf * kFusedWarps + v) * 32 + lane];
-    buf ^= 1;
-    const float rkk = sqrtf(__shfl_sync(0xffffffffu, tot, 0));
-    const bool zero = !(rkk > 0.f) || !isfinite(rkk);
-    if (check && zero && threadIdx.x == 0 && status) atomicMin(status, col0 + k + 1);
-    const float rkj = zero ? 0.f : (lane == 0 ? rkk : tot / rkk);
-    if (warp == 0) {
-      if (lane < w - k) Rdst[k + (long long)(k + lane) * ldR] = rkj;
-      if (lane < k) Rdst[k + (long long)lane * ldR] = 0.f;
-    }
-    float q[kFusedRPT];
-#pragma unroll
-    for (int r = 0; r < kFusedRPT; ++r) {
-      q[r] = zero ? 0.f : x[r][0] / rkk;
-      const int row = threadIdx.x + r * kFusedThreads;
-      if (row < nrows) qs[row * 33 + k] = q[r];
-    }
-#pragma unroll
-    for (int j = 1; j < 32; ++j) {
-      const float rj = __shfl_sync(0xffffffffu, rkj, j);
-#pragma unroll
-      for (int r = 0; r < kFusedRPT; ++r) x[r][j - 1] = fmaf(-q[r], rj, x[r][j]);
-    }
-#pragma unroll
-    for (int r = 0; r < kFusedRPT; ++r) x[r][31] = 0.f;
+    const int act = w - k;
+    if (act > 16)
+      mgs_step<NT, RPT, 32>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+    else if (act > 8)
+      mgs_step<NT, RPT, 16>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+    else if (act > 4)
+      mgs_step<NT, RPT, 8>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+    else if (act > 2)
+      mgs_step<NT, RPT, 4>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+    else if (act > 1)
+      mgs_step<NT, RPT, 2>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+    else
+      mgs_step<NT, RPT, 1>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
   }
 }
 
-__global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelArgs a) {
+template <int NT, int RPT>
+struct FusedShape {
+  static constexpr int CAP = NT * RPT;
+  static constexpr int SMEM = (int)sizeof(float) * (CAP * 33 + 3 * 32 * 33 + 2 * (NT / 32) * 32);
+};
+
+// Balanced row blocks: block b covers [b*m/nb, (b+1)*m/nb), every block <= br rows (Eq. (6) is
+// exact for any blocking; reading R-A6 folds remainders, this spreads them).
+__device__ __forceinline__ int blk_row(int b, int m, int nb) {
+  return (int)((long long)b * m / nb);
+}
+
+template <int NT, int RPT>
+__global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
+  using Sh = FusedShape<NT, RPT>;
   extern __shared__ float fsm[];
-  float* qA = fsm;                      // level-1 Q_b   [kFusedCap][33]
-  float* qB = qA + kFusedCap * 33;      // stack-level Q [kFusedCap][33]
-  float* T = qB + kFusedCap * 33;       // [32][33]
-  float* T2 = T + 32 * 33;              // [32][33]
-  float* red = T2 + 32 * 33;            // [2][warps][32]
+  float* qA = fsm;                 // level-1 Q_b [CAP][33]
+  float* T = qA + Sh::CAP * 33;    // [32][33]
+  float* T2 = T + 32 * 33;         // [32][33]
+  float* Sst = T2 + 32 * 33;       // [32][33] staged stack-Q slice
+  float* red = Sst + 32 * 33;      // [2][NT/32][32]
   __shared__ int s_last;
   const int b = blockIdx.x, w = a.w;
-  const int row0 = b * a.br;
-  const int nrows = (b == a.nb - 1) ? a.m - row0 : a.br;
+  const int row0 = blk_row(b, a.m, a.nb);
+  const int nrows = blk_row(b + 1, a.m, a.nb) - row0;
 
   // ---- step 1: Alg. 4 on this row block ----
   if (b == 0) DBG_T(0);
-  float x[kFusedRPT][32];
+  float x[RPT][32];
 #pragma unroll
-  for (int r = 0; r < kFusedRPT; ++r) {
-    const int i = threadIdx.x + r * kFusedThreads;
+  for (int r = 0; r < RPT; ++r) {
+    const int i = threadIdx.x + r * NT;
     const bool ok = i < nrows;
 #pragma unroll
     for (int j = 0; j < 32; ++j)
@@ -236,8 +288,8 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
   const bool single = (a.L == 0);
   float* Rb = single ? a.Rout : a.Rbuf[0] + (long long)b * w * w;
   if (b == 0) DBG_T(1);
-  mgs_rotating(x, nrows, w, qA, Rb, single ? a.ldr : w, single && a.root_is_global, a.status,
-               a.col0, red);
+  mgs_rotating<NT, RPT>(x, nrows, w, QSink{qA, nullptr, w}, Rb, single ? a.ldr : w,
+                        single && a.root_is_global, a.status, a.col0, red);
   if (b == 0) DBG_T(2);
 
   // ---- steps 2-3: the last child to arrive factors each tree node ----
@@ -257,30 +309,22 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
     const int srows = nchild * w;
     const float* Rc = a.Rbuf[l - 1] + (long long)first * w * w;
 #pragma unroll
-    for (int r = 0; r < kFusedRPT; ++r) {
-      const int s = threadIdx.x + r * kFusedThreads;
+    for (int r = 0; r < RPT; ++r) {
+      const int s = threadIdx.x + r * NT;
       const bool ok = s < srows;
-      const int ci = ok ? s / w : 0, aa = ok ? s % w : 0;
+      const int ci = ok ? s / w : 0, aa = ok ? s - ci * w : 0;
+      const float* src = Rc + (long long)ci * w * w + aa;
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        x[r][j] = (ok && j < w) ? __ldcg(Rc + (long long)ci * w * w + aa + (long long)j * w) : 0.f;
+      for (int j = 0; j < 32; ++j) x[r][j] = (ok && j < w) ? __ldcg(src + (long long)j * w) : 0.f;
     }
     const bool top = (l == a.L);
     float* Rn = top ? a.Rout : a.Rbuf[l] + (long long)parent * w * w;
     DBG_T(9 + 4 * l);
-    mgs_rotating(x, srows, w, qB, Rn, top ? a.ldr : w, top && a.root_is_global, a.status, a.col0,
-                 red);
+    mgs_rotating<NT, RPT>(x, srows, w, QSink{nullptr, a.Qst[l] + (long long)first * w * w, w}, Rn,
+                          top ? a.ldr : w, top && a.root_is_global, a.status, a.col0, red);
     DBG_T(10 + 4 * l);
-    __syncthreads();
-    float* Qd = a.Qst[l] + (long long)first * w * w;  // slice of child ci at Qd + ci*w*w
-    for (int e = threadIdx.x; e < srows * w; e += kFusedThreads) {
-      const int s = e % srows, j = e / srows;
-      const int ci = s / w, aa = s % w;
-      Qd[(long long)ci * w * w + aa + (long long)j * w] = qB[s * 33 + j];
-    }
     node = parent;
     root = top;
-    DBG_T(11 + 4 * l);
   }
   if (root && !single) {
     __threadfence();
@@ -290,53 +334,50 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
 
   // ---- step 4: T_b = S1[b] S2[b/F] ... ; Q_b <- Q_b T_b ----
   if (!single) {
-    if (threadIdx.x == 0)
-      while (ld_acquire(a.done) == 0) __nanosleep(64);
+    if (threadIdx.x == 0) {
+      while (ld_relaxed(a.done) == 0) __nanosleep(32);
+      __threadfence();
+    }
     __syncthreads();
     if (b == 0) DBG_T(3);
     int idx = b;
-    for (int e = threadIdx.x; e < 32 * 32; e += kFusedThreads) {
-      const int l_ = e % 32, j = e / 32;
-      T[l_ * 33 + j] = (l_ < w && j < w) ? __ldcg(a.Qst[1] + (long long)idx * w * w + l_ + j * w)
-                                         : 0.f;
+    for (int e = threadIdx.x; e < 32 * 32; e += NT) {
+      const int i = e & 31, j = e >> 5;
+      T[i * 33 + j] = (i < w && j < w) ? __ldcg(a.Qst[1] + (long long)idx * w * w + i + j * w) : 0.f;
     }
     for (int l = 2; l <= a.L; ++l) {
       idx /= a.F;
       const float* S = a.Qst[l] + (long long)idx * w * w;
+      for (int e = threadIdx.x; e < 32 * 32; e += NT) {
+        const int i = e & 31, j = e >> 5;
+        Sst[i * 33 + j] = (i < w && j < w) ? __ldcg(S + i + j * w) : 0.f;
+      }
       __syncthreads();
-      for (int e = threadIdx.x; e < 32 * 32; e += kFusedThreads) {
-        const int i = e % 32, j = e / 32;
+      for (int e = threadIdx.x; e < 32 * 32; e += NT) {
+        const int i = e & 31, j = e >> 5;
         float acc = 0.f;
-        if (i < w && j < w)
-          for (int t = 0; t < w; ++t) acc = fmaf(T[i * 33 + t], __ldcg(S + t + j * w), acc);
+#pragma unroll 8
+        for (int t = 0; t < 32; ++t) acc = fmaf(T[i * 33 + t], Sst[t * 33 + j], acc);
         T2[i * 33 + j] = acc;
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < 32 * 32; e += kFusedThreads) {
-        const int i = e % 32, j = e / 32;
-        T[i * 33 + j] = T2[i * 33 + j];
-      }
-    }
-    __syncthreads();
-  } else {
-    for (int e = threadIdx.x; e < 32 * 32; e += kFusedThreads) {
-      const int i = e % 32, j = e / 32;
-      T[i * 33 + j] = (i == j) ? 1.f : 0.f;
+      for (int e = threadIdx.x; e < 32 * 32; e += NT) T[(e & 31) * 33 + (e >> 5)] = T2[(e & 31) * 33 + (e >> 5)];
     }
     __syncthreads();
   }
   if (b == 0) DBG_T(4);
   // ---- step 5: final Q rows (FP32 + FP16 shadow) ----
-  for (int r = 0; r < kFusedRPT; ++r) {
-    const int i = threadIdx.x + r * kFusedThreads;
+#pragma unroll 1
+  for (int r = 0; r < RPT; ++r) {
+    const int i = threadIdx.x + r * NT;
     if (i >= nrows) continue;
     float y[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) y[j] = 0.f;
     if (single) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) y[j] = qA[i * 33 + j];
     } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) y[j] = 0.f;
       for (int l_ = 0; l_ < w; ++l_) {
         const float ql = qA[i * 33 + l_];
 #pragma unroll
@@ -371,19 +412,21 @@ __global__ void __launch_bounds__(kFusedThreads) panel_fused_kernel(FusedPanelAr
 
 // One CAQR level as its own launch (used when the fused tree does not fit the co-resident grid):
 // MGS on every row block of X; local Q in place; R_b -> stack rows [b*w, (b+1)*w) of S or Rout.
-__global__ void __launch_bounds__(kFusedThreads) panel_mgs_kernel(
+// Blocks follow the fold rule of reading R-A6 (panel_num_blocks).
+constexpr int kLvlNT = 128, kLvlRPT = 4;
+__global__ void __launch_bounds__(kLvlNT) panel_mgs_kernel(
     int rows, int w, float* __restrict__ X, long long ldx, int br, int nb, float* __restrict__ S,
     long long lds, float* __restrict__ Rout, long long ldr, int top, int* status, int col0) {
   extern __shared__ float fsm[];
   float* qs = fsm;
-  float* red = qs + kFusedCap * 33;
+  float* red = qs + kLvlNT * kLvlRPT * 33;
   const int b = blockIdx.x;
   const int row0 = b * br;
   const int nrows = (b == nb - 1) ? rows - row0 : br;
-  float x[kFusedRPT][32];
+  float x[kLvlRPT][32];
 #pragma unroll
-  for (int r = 0; r < kFusedRPT; ++r) {
-    const int i = threadIdx.x + r * kFusedThreads;
+  for (int r = 0; r < kLvlRPT; ++r) {
+    const int i = threadIdx.x + r * kLvlNT;
     const bool ok = i < nrows;
 #pragma unroll
     for (int j = 0; j < 32; ++j)
@@ -391,10 +434,11 @@ __global__ void __launch_bounds__(kFusedThreads) panel_mgs_kernel(
   }
   float* Rdst = (nb == 1) ? Rout : S + (long long)b * w;
   const long long ldR = (nb == 1) ? ldr : lds;
-  mgs_rotating(x, nrows, w, qs, Rdst, ldR, top != 0, status, col0, red);
+  mgs_rotating<kLvlNT, kLvlRPT>(x, nrows, w, QSink{qs, nullptr, w}, Rdst, ldR, top != 0, status,
+                                col0, red);
   __syncthreads();
-  for (int r = 0; r < kFusedRPT; ++r) {
-    const int i = threadIdx.x + r * kFusedThreads;
+  for (int r = 0; r < kLvlRPT; ++r) {
+    const int i = threadIdx.x + r * kLvlNT;
     if (i < nrows)
       for (int j = 0; j < w; ++j) X[(long long)(row0 + i) + (long long)j * ldx] = qs[i * 33 + j];
   }
@@ -403,47 +447,50 @@ __global__ void __launch_bounds__(kFusedThreads) panel_mgs_kernel(
 cudaError_t panel_mgs_level(int rows, int w, float* X, long long ldx, int br, int nb, float* S,
                             long long lds, float* Rout, long long ldr, int top, int* status,
                             int col0, cudaStream_t st) {
-  if (br + w - 1 > kFusedCap && nb > 1) return cudaErrorInvalidValue;
-  if (nb == 1 && rows > kFusedCap) return cudaErrorInvalidValue;
-  const int smem = (int)sizeof(float) * (kFusedCap * 33 + 2 * kFusedWarps * 32);
+  constexpr int cap = kLvlNT * kLvlRPT;
+  if (nb > 1 && br + w - 1 > cap) return cudaErrorInvalidValue;
+  if (nb == 1 && rows > cap) return cudaErrorInvalidValue;
+  const int smem = (int)sizeof(float) * (cap * 33 + 2 * (kLvlNT / 32) * 32);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(panel_mgs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  panel_mgs_kernel<<<nb, kFusedThreads, smem, st>>>(rows, w, X, ldx, br, nb, S, lds, Rout, ldr,
-                                                    top, status, col0);
+  panel_mgs_kernel<<<nb, kLvlNT, smem, st>>>(rows, w, X, ldx, br, nb, S, lds, Rout, ldr, top,
+                                             status, col0);
   return cudaGetLastError();
 }
 
 unsigned long long* g_panel_dbg = nullptr;
 
-int fused_panel_capacity(int num_sms) {
+template <int NT, int RPT>
+static int fused_capacity(int num_sms) {
   static int per_sm = -1;
   if (per_sm < 0) {
-    const int smem = fused_panel_smem_bytes();
-    cudaFuncSetAttribute(panel_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_fused_kernel, kFusedThreads,
+    const int smem = FusedShape<NT, RPT>::SMEM;
+    cudaFuncSetAttribute(panel_fused_kernel<NT, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_fused_kernel<NT, RPT>, NT,
                                                       smem) != cudaSuccess)
       per_sm = 0;
   }
   return per_sm * num_sms;
 }
 
-int fused_panel_smem_bytes() {
-  return (int)sizeof(float) * (2 * kFusedCap * 33 + 2 * 32 * 33 + 2 * kFusedWarps * 32);
-}
+int fused_panel_capacity(int num_sms) { return fused_capacity<256, 4>(num_sms); }
+int fused_panel_smem_bytes() { return FusedShape<256, 4>::SMEM; }
+int fused_panel_max_rows() { return 1024; }
 
-int fused_panel_max_rows() { return kFusedCap; }
-
-// Plan the tree and launch.  ws: float scratch (Rbuf/Qst), iws: zeroed int scratch (counters,
-// done flags) that the kernel leaves zeroed.  Returns cudaErrorNotSupported if the tree does not
-// fit the co-resident grid (the caller then uses the multi-launch path).
+// Plan the tree and launch.  br <= 256 uses the 128 x 2 shape, else the 256 x 4 shape (br <=
+// 1024).  ws: float scratch (node R's and stack-Q slices), iws: zeroed int scratch (counters,
+// flags) that the kernel leaves zeroed.  cudaErrorNotSupported if the tree does not fit the
+// co-resident grid (the caller then uses the multi-launch path).
 cudaError_t panel_fused(int m, int w, float* X, long long ldx, __half* Xh, long long ldh, int br,
                         float* Rout, long long ldr, int root_is_global, int* status, int col0,
                         float* ws, long long ws_cap, int* iws, long long iws_cap, int num_sms,
                         cudaStream_t st) {
-  if (w < 1 || w > 32 || br + w - 1 > kFusedCap) return cudaErrorNotSupported;
+  const bool big = br > 256;
+  if (w < 1 || w > 32 || br > 1024) return cudaErrorNotSupported;
   FusedPanelArgs a{};
   a.X = X;
   a.ldx = ldx;
@@ -452,8 +499,10 @@ cudaError_t panel_fused(int m, int w, float* X, long long ldx, __half* Xh, long 
   a.m = m;
   a.w = w;
   a.br = br;
-  a.nb = panel_num_blocks(m, br, w);
-  if (a.nb > fused_panel_capacity(num_sms)) return cudaErrorNotSupported;
+  a.nb = (m + br - 1) / br;
+  if (a.nb < 1) a.nb = 1;
+  const int cap = big ? fused_capacity<256, 4>(num_sms) : fused_capacity<128, 2>(num_sms);
+  if (a.nb > cap) return cudaErrorNotSupported;
   a.F = br / w;
   if (a.F < 2) return cudaErrorNotSupported;
   a.nodes[0] = a.nb;
@@ -487,15 +536,16 @@ cudaError_t panel_fused(int m, int w, float* X, long long ldx, __half* Xh, long 
   a.dbg = g_panel_dbg;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.nb);
-  cfg.blockDim = dim3(kFusedThreads);
-  cfg.dynamicSmemBytes = fused_panel_smem_bytes();
+  cfg.blockDim = dim3(big ? 256 : 128);
+  cfg.dynamicSmemBytes = big ? FusedShape<256, 4>::SMEM : FusedShape<128, 2>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = (a.L > 0) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, panel_fused_kernel, a);
+  return big ? cudaLaunchKernelEx(&cfg, panel_fused_kernel<256, 4>, a)
+             : cudaLaunchKernelEx(&cfg, panel_fused_kernel<128, 2>, a);
 }
 
 }  // namespace tcqr

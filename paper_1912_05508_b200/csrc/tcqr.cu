@@ -335,7 +335,7 @@ static void prof_drain() {
 static int caqr_rec(FactorWs& ws, long long& stack_off, int rows, int w, float* X, long long ldx,
                     float* Rout, long long ldr, bool top, int col0) {
   Context& c = g_ctx;
-  const int br = c.cfg.panel_rows;
+  const int br = std::min(c.cfg.panel_rows, 480);  // the per-level kernel holds <= 512 rows
   const int nb = panel_num_blocks(rows, br, w);
   if (nb == 1) {
     PROF(TCQR_K2_MGS, 2.0 * rows * w * w, 8.0 * rows * w,
@@ -564,7 +564,7 @@ const char* tcqr_version(void) { return "tcqr 0.1 (sm_100a tcgen05; arXiv 1912.0
 void tcqr_default_config(tcqr_config_t* c) {
   if (!c) return;
   c->cutoff = 128;
-  c->panel_rows = 256;
+  c->panel_rows = 1024;
   c->col_scaling = 1;
   c->restart = 1;
   c->tol2 = 1e-6;
@@ -577,7 +577,7 @@ int tcqr_set_config(const tcqr_config_t* cfg) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!cfg) return -1;
   if (cfg->cutoff < 32 || cfg->cutoff > 128 || cfg->cutoff % 32) return -1;
-  if (cfg->panel_rows < 64 || cfg->panel_rows > 288 || cfg->panel_rows % 32) return -1;
+  if (cfg->panel_rows < 64 || cfg->panel_rows > 1024 || cfg->panel_rows % 32) return -1;
   if (cfg->tol2 <= 0 || cfg->stag_window < 1 || cfg->stag_floor < 0) return -1;
   g_ctx.cfg = *cfg;
   return 0;
@@ -954,7 +954,7 @@ int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t
   if (ldx < m) return -4;
   if (!R) return -5;
   if (ldr < w) return -6;
-  if (br < 64 || br > 288 || br % 32) return -7;
+  if (br < 64 || br > 1024 || br % 32) return -7;
   Context& c = g_ctx;
   begin_call();
   const int saved = c.cfg.panel_rows;

@@ -106,7 +106,8 @@ def test_gemm_exact_small_integers(tq):
 
 @pytest.mark.parametrize("m,w,br", [(256, 32, 256), (300, 32, 256), (1024, 32, 256),
                                     (4096, 32, 256), (70000, 32, 256), (5000, 17, 128),
-                                    (33, 32, 64)])
+                                    (33, 32, 64), (32768, 32, 1024), (5000, 17, 1024),
+                                    (70000, 32, 1024), (1000, 32, 1024), (200000, 32, 1024)])
 def test_panel_vs_oracle(tq, m, w, br):
     a = W.gaussian(m, w, seed=m + w)
     X = tq.to_device_colmajor(a)
@@ -119,10 +120,12 @@ def test_panel_vs_oracle(tq, m, w, br):
     assert np.linalg.norm(a - q @ r) / np.linalg.norm(a) < 1e-6
 
 
-def test_panel_planted_hadamard_bitwise(tq):
-    a, qt, r0 = W.planted_hadamard(1024, 32, seed=201)
+@pytest.mark.parametrize("m,br", [(1024, 256), (4096, 1024), (1024, 1024), (16384, 256)])
+def test_panel_planted_hadamard_bitwise(tq, m, br):
+    # block rows, rank-local rows and the number of stacked R's are powers of 4
+    a, qt, r0 = W.planted_hadamard(m, 32, seed=201)
     X = tq.to_device_colmajor(a)
-    Xq, R = tq.panel_qr(X, br=256)
+    Xq, R = tq.panel_qr(X, br=br)
     assert np.array_equal(R.cpu().numpy().astype(np.float64), r0)
     assert np.array_equal(Xq.cpu().numpy().astype(np.float64), qt)
 

@@ -65,10 +65,12 @@ def test_factor_spectrum_gates(tq, kind, cond):
     _gates(a, q, r, r_o)
 
 
-@pytest.mark.parametrize("n,cutoff", [(128, 32), (128, 128), (256, 32), (256, 64)])
-def test_factor_planted_hadamard_bitwise(tq, n, cutoff):
-    a, qt, r0 = W.planted_hadamard(1024, n, seed=201)
-    q, r = _factor(tq, a, cutoff=cutoff, panel_rows=256)
+@pytest.mark.parametrize("m,n,cutoff,br", [(1024, 128, 32, 256), (1024, 128, 128, 256),
+                                           (1024, 256, 32, 256), (1024, 256, 64, 256),
+                                           (4096, 256, 64, 1024), (4096, 512, 128, 1024)])
+def test_factor_planted_hadamard_bitwise(tq, m, n, cutoff, br):
+    a, qt, r0 = W.planted_hadamard(m, n, seed=201)
+    q, r = _factor(tq, a, cutoff=cutoff, panel_rows=br)
     assert np.array_equal(r, r0)
     assert np.array_equal(q, qt)
 
