@@ -169,19 +169,19 @@ struct QSink {
   float* sm;       // shared rows x 33, or null
   float* g;        // global slices base, or null
   int w;
-  __device__ __forceinline__ void put(int row, int k, float v) const {
-    if (sm)
-      sm[row * 33 + k] = v;
-    else
-      g[(long long)(row / w) * w * w + (row % w) + (long long)k * w] = v;
+  // element (row, k) lives at base(row) + k * stride
+  __device__ __forceinline__ float* base(int row) const {
+    return sm ? sm + row * 33 : g + (long long)(row / w) * w * w + (row % w);
   }
+  __device__ __forceinline__ int stride() const { return sm ? 1 : w; }
 };
 
 // One MGS step with reduction width W (>= active columns).  Columns >= W are zero.
 template <int NT, int RPT, int W>
 __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, int k,
-                                         const QSink& qs, float* Rdst, long long ldR, bool check,
-                                         int* status, int col0, float* red, int& buf) {
+                                         float* const (&qp)[RPT], int qstride, float* Rdst,
+                                         long long ldR, bool check, int* status, int col0,
+                                         float* red, int& buf) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float p[32];
@@ -213,7 +213,7 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
   for (int r = 0; r < RPT; ++r) {
     q[r] = zero ? 0.f : x[r][0] / rkk;
     const int row = threadIdx.x + r * NT;
-    if (row < nrows) qs.put(row, k, q[r]);
+    if (row < nrows) qp[r][k * qstride] = q[r];
   }
 #pragma unroll
   for (int j = 1; j < W; ++j) {
@@ -230,21 +230,28 @@ template <int NT, int RPT>
 __device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int w,
                                              const QSink& qs, float* Rdst, long long ldR,
                                              bool check, int* status, int col0, float* red) {
+  float* qp[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int row = threadIdx.x + r * NT;
+    qp[r] = qs.base(row < nrows ? row : 0);
+  }
+  const int qstride = qs.stride();
   int buf = 0;
   for (int k = 0; k < w; ++k) {
     const int act = w - k;
     if (act > 16)
-      mgs_step<NT, RPT, 32>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
     else if (act > 8)
-      mgs_step<NT, RPT, 16>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
     else if (act > 4)
-      mgs_step<NT, RPT, 8>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
     else if (act > 2)
-      mgs_step<NT, RPT, 4>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
     else if (act > 1)
-      mgs_step<NT, RPT, 2>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
     else
-      mgs_step<NT, RPT, 1>(x, nrows, w, k, qs, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
   }
 }
 

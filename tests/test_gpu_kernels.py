@@ -120,7 +120,7 @@ def test_panel_vs_oracle(tq, m, w, br):
     assert np.linalg.norm(a - q @ r) / np.linalg.norm(a) < 1e-6
 
 
-@pytest.mark.parametrize("m,br", [(1024, 256), (4096, 1024), (1024, 1024), (16384, 256)])
+@pytest.mark.parametrize("m,br", [(1024, 256), (4096, 1024), (1024, 1024), (16384, 1024)])
 def test_panel_planted_hadamard_bitwise(tq, m, br):
     # block rows, rank-local rows and the number of stacked R's are powers of 4
     a, qt, r0 = W.planted_hadamard(m, 32, seed=201)

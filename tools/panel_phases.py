@@ -13,15 +13,15 @@ import workloads as W  # noqa: E402
 tq.init(0)
 L = tq.lib()
 L.tcqr_debug_panel_timestamps.argtypes = [ctypes.c_void_p]
-for m in (32768, 8192, 1024):
+for m, br in ((32768, 1024), (32768, 256), (8192, 1024), (1024, 1024)):
     dbg = torch.zeros(64, dtype=torch.int64, device="cuda")
     L.tcqr_debug_panel_timestamps(ctypes.c_void_p(dbg.data_ptr()))
     X = W.gaussian_cuda(m, 32, 3)
     for _ in range(3):
         dbg.zero_()
-        tq.panel_qr(X.clone(), br=256)
+        tq.panel_qr(X.clone(), br=br)
     torch.cuda.synchronize()
     d = dbg.cpu().numpy()
     t0 = int(d[0])
-    print(m, {i: round((int(v) - t0) / 1000.0, 2) for i, v in enumerate(d) if v})
+    print(m, br, {i: round((int(v) - t0) / 1000.0, 2) for i, v in enumerate(d) if v})
 L.tcqr_debug_panel_timestamps(None)
