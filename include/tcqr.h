@@ -59,7 +59,7 @@ typedef struct tcqr_config {
                         B200, reading R-A6; 64..1024, multiple of 32)                        */
   int col_scaling;   /* 1: per-column power-of-two FP16 range guard (reading R-A4; default 1) */
   int restart;       /* 1: FP64 target, one CGLS restart from the true residual (R-A12)        */
-  double tol2;       /* restart-pass tolerance (default 1e-6, R-A12)                           */
+  double tol2;       /* restart-pass tolerance (default 1e-8, R-A12 as calibrated on this path)*/
   int stag_window;   /* stagnation window W (default 10, R-A11)                                */
   double stag_floor; /* stagnation floor relative to pass 1's ||s0|| (default 1e-11, R-A11)    */
   int use_graphs;    /* 1: capture the factorization into a CUDA graph and replay (default 1)  */

@@ -27,12 +27,23 @@ __global__ void __launch_bounds__(256) f32_tn_kernel(int m, int h, int w2,
     for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
   for (long long c0 = r0; c0 < r1; c0 += kTnRows) {
     __syncthreads();
-    for (int e = tid; e < kTnRows * 64; e += 256) {
+    // all 32 loads of this thread in flight before any shared store (latency-bound otherwise)
+    float qv_[16], av_[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + u * 256;
       const int rr = e & (kTnRows - 1), cc = e / kTnRows;
       const long long row = c0 + rr;
       const bool rok = row < r1;
-      Qs[rr][cc] = (rok && cc < h) ? Q1[row + cc * ldq] : 0.f;
-      As[rr][cc] = (rok && cc < w2) ? A2[row + cc * lda] : 0.f;
+      qv_[u] = (rok && cc < h) ? __ldg(Q1 + row + cc * ldq) : 0.f;
+      av_[u] = (rok && cc < w2) ? __ldg(A2 + row + cc * lda) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + u * 256;
+      const int rr = e & (kTnRows - 1), cc = e / kTnRows;
+      Qs[rr][cc] = qv_[u];
+      As[rr][cc] = av_[u];
     }
     __syncthreads();
 #pragma unroll 4
@@ -117,23 +128,30 @@ __global__ void __launch_bounds__(128) f32_nn_kernel(int m, int h, int w2,
   float acc[W2];
 #pragma unroll
   for (int j = 0; j < W2; ++j) acc[j] = 0.f;
-  for (int i = 0; i < h; ++i) {
-    const float q = Q1[row + (long long)i * ldq];
+  for (int i0 = 0; i0 < h; i0 += 8) {
+    float qb[8];
 #pragma unroll
-    for (int j = 0; j < W2; j += 4) {
-      const float4 tv = *reinterpret_cast<const float4*>(&Ts[i][j]);
-      acc[j] = fmaf(q, tv.x, acc[j]);
-      acc[j + 1] = fmaf(q, tv.y, acc[j + 1]);
-      acc[j + 2] = fmaf(q, tv.z, acc[j + 2]);
-      acc[j + 3] = fmaf(q, tv.w, acc[j + 3]);
+    for (int u = 0; u < 8; ++u) qb[u] = (i0 + u < h) ? __ldg(Q1 + row + (long long)(i0 + u) * ldq) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (i0 + u < h) {
+#pragma unroll
+        for (int j = 0; j < W2; j += 4) {
+          const float4 tv = *reinterpret_cast<const float4*>(&Ts[i0 + u][j]);
+          acc[j] = fmaf(qb[u], tv.x, acc[j]);
+          acc[j + 1] = fmaf(qb[u], tv.y, acc[j + 1]);
+          acc[j + 2] = fmaf(qb[u], tv.z, acc[j + 2]);
+          acc[j + 3] = fmaf(qb[u], tv.w, acc[j + 3]);
+        }
+      }
     }
   }
+  float cold[W2];
+#pragma unroll
+  for (int j = 0; j < W2; ++j) cold[j] = (j < w2) ? A2[row + (long long)j * lda] : 0.f;
 #pragma unroll
   for (int j = 0; j < W2; ++j)
-    if (j < w2) {
-      float* p = A2 + row + (long long)j * lda;
-      *p = *p - acc[j];
-    }
+    if (j < w2) A2[row + (long long)j * lda] = cold[j] - acc[j];
 }
 
 cudaError_t f32_nn_update(int m, int h, int w2, const float* Q1, long long ldq, const float* T,

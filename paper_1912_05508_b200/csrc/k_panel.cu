@@ -258,7 +258,7 @@ __device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int
 template <int NT, int RPT>
 struct FusedShape {
   static constexpr int CAP = NT * RPT;
-  static constexpr int SMEM = (int)sizeof(float) * (CAP * 33 + 3 * 32 * 33 + 2 * (NT / 32) * 32);
+  static constexpr int SMEM = (int)sizeof(float) * (CAP * 33 + 3 * 32 * 36 + 2 * (NT / 32) * 32) + 16;
 };
 
 // Balanced row blocks: block b covers [b*m/nb, (b+1)*m/nb), every block <= br rows (Eq. (6) is
@@ -271,11 +271,11 @@ template <int NT, int RPT>
 __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
   using Sh = FusedShape<NT, RPT>;
   extern __shared__ float fsm[];
-  float* qA = fsm;                 // level-1 Q_b [CAP][33]
-  float* T = qA + Sh::CAP * 33;    // [32][33]
-  float* T2 = T + 32 * 33;         // [32][33]
-  float* Sst = T2 + 32 * 33;       // [32][33] staged stack-Q slice
-  float* red = Sst + 32 * 33;      // [2][NT/32][32]
+  float* qA = fsm;                                     // Q of the current MGS [CAP][33]
+  float* T = fsm + ((Sh::CAP * 33 + 3) & ~3);          // [32][36] (16-byte aligned rows)
+  float* T2 = T + 32 * 36;                             // [32][36]
+  float* Sst = T2 + 32 * 36;                           // [32][36] staged stack-Q slice
+  float* red = Sst + 32 * 36;                          // [2][NT/32][32]
   __shared__ int s_last;
   const int b = blockIdx.x, w = a.w;
   const int row0 = blk_row(b, a.m, a.nb);
@@ -298,6 +298,16 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
   mgs_rotating<NT, RPT>(x, nrows, w, QSink{qA, nullptr, w}, Rb, single ? a.ldr : w,
                         single && a.root_is_global, a.status, a.col0, red);
   if (b == 0) DBG_T(2);
+  if (!single) {
+    // local Q_b -> X (re-read by step 4), so shared memory is free for the stack levels
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = threadIdx.x + r * NT;
+      if (i < nrows)
+        for (int j = 0; j < w; ++j) a.X[(long long)(row0 + i) + (long long)j * a.ldx] = qA[i * 33 + j];
+    }
+  }
 
   // ---- steps 2-3: the last child to arrive factors each tree node ----
   int node = b;
@@ -327,8 +337,22 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
     const bool top = (l == a.L);
     float* Rn = top ? a.Rout : a.Rbuf[l] + (long long)parent * w * w;
     DBG_T(9 + 4 * l);
-    mgs_rotating<NT, RPT>(x, srows, w, QSink{nullptr, a.Qst[l] + (long long)first * w * w, w}, Rn,
-                          top ? a.ldr : w, top && a.root_is_global, a.status, a.col0, red);
+    __syncthreads();
+    mgs_rotating<NT, RPT>(x, srows, w, QSink{qA, nullptr, w}, Rn, top ? a.ldr : w,
+                          top && a.root_is_global, a.status, a.col0, red);
+    __syncthreads();
+    {  // stack Q -> per-child w x w slices (column-major) of Qst[l]
+      float* Qd = a.Qst[l] + (long long)first * w * w;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int sr = threadIdx.x + r * NT;
+        if (sr < srows) {
+          const int ci = sr / w, aa = sr - ci * w;
+          float* dst = Qd + (long long)ci * w * w + aa;
+          for (int j = 0; j < w; ++j) dst[(long long)j * w] = qA[sr * 33 + j];
+        }
+      }
+    }
     DBG_T(10 + 4 * l);
     node = parent;
     root = top;
@@ -350,25 +374,25 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
     int idx = b;
     for (int e = threadIdx.x; e < 32 * 32; e += NT) {
       const int i = e & 31, j = e >> 5;
-      T[i * 33 + j] = (i < w && j < w) ? __ldcg(a.Qst[1] + (long long)idx * w * w + i + j * w) : 0.f;
+      T[i * 36 + j] = (i < w && j < w) ? __ldcg(a.Qst[1] + (long long)idx * w * w + i + j * w) : 0.f;
     }
     for (int l = 2; l <= a.L; ++l) {
       idx /= a.F;
       const float* S = a.Qst[l] + (long long)idx * w * w;
       for (int e = threadIdx.x; e < 32 * 32; e += NT) {
         const int i = e & 31, j = e >> 5;
-        Sst[i * 33 + j] = (i < w && j < w) ? __ldcg(S + i + j * w) : 0.f;
+        Sst[i * 36 + j] = (i < w && j < w) ? __ldcg(S + i + j * w) : 0.f;
       }
       __syncthreads();
       for (int e = threadIdx.x; e < 32 * 32; e += NT) {
         const int i = e & 31, j = e >> 5;
         float acc = 0.f;
 #pragma unroll 8
-        for (int t = 0; t < 32; ++t) acc = fmaf(T[i * 33 + t], Sst[t * 33 + j], acc);
-        T2[i * 33 + j] = acc;
+        for (int t = 0; t < 32; ++t) acc = fmaf(T[i * 36 + t], Sst[t * 36 + j], acc);
+        T2[i * 36 + j] = acc;
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < 32 * 32; e += NT) T[(e & 31) * 33 + (e >> 5)] = T2[(e & 31) * 33 + (e >> 5)];
+      for (int e = threadIdx.x; e < 32 * 32; e += NT) T[(e & 31) * 36 + (e >> 5)] = T2[(e & 31) * 36 + (e >> 5)];
     }
     __syncthreads();
   }
@@ -378,20 +402,30 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
   for (int r = 0; r < RPT; ++r) {
     const int i = threadIdx.x + r * NT;
     if (i >= nrows) continue;
+    const long long gi = (long long)(row0 + i);
     float y[32];
     if (single) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) y[j] = qA[i * 33 + j];
     } else {
+      float xr[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) xr[j] = (j < w) ? a.X[gi + (long long)j * a.ldx] : 0.f;
 #pragma unroll
       for (int j = 0; j < 32; ++j) y[j] = 0.f;
-      for (int l_ = 0; l_ < w; ++l_) {
-        const float ql = qA[i * 33 + l_];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) y[j] = fmaf(ql, T[l_ * 33 + j], y[j]);
+      for (int l_ = 0; l_ < 32; ++l_) {
+        const float ql = xr[l_];
+#pragma unroll
+        for (int j4 = 0; j4 < 32; j4 += 4) {
+          const float4 tv = *reinterpret_cast<const float4*>(T + l_ * 36 + j4);
+          y[j4] = fmaf(ql, tv.x, y[j4]);
+          y[j4 + 1] = fmaf(ql, tv.y, y[j4 + 1]);
+          y[j4 + 2] = fmaf(ql, tv.z, y[j4 + 2]);
+          y[j4 + 3] = fmaf(ql, tv.w, y[j4 + 3]);
+        }
       }
     }
-    const long long gi = (long long)(row0 + i);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       if (j < w) {

@@ -567,7 +567,7 @@ void tcqr_default_config(tcqr_config_t* c) {
   c->panel_rows = 1024;
   c->col_scaling = 1;
   c->restart = 1;
-  c->tol2 = 1e-6;
+  c->tol2 = 1e-8;
   c->stag_window = 10;
   c->stag_floor = 1e-11;
   c->use_graphs = 1;
