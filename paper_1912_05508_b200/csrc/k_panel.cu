@@ -229,7 +229,8 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
 template <int NT, int RPT>
 __device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int w,
                                              const QSink& qs, float* Rdst, long long ldR,
-                                             bool check, int* status, int col0, float* red) {
+                                             bool check, int* status, int col0, float* red,
+                                             unsigned long long* dbg = nullptr) {
   float* qp[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -239,6 +240,7 @@ __device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int
   const int qstride = qs.stride();
   int buf = 0;
   for (int k = 0; k < w; ++k) {
+    if (dbg && threadIdx.x == 0) dbg[k] = gtimer();
     const int act = w - k;
     if (act > 16)
       mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
@@ -296,7 +298,8 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
   float* Rb = single ? a.Rout : a.Rbuf[0] + (long long)b * w * w;
   if (b == 0) DBG_T(1);
   mgs_rotating<NT, RPT>(x, nrows, w, QSink{qA, nullptr, w}, Rb, single ? a.ldr : w,
-                        single && a.root_is_global, a.status, a.col0, red);
+                        single && a.root_is_global, a.status, a.col0, red,
+                        (a.dbg && b == 0) ? a.dbg + 32 : nullptr);
   if (b == 0) DBG_T(2);
   if (!single) {
     // local Q_b -> X (re-read by step 4), so shared memory is free for the stack levels
@@ -339,7 +342,8 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
     DBG_T(9 + 4 * l);
     __syncthreads();
     mgs_rotating<NT, RPT>(x, srows, w, QSink{qA, nullptr, w}, Rn, top ? a.ldr : w,
-                          top && a.root_is_global, a.status, a.col0, red);
+                          top && a.root_is_global, a.status, a.col0, red,
+                          a.dbg ? a.dbg + 64 : nullptr);
     __syncthreads();
     {  // stack Q -> per-child w x w slices (column-major) of Qst[l]
       float* Qd = a.Qst[l] + (long long)first * w * w;

@@ -14,7 +14,7 @@ tq.init(0)
 L = tq.lib()
 L.tcqr_debug_panel_timestamps.argtypes = [ctypes.c_void_p]
 for m, br in ((32768, 1024), (32768, 256), (8192, 1024), (1024, 1024)):
-    dbg = torch.zeros(64, dtype=torch.int64, device="cuda")
+    dbg = torch.zeros(128, dtype=torch.int64, device="cuda")
     L.tcqr_debug_panel_timestamps(ctypes.c_void_p(dbg.data_ptr()))
     X = W.gaussian_cuda(m, 32, 3)
     for _ in range(3):
@@ -23,5 +23,9 @@ for m, br in ((32768, 1024), (32768, 256), (8192, 1024), (1024, 1024)):
     torch.cuda.synchronize()
     d = dbg.cpu().numpy()
     t0 = int(d[0])
-    print(m, br, {i: round((int(v) - t0) / 1000.0, 2) for i, v in enumerate(d) if v})
+    print(m, br, {i: round((int(v) - t0) / 1000.0, 2) for i, v in enumerate(d[:32]) if v})
+    l1 = [int(v) for v in d[32:64] if v]
+    l2 = [int(v) for v in d[64:96] if v]
+    print("  level-1 step us:", [round((b - a) / 1000, 2) for a, b in zip(l1, l1[1:])])
+    print("  stack   step us:", [round((b - a) / 1000, 2) for a, b in zip(l2, l2[1:])])
 L.tcqr_debug_panel_timestamps(None)
