@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
   const int row0 = blk_row(b, a.m, a.nb);
   const int nrows = blk_row(b + 1, a.m, a.nb) - row0;
 
-  // ---- step 1: Alg. 4 on this row block ----
+  // ---- step 1: Alg. 4 on this row block; steps 2-3: the last child to arrive factors each
+  // tree node (single MGS call site so the step body is instantiated once) ----
   if (b == 0) DBG_T(0);
   float x[RPT][32];
 #pragma unroll
@@ -295,71 +296,70 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
       x[r][j] = (ok && j < w) ? a.X[(long long)(row0 + i) + (long long)j * a.ldx] : 0.f;
   }
   const bool single = (a.L == 0);
-  float* Rb = single ? a.Rout : a.Rbuf[0] + (long long)b * w * w;
-  if (b == 0) DBG_T(1);
-  mgs_rotating<NT, RPT>(x, nrows, w, QSink{qA, nullptr, w}, Rb, single ? a.ldr : w,
-                        single && a.root_is_global, a.status, a.col0, red,
-                        (a.dbg && b == 0) ? a.dbg + 32 : nullptr);
-  if (b == 0) DBG_T(2);
-  if (!single) {
-    // local Q_b -> X (re-read by step 4), so shared memory is free for the stack levels
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const int i = threadIdx.x + r * NT;
-      if (i < nrows)
-        for (int j = 0; j < w; ++j) a.X[(long long)(row0 + i) + (long long)j * a.ldx] = qA[i * 33 + j];
-    }
-  }
-
-  // ---- steps 2-3: the last child to arrive factors each tree node ----
-  int node = b;
+  int node = b, level = 0, rows_now = nrows, first = 0;
   bool root = single;
-  for (int l = 1; l <= a.L; ++l) {
-    __threadfence();
-    __syncthreads();
-    const int parent = node / a.F;
-    const int first = parent * a.F;
-    const int nchild = min(a.F, a.nodes[l - 1] - first);
-    if (threadIdx.x == 0) s_last = (atomicAdd(a.cnt[l] + parent, 1) == nchild - 1);
-    __syncthreads();
-    if (!s_last) break;
-    __threadfence();
-    DBG_T(8 + 4 * l);
-    const int srows = nchild * w;
-    const float* Rc = a.Rbuf[l - 1] + (long long)first * w * w;
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const int s = threadIdx.x + r * NT;
-      const bool ok = s < srows;
-      const int ci = ok ? s / w : 0, aa = ok ? s - ci * w : 0;
-      const float* src = Rc + (long long)ci * w * w + aa;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) x[r][j] = (ok && j < w) ? __ldcg(src + (long long)j * w) : 0.f;
-    }
-    const bool top = (l == a.L);
-    float* Rn = top ? a.Rout : a.Rbuf[l] + (long long)parent * w * w;
-    DBG_T(9 + 4 * l);
-    __syncthreads();
-    mgs_rotating<NT, RPT>(x, srows, w, QSink{qA, nullptr, w}, Rn, top ? a.ldr : w,
+  while (true) {
+    const bool top = (level == a.L);
+    float* Rn = top ? a.Rout : a.Rbuf[level] + (long long)node * w * w;
+    if (b == 0 && level == 0) DBG_T(1);
+    mgs_rotating<NT, RPT>(x, rows_now, w, QSink{qA, nullptr, w}, Rn, top ? a.ldr : w,
                           top && a.root_is_global, a.status, a.col0, red,
-                          a.dbg ? a.dbg + 64 : nullptr);
+                          a.dbg ? (level == 0 ? (b == 0 ? a.dbg + 32 : nullptr) : a.dbg + 64)
+                                : nullptr);
     __syncthreads();
-    {  // stack Q -> per-child w x w slices (column-major) of Qst[l]
-      float* Qd = a.Qst[l] + (long long)first * w * w;
+    if (level == 0) {
+      if (b == 0) DBG_T(2);
+      if (single) break;
+      // local Q_b -> X (re-read by step 4), so shared memory is free for the stack levels
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = threadIdx.x + r * NT;
+        if (i < nrows)
+          for (int j = 0; j < w; ++j) a.X[(long long)(row0 + i) + (long long)j * a.ldx] = qA[i * 33 + j];
+      }
+    } else {
+      // stack Q -> per-child w x w slices (column-major) of Qst[level]
+      float* Qd = a.Qst[level] + (long long)first * w * w;
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         const int sr = threadIdx.x + r * NT;
-        if (sr < srows) {
+        if (sr < rows_now) {
           const int ci = sr / w, aa = sr - ci * w;
           float* dst = Qd + (long long)ci * w * w + aa;
           for (int j = 0; j < w; ++j) dst[(long long)j * w] = qA[sr * 33 + j];
         }
       }
+      DBG_T(10 + 4 * level);
+      if (top) {
+        root = true;
+        break;
+      }
     }
-    DBG_T(10 + 4 * l);
+    // arrive at the parent; continue only if this CTA completed it
+    __threadfence();
+    __syncthreads();
+    const int parent = node / a.F;
+    first = parent * a.F;
+    const int nchild = min(a.F, a.nodes[level] - first);
+    if (threadIdx.x == 0) s_last = (atomicAdd(a.cnt[level + 1] + parent, 1) == nchild - 1);
+    __syncthreads();
+    if (!s_last) break;
+    __threadfence();
+    ++level;
     node = parent;
-    root = top;
+    DBG_T(8 + 4 * level);
+    rows_now = nchild * w;
+    const float* Rc = a.Rbuf[level - 1] + (long long)first * w * w;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int sr = threadIdx.x + r * NT;
+      const bool ok = sr < rows_now;
+      const int ci = ok ? sr / w : 0, aa = ok ? sr - ci * w : 0;
+      const float* src = Rc + (long long)ci * w * w + aa;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[r][j] = (ok && j < w) ? __ldcg(src + (long long)j * w) : 0.f;
+    }
+    DBG_T(9 + 4 * level);
   }
   if (root && !single) {
     __threadfence();
