@@ -203,7 +203,11 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
   const bool zero = !(rkk > 0.f) || !isfinite(rkk);
   if (check && zero && threadIdx.x == 0 && status) atomicMin(status, col0 + k + 1);
   const int jl = lane & (W - 1);
-  const float rkj = zero ? 0.f : (jl == 0 ? rkk : tot / rkk);
+  // Q(:,k)/R(k,k) and the R(k,j) quotients use one correctly rounded reciprocal: the IEEE
+  // divide's FCHK slow path fires on zero dividends (half of every stacked-triangle level) and
+  // made those steps 1.6x slower (tools/micro/mgs_step2.cu).  <= 1 extra rounding.
+  const float inv = zero ? 0.f : __frcp_rn(rkk);
+  const float rkj = zero ? 0.f : (jl == 0 ? rkk : tot * inv);
   if (warp == 0) {
     if (lane < w - k && lane < W) Rdst[k + (long long)(k + lane) * ldR] = rkj;
     if (lane < k) Rdst[k + (long long)lane * ldR] = 0.f;
@@ -211,7 +215,7 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
   float q[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
-    q[r] = zero ? 0.f : x[r][0] / rkk;
+    q[r] = x[r][0] * inv;
     const int row = threadIdx.x + r * NT;
     if (row < nrows) qp[r][k * qstride] = q[r];
   }
@@ -370,7 +374,7 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
   // ---- step 4: T_b = S1[b] S2[b/F] ... ; Q_b <- Q_b T_b ----
   if (!single) {
     if (threadIdx.x == 0) {
-      while (ld_relaxed(a.done) == 0) __nanosleep(32);
+      while (ld_relaxed(a.done) == 0) __nanosleep(64);
       __threadfence();
     }
     __syncthreads();

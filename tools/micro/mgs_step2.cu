@@ -2,6 +2,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
+__device__ int g_divmode = 0;
 // Lane l ends with the warp sum of v[l % W] (all lanes that share l % W hold the same value).
 template <int W>
 __device__ __forceinline__ float tr_reduce(float (&v)[32]) {
@@ -42,11 +43,16 @@ __device__ __forceinline__ void step(float (&x)[RPT][32], float* red, int& buf, 
   for (int v = 0; v < NT / 32; ++v) tot += red[(buf * (NT / 32) + v) * 32 + lane];
   buf ^= 1;
   const float rkk = sqrtf(__shfl_sync(0xffffffffu, tot, 0));
-  const float rkj = ((lane & (W - 1)) == 0) ? rkk : tot / rkk;
-  float q[RPT];
+  const int dm = g_divmode;
+  float rkj, q[RPT];
+  if (dm == 0) rkj = ((lane & (W - 1)) == 0) ? rkk : tot / rkk;
+  else if (dm == 1) { const float inv = __frcp_rn(rkk); rkj = ((lane & (W - 1)) == 0) ? rkk : tot * inv; }
+  else { rkj = rkk; if ((lane & (W - 1)) != 0) { rkj = 0.f; if (tot != 0.f) rkj = tot / rkk; } }
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
-    q[r] = x[r][0] / rkk;
+    if (dm == 0) q[r] = x[r][0] / rkk;
+    else if (dm == 1) q[r] = x[r][0] * __frcp_rn(rkk);
+    else { q[r] = 0.f; if (x[r][0] != 0.f) q[r] = x[r][0] / rkk; }
     const int row = threadIdx.x + r * NT;
     if (row < nrows) qs[row * 33 + k] = q[r];
   }
@@ -90,7 +96,7 @@ __global__ void __launch_bounds__(NT) mgs_bench(const float* X, int nrows, int w
 }
 
 template <int NT, int RPT>
-void run() {
+void run(int tri = 0) {
   int nrows = NT * RPT, w = 32;
   float *X, *Q;
   long long* clk;
@@ -99,6 +105,13 @@ void run() {
   cudaMalloc(&clk, sizeof(long long) * 8);
   float* h = new float[nrows * 32];
   for (int i = 0; i < nrows * 32; ++i) h[i] = (float)((i * 7919) % 1000) / 1000.f + (i % 33 == 0);
+  if (tri)  // stack of 32x32 upper triangles (rows a > column j are zero)
+    for (int j = 0; j < 32; ++j)
+      for (int i = 0; i < nrows; ++i) {
+        int a = i % 32;
+        if (a > j) h[i + j * nrows] = 0.f;
+        if (a == j) h[i + j * nrows] += 2.f;
+      }
   cudaMemcpy(X, h, sizeof(float) * nrows * 32, cudaMemcpyHostToDevice);
   int smem = NT * RPT * 33 * 4;
   cudaFuncSetAttribute(mgs_bench<NT, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -125,16 +138,18 @@ void run() {
       double e = fabs(s - (a1 == b1));
       if (e > worst) worst = e;
     }
-  printf("v2 NT=%d RPT=%d rows=%d: %.2f us/launch, 32 steps = %lld cycles (%.0f/step), max|QtQ-I|=%.2e\n",
-         NT, RPT, nrows, ms * 100.f, c, c / 32.0, worst);
+  printf("v2 tri=%d NT=%d RPT=%d rows=%d: %.2f us/launch, 32 steps = %lld cycles (%.0f/step), max|QtQ-I|=%.2e\n",
+         tri, NT, RPT, nrows, ms * 100.f, c, c / 32.0, worst);
 }
 
 int main() {
-  run<128, 2>();
-  run<128, 4>();
-  run<256, 1>();
-  run<256, 2>();
-  run<256, 4>();
-  run<64, 4>();
+  for (int dm = 0; dm < 3; ++dm) {
+    cudaMemcpyToSymbol(g_divmode, &dm, sizeof(int));
+    printf("divmode %d\n", dm);
+    for (int t = 0; t < 2; ++t) {
+      run<128, 2>(t);
+      run<256, 4>(t);
+    }
+  }
   return 0;
 }
