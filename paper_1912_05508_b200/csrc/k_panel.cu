@@ -180,8 +180,8 @@ struct QSink {
 template <int NT, int RPT, int W>
 __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, int k,
                                          float* const (&qp)[RPT], int qstride, float* Rdst,
-                                         long long ldR, bool check, int* status, int col0,
-                                         float* red, int& buf) {
+                                         long long rs, long long cs, bool check, int* status,
+                                         int col0, float* red, int& buf) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float p[32];
@@ -208,9 +208,9 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
   // made those steps 1.6x slower (tools/micro/mgs_step2.cu).  <= 1 extra rounding.
   const float inv = zero ? 0.f : __frcp_rn(rkk);
   const float rkj = zero ? 0.f : (jl == 0 ? rkk : tot * inv);
-  if (warp == 0) {
-    if (lane < w - k && lane < W) Rdst[k + (long long)(k + lane) * ldR] = rkj;
-    if (lane < k) Rdst[k + (long long)lane * ldR] = 0.f;
+  if (warp == 0) {  // R(k, j) at Rdst[k*rs + j*cs]
+    if (lane < w - k && lane < W) Rdst[k * rs + (long long)(k + lane) * cs] = rkj;
+    if (lane < k) Rdst[k * rs + (long long)lane * cs] = 0.f;
   }
   float q[RPT];
 #pragma unroll
@@ -232,9 +232,9 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
 // Alg. 4 on the rows held in x (thread t owns rows t + r*NT): Q columns -> qs, R rows -> Rdst.
 template <int NT, int RPT>
 __device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int w,
-                                             const QSink& qs, float* Rdst, long long ldR,
-                                             bool check, int* status, int col0, float* red,
-                                             unsigned long long* dbg = nullptr) {
+                                             const QSink& qs, float* Rdst, long long rs,
+                                             long long cs, bool check, int* status, int col0,
+                                             float* red, unsigned long long* dbg = nullptr) {
   float* qp[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -247,17 +247,17 @@ __device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int
     if (dbg && threadIdx.x == 0) dbg[k] = gtimer();
     const int act = w - k;
     if (act > 16)
-      mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
     else if (act > 8)
-      mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
     else if (act > 4)
-      mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
     else if (act > 2)
-      mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
     else if (act > 1)
-      mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
     else
-      mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, ldR, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
   }
 }
 
@@ -301,26 +301,21 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
   }
   const bool single = (a.L == 0);
   int node = b, level = 0, rows_now = nrows, first = 0;
-  bool root = single;
+  bool root = single, spilled = false;
   while (true) {
     const bool top = (level == a.L);
+    // node R's are stored ROW-major (stack rows become contiguous 128-byte loads); the final R
+    // is column-major with leading dimension ldr.
     float* Rn = top ? a.Rout : a.Rbuf[level] + (long long)node * w * w;
     if (b == 0 && level == 0) DBG_T(1);
-    mgs_rotating<NT, RPT>(x, rows_now, w, QSink{qA, nullptr, w}, Rn, top ? a.ldr : w,
-                          top && a.root_is_global, a.status, a.col0, red,
+    mgs_rotating<NT, RPT>(x, rows_now, w, QSink{qA, nullptr, w}, Rn, top ? 1 : w,
+                          top ? a.ldr : 1, top && a.root_is_global, a.status, a.col0, red,
                           a.dbg ? (level == 0 ? (b == 0 ? a.dbg + 32 : nullptr) : a.dbg + 64)
                                 : nullptr);
     __syncthreads();
     if (level == 0) {
       if (b == 0) DBG_T(2);
       if (single) break;
-      // local Q_b -> X (re-read by step 4), so shared memory is free for the stack levels
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const int i = threadIdx.x + r * NT;
-        if (i < nrows)
-          for (int j = 0; j < w; ++j) a.X[(long long)(row0 + i) + (long long)j * a.ldx] = qA[i * 33 + j];
-      }
     } else {
       // stack Q -> per-child w x w slices (column-major) of Qst[level]
       float* Qd = a.Qst[level] + (long long)first * w * w;
@@ -349,19 +344,43 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
     __syncthreads();
     if (!s_last) break;
     __threadfence();
+    if (level == 0) {
+      // this CTA climbs the tree: park its local Q_b in X (re-read by step 4) so shared memory
+      // is free for the stack levels; the other CTAs keep Q_b in shared memory.
+      spilled = true;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = threadIdx.x + r * NT;
+        if (i < nrows)
+          for (int j = 0; j < w; ++j) a.X[(long long)(row0 + i) + (long long)j * a.ldx] = qA[i * 33 + j];
+      }
+    }
     ++level;
     node = parent;
     DBG_T(8 + 4 * level);
     rows_now = nchild * w;
+    // stack row sr = child sr / w, row sr % w of its row-major R: w contiguous floats
     const float* Rc = a.Rbuf[level - 1] + (long long)first * w * w;
+    const bool vec = (w == 32);
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int sr = threadIdx.x + r * NT;
       const bool ok = sr < rows_now;
-      const int ci = ok ? sr / w : 0, aa = ok ? sr - ci * w : 0;
-      const float* src = Rc + (long long)ci * w * w + aa;
+      const float* src = Rc + (long long)(ok ? sr : 0) * w;
+      if (vec) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) x[r][j] = (ok && j < w) ? __ldcg(src + (long long)j * w) : 0.f;
+        for (int j4 = 0; j4 < 32; j4 += 4) {
+          const float4 v = ok ? __ldcg(reinterpret_cast<const float4*>(src + j4))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[r][j4] = v.x;
+          x[r][j4 + 1] = v.y;
+          x[r][j4 + 2] = v.z;
+          x[r][j4 + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[r][j] = (ok && j < w) ? __ldcg(src + j) : 0.f;
+      }
     }
     DBG_T(9 + 4 * level);
   }
@@ -417,8 +436,13 @@ __global__ void __launch_bounds__(NT, 1) panel_fused_kernel(FusedPanelArgs a) {
       for (int j = 0; j < 32; ++j) y[j] = qA[i * 33 + j];
     } else {
       float xr[32];
+      if (spilled) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) xr[j] = (j < w) ? a.X[gi + (long long)j * a.ldx] : 0.f;
+        for (int j = 0; j < 32; ++j) xr[j] = (j < w) ? a.X[gi + (long long)j * a.ldx] : 0.f;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) xr[j] = qA[i * 33 + j];
+      }
 #pragma unroll
       for (int j = 0; j < 32; ++j) y[j] = 0.f;
 #pragma unroll
@@ -483,8 +507,8 @@ __global__ void __launch_bounds__(kLvlNT) panel_mgs_kernel(
   }
   float* Rdst = (nb == 1) ? Rout : S + (long long)b * w;
   const long long ldR = (nb == 1) ? ldr : lds;
-  mgs_rotating<kLvlNT, kLvlRPT>(x, nrows, w, QSink{qs, nullptr, w}, Rdst, ldR, top != 0, status,
-                                col0, red);
+  mgs_rotating<kLvlNT, kLvlRPT>(x, nrows, w, QSink{qs, nullptr, w}, Rdst, 1, ldR, top != 0,
+                                status, col0, red);
   __syncthreads();
   for (int r = 0; r < kLvlRPT; ++r) {
     const int i = threadIdx.x + r * kLvlNT;
