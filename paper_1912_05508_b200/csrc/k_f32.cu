@@ -165,4 +165,204 @@ cudaError_t f32_nn_update(int m, int h, int w2, const float* Q1, long long ldq, 
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Fused projection (one cooperative launch): R12 = Q1' A2 (deterministic), R block <- R12,
+// A2 -= Q1 R12.  CTA b owns rows [b m / G, (b+1) m / G).
+//   phase 1  partial P_b = Q1_b' A2_b (same micro-tiles as f32_tn_kernel)
+//   barrier
+//   phase 2  CTA b sums its slice of the h*w2 entries over all G partials in a fixed order
+//   barrier
+//   phase 3  A2_b -= Q1_b R12 (R12 staged in shared memory)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ int ld_relaxed_i(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Sense-free grid barrier: bar[0] arrival counter (returns to 0), bar[1] generation.
+__device__ __forceinline__ void grid_barrier(int* bar, int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int g = ld_relaxed_i(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      st_release_i(bar + 1, g + 1);
+    } else {
+      while (ld_relaxed_i(bar + 1) == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w2,
+                                                             const float* __restrict__ Q1,
+                                                             long long ldq, float* A2,
+                                                             long long lda, float* Rblk,
+                                                             long long ldr, float* P, float* T,
+                                                             int* bar) {
+  __shared__ __align__(16) float Qs[kTnRows][kTnPad];
+  __shared__ __align__(16) float As[kTnRows][kTnPad];
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long r0 = (long long)b * m / G, r1 = (long long)(b + 1) * m / G;
+  const int tid = threadIdx.x, grp = tid >> 6, t = tid & 63, ti = t & 7, tj = t >> 3;
+  const int hw = h * w2;
+  // ---- phase 1 ----
+  {
+    float acc[8][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[a][c] = 0.f;
+    for (long long c0 = r0; c0 < r1; c0 += kTnRows) {
+      __syncthreads();
+      float qv_[16], av_[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = tid + u * 256;
+        const int rr = e & (kTnRows - 1), cc = e / kTnRows;
+        const long long row = c0 + rr;
+        const bool rok = row < r1;
+        qv_[u] = (rok && cc < h) ? __ldg(Q1 + row + cc * ldq) : 0.f;
+        av_[u] = (rok && cc < w2) ? A2[row + cc * lda] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = tid + u * 256;
+        const int rr = e & (kTnRows - 1), cc = e / kTnRows;
+        Qs[rr][cc] = qv_[u];
+        As[rr][cc] = av_[u];
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int rr = grp; rr < kTnRows; rr += 4) {
+        const float4 q0 = *reinterpret_cast<const float4*>(&Qs[rr][ti * 8]);
+        const float4 q1 = *reinterpret_cast<const float4*>(&Qs[rr][ti * 8 + 4]);
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[rr][tj * 8]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[rr][tj * 8 + 4]);
+        const float qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[a][c] = fmaf(qv[a], av[c], acc[a][c]);
+      }
+    }
+    __syncthreads();
+    float* red = &Qs[0][0];
+    for (int g = 0; g < 4; ++g) {
+      if (grp == g) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float* p = red + (ti * 8 + a) * kTnPad + tj * 8 + c;
+            *p = (g == 0) ? acc[a][c] : *p + acc[a][c];
+          }
+      }
+      __syncthreads();
+    }
+    float* out = P + (long long)b * hw;
+    for (int e = tid; e < hw; e += 256) {
+      const int i = e % h, j = e / h;
+      out[e] = red[i * kTnPad + j];
+    }
+  }
+  grid_barrier(bar, G);
+  // ---- phase 2: fixed-order sum of this CTA's slice of entries ----
+  {
+    const int e0 = (int)((long long)b * hw / G), e1 = (int)((long long)(b + 1) * hw / G);
+    for (int e = e0 + tid; e < e1; e += 256) {
+      float s = 0.f;
+      int g = 0;
+      for (; g + 8 <= G; g += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(P + (long long)(g + u) * hw + e);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      for (; g < G; ++g) s += __ldcg(P + (long long)g * hw + e);
+      T[e] = s;
+      const int i = e % h, j = e / h;
+      Rblk[i + (long long)j * ldr] = s;
+    }
+  }
+  grid_barrier(bar, G);
+  // ---- phase 3: A2_b -= Q1_b T ----
+  {
+    float* Ts = &Qs[0][0];  // [h][64] (h <= 64)
+    for (int e = tid; e < h * 64; e += 256) {
+      const int i = e / 64, j = e % 64;
+      Ts[i * 64 + j] = (j < w2) ? __ldcg(T + i + (long long)j * h) : 0.f;
+    }
+    __syncthreads();
+    for (long long row = r0 + tid; row < r1; row += 256) {
+      float acc[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+      for (int i0 = 0; i0 < h; i0 += 8) {
+        float qb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) qb[u] = (i0 + u < h) ? __ldg(Q1 + row + (long long)(i0 + u) * ldq) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0 + u < h) {
+#pragma unroll
+            for (int j = 0; j < 64; j += 4) {
+              const float4 tv = *reinterpret_cast<const float4*>(&Ts[(i0 + u) * 64 + j]);
+              acc[j] = fmaf(qb[u], tv.x, acc[j]);
+              acc[j + 1] = fmaf(qb[u], tv.y, acc[j + 1]);
+              acc[j + 2] = fmaf(qb[u], tv.z, acc[j + 2]);
+              acc[j + 3] = fmaf(qb[u], tv.w, acc[j + 3]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if (j < w2) A2[row + (long long)j * lda] -= acc[j];
+    }
+  }
+}
+
+int f32_project_capacity(int num_sms) {
+  static int per_sm = -1;
+  if (per_sm < 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f32_project_kernel, 256, 0) !=
+          cudaSuccess)
+    per_sm = 0;
+  return per_sm * num_sms;
+}
+
+// One cooperative launch; cudaErrorNotSupported when it cannot be made co-resident.
+cudaError_t f32_project(int m, int h, int w2, const float* Q1, long long ldq, float* A2,
+                        long long lda, float* Rblk, long long ldr, float* T, float* P,
+                        long long p_cap, int* bar, int num_sms, cudaStream_t st) {
+  if (h > 64 || w2 > 64) return cudaErrorNotSupported;
+  int G = (m + 255) / 256;
+  const int cap = f32_project_capacity(num_sms);
+  if (G > cap) G = cap;
+  if ((long long)G * h * w2 > p_cap) G = (int)(p_cap / ((long long)h * w2));
+  if (G < 1) return cudaErrorNotSupported;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, f32_project_kernel, m, h, w2, Q1, ldq, A2, lda, Rblk, ldr, P,
+                            T, bar);
+}
+
 }  // namespace tcqr

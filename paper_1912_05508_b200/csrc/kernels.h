@@ -58,6 +58,11 @@ extern unsigned long long* g_panel_dbg;  // debug: phase timestamps of the fused
 cudaError_t f32_tn(int m, int h, int w2, const float* Q1, long long ldq, const float* A2,
                    long long lda, float* T, float* P, long long p_cap, int num_sms,
                    cudaStream_t st);
+// Fused (one cooperative launch): T = R12 = Q1' A2, R block <- T, A2 -= Q1 T.  bar: two zeroed
+// ints.  cudaErrorNotSupported -> use f32_tn / f32_nn_update.
+cudaError_t f32_project(int m, int h, int w2, const float* Q1, long long ldq, float* A2,
+                        long long lda, float* Rblk, long long ldr, float* T, float* P,
+                        long long p_cap, int* bar, int num_sms, cudaStream_t st);
 // A2 (m x w2) -= Q1 (m x h) T (h x w2, ld h).
 cudaError_t f32_nn_update(int m, int h, int w2, const float* Q1, long long ldq, const float* T,
                           float* A2, long long lda, cudaStream_t st);

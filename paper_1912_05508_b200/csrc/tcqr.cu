@@ -441,6 +441,23 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
       PROF(TCQR_K4_NN, 2.0 * m * h * w2, 2.0 * m * h + 2.0 * h * w2 + 8.0 * m * w2,
            CK(tc_gemm_nn_update(m, h, w2, A1h, ws.ldh, ws.R12h, ldh2, A2, J.ldq,
                                 ws.inv_s2 + c0 + h, c.num_sms, c.stream)));
+    } else if (c.nranks == 1) {
+      // one cooperative launch: R12 = Q1' A2 (deterministic), R block, A2 -= Q1 R12
+      cudaError_t e = cudaErrorNotSupported;
+      PROF(TCQR_K2B_TN, 4.0 * m * h * w2, 8.0 * m * h + 12.0 * m * w2,
+           e = f32_project(m, h, w2, Qc, J.ldq, A2, J.ldq, Rblk, J.ldr, ws.T, ws.P, ws.p_cap,
+                           ws.iws + ws.iws_cap - 8, c.num_sms, c.stream));
+      if (e != cudaSuccess) {
+        if (e != cudaErrorNotSupported) CK(e);
+        cudaGetLastError();
+        PROF(TCQR_K2B_TN, 2.0 * m * h * w2, 4.0 * m * (h + w2),
+             CK(f32_tn(m, h, w2, Qc, J.ldq, A2, J.ldq, ws.T, ws.P, ws.p_cap, c.num_sms,
+                       c.stream)));
+        PROF(TCQR_K3_FINALIZE, 0, 8.0 * h * w2,
+             CK(copy_block(h, w2, ws.T, h, Rblk, J.ldr, c.stream)));
+        PROF(TCQR_K2B_NN, 2.0 * m * h * w2, 4.0 * m * h + 8.0 * m * w2,
+             CK(f32_nn_update(m, h, w2, Qc, J.ldq, ws.T, A2, J.ldq, c.stream)));
+      }
     } else {
       PROF(TCQR_K2B_TN, 2.0 * m * h * w2, 4.0 * m * (h + w2),
            CK(f32_tn(m, h, w2, Qc, J.ldq, A2, J.ldq, ws.T, ws.P, ws.p_cap, c.num_sms,
