@@ -275,23 +275,38 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
     }
   }
   grid_barrier(bar, G);
-  // ---- phase 2: fixed-order sum of this CTA's slice of entries ----
+  // ---- phase 2: fixed-order sum of this CTA's slice of entries: 8 partial-groups x 32 entries
+  // per pass, all loads of a thread in flight, then a fixed-order combine in shared memory ----
   {
     const int e0 = (int)((long long)b * hw / G), e1 = (int)((long long)(b + 1) * hw / G);
-    for (int e = e0 + tid; e < e1; e += 256) {
+    float* part = &As[0][0];  // [8][32]
+    const int el = tid & 31, pg = tid >> 5;
+    const int gper = (G + 7) / 8, g0 = pg * gper, g1 = min(G, g0 + gper);
+    for (int eb = e0; eb < e1; eb += 32) {
+      const int e = eb + el;
       float s = 0.f;
-      int g = 0;
-      for (; g + 8 <= G; g += 8) {
-        float v[8];
+      if (e < e1) {
+        int g = g0;
+        for (; g + 8 <= g1; g += 8) {
+          float v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(P + (long long)(g + u) * hw + e);
+          for (int u = 0; u < 8; ++u) v[u] = __ldcg(P + (long long)(g + u) * hw + e);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
+          for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; g < g1; ++g) s += __ldcg(P + (long long)g * hw + e);
       }
-      for (; g < G; ++g) s += __ldcg(P + (long long)g * hw + e);
-      T[e] = s;
-      const int i = e % h, j = e / h;
-      Rblk[i + (long long)j * ldr] = s;
+      __syncthreads();
+      part[pg * 32 + el] = s;
+      __syncthreads();
+      if (pg == 0 && e < e1) {
+        float tot = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tot += part[q * 32 + el];
+        T[e] = tot;
+        const int i = e % h, j = e / h;
+        Rblk[i + (long long)j * ldr] = tot;
+      }
     }
   }
   grid_barrier(bar, G);
