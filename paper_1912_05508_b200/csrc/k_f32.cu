@@ -201,12 +201,21 @@ __device__ __forceinline__ void grid_barrier(int* bar, int nblocks) {
   __syncthreads();
 }
 
+__device__ __forceinline__ unsigned long long gtimer_f() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+unsigned long long* g_proj_dbg = nullptr;
+
 __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w2,
                                                              const float* __restrict__ Q1,
                                                              long long ldq, float* A2,
                                                              long long lda, float* Rblk,
                                                              long long ldr, float* P, float* T,
-                                                             int* bar) {
+                                                             int* bar, unsigned long long* dbg) {
+#define PDBG(i) if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[i] = gtimer_f();
+  PDBG(0);
   __shared__ __align__(16) float Qs[kTnRows][kTnPad];
   __shared__ __align__(16) float As[kTnRows][kTnPad];
   const int G = gridDim.x, b = blockIdx.x;
@@ -274,7 +283,9 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
       out[e] = red[i * kTnPad + j];
     }
   }
+  PDBG(1);
   grid_barrier(bar, G);
+  PDBG(2);
   // ---- phase 2: fixed-order sum of this CTA's slice of entries: 8 partial-groups x 32 entries
   // per pass, all loads of a thread in flight, then a fixed-order combine in shared memory ----
   {
@@ -309,7 +320,9 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
       }
     }
   }
+  PDBG(3);
   grid_barrier(bar, G);
+  PDBG(4);
   // ---- phase 3: A2_b -= Q1_b T ----
   {
     float* Ts = &Qs[0][0];  // [h][64] (h <= 64)
@@ -345,6 +358,8 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
         if (j < w2) A2[row + (long long)j * lda] -= acc[j];
     }
   }
+  PDBG(5);
+#undef PDBG
 }
 
 int f32_project_capacity(int num_sms) {
@@ -377,7 +392,7 @@ cudaError_t f32_project(int m, int h, int w2, const float* Q1, long long ldq, fl
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, f32_project_kernel, m, h, w2, Q1, ldq, A2, lda, Rblk, ldr, P,
-                            T, bar);
+                            T, bar, g_proj_dbg);
 }
 
 }  // namespace tcqr

@@ -51,7 +51,8 @@ cudaError_t panel_fused(int m, int w, float* X, long long ldx, __half* Xh, long 
 int fused_panel_capacity(int num_sms);
 int fused_panel_smem_bytes();
 int fused_panel_max_rows();
-extern unsigned long long* g_panel_dbg;  // debug: phase timestamps of the fused panel
+extern unsigned long long* g_panel_dbg;
+extern unsigned long long* g_proj_dbg;  // debug: phase timestamps of the FP32 projection  // debug: phase timestamps of the fused panel
 
 // ---- K2b FP32 intra-leaf products (k_f32.cu) ----
 // T (h x w2, ld h) = Q1' A2 over m rows (deterministic split-K with partials in P).

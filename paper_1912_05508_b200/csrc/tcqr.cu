@@ -1037,6 +1037,10 @@ int tcqr_debug_panel_timestamps(void* dptr) {
   g_panel_dbg = static_cast<unsigned long long*>(dptr);
   return 0;
 }
+int tcqr_debug_proj_timestamps(void* dptr) {
+  g_proj_dbg = static_cast<unsigned long long*>(dptr);
+  return 0;
+}
 
 int tcqr_gemv(int trans, int64_t m, int64_t n, const float* A, int64_t lda, const double* v,
               double* y) {
