@@ -208,6 +208,7 @@ __device__ __forceinline__ unsigned long long gtimer_f() {
 }
 unsigned long long* g_proj_dbg = nullptr;
 
+template <int TD>  // TD = 32 or 64: h, w2 <= TD
 __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w2,
                                                              const float* __restrict__ Q1,
                                                              long long ldq, float* A2,
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
                                                              long long ldr, float* P, float* T,
                                                              int* bar, unsigned long long* dbg) {
 #define PDBG(i) if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[i] = gtimer_f();
+  constexpr int MT = TD / 8;  // micro-tile edge
   PDBG(0);
   __shared__ __align__(16) float Qs[kTnRows][kTnPad];
   __shared__ __align__(16) float As[kTnRows][kTnPad];
@@ -222,18 +224,19 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
   const long long r0 = (long long)b * m / G, r1 = (long long)(b + 1) * m / G;
   const int tid = threadIdx.x, grp = tid >> 6, t = tid & 63, ti = t & 7, tj = t >> 3;
   const int hw = h * w2;
-  // ---- phase 1 ----
+  // ---- phase 1: P_b = Q1_b' A2_b ----
   {
-    float acc[8][8];
+    float acc[MT][MT];
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < MT; ++a)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) acc[a][c] = 0.f;
+      for (int c = 0; c < MT; ++c) acc[a][c] = 0.f;
+    constexpr int NL = kTnRows * TD / 256;  // loads per thread per matrix per chunk
     for (long long c0 = r0; c0 < r1; c0 += kTnRows) {
       __syncthreads();
-      float qv_[16], av_[16];
+      float qv_[NL], av_[NL];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < NL; ++u) {
         const int e = tid + u * 256;
         const int rr = e & (kTnRows - 1), cc = e / kTnRows;
         const long long row = c0 + rr;
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
         av_[u] = (rok && cc < w2) ? A2[row + cc * lda] : 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < NL; ++u) {
         const int e = tid + u * 256;
         const int rr = e & (kTnRows - 1), cc = e / kTnRows;
         Qs[rr][cc] = qv_[u];
@@ -251,16 +254,18 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
       __syncthreads();
 #pragma unroll 4
       for (int rr = grp; rr < kTnRows; rr += 4) {
-        const float4 q0 = *reinterpret_cast<const float4*>(&Qs[rr][ti * 8]);
-        const float4 q1 = *reinterpret_cast<const float4*>(&Qs[rr][ti * 8 + 4]);
-        const float4 a0 = *reinterpret_cast<const float4*>(&As[rr][tj * 8]);
-        const float4 a1 = *reinterpret_cast<const float4*>(&As[rr][tj * 8 + 4]);
-        const float qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        float qv[MT], av[MT];
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
+        for (int v4 = 0; v4 < MT; v4 += 4) {
+          const float4 q4 = *reinterpret_cast<const float4*>(&Qs[rr][ti * MT + v4]);
+          const float4 a4 = *reinterpret_cast<const float4*>(&As[rr][tj * MT + v4]);
+          qv[v4] = q4.x; qv[v4 + 1] = q4.y; qv[v4 + 2] = q4.z; qv[v4 + 3] = q4.w;
+          av[v4] = a4.x; av[v4 + 1] = a4.y; av[v4 + 2] = a4.z; av[v4 + 3] = a4.w;
+        }
 #pragma unroll
-          for (int c = 0; c < 8; ++c) acc[a][c] = fmaf(qv[a], av[c], acc[a][c]);
+        for (int a = 0; a < MT; ++a)
+#pragma unroll
+          for (int c = 0; c < MT; ++c) acc[a][c] = fmaf(qv[a], av[c], acc[a][c]);
       }
     }
     __syncthreads();
@@ -268,10 +273,10 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
     for (int g = 0; g < 4; ++g) {
       if (grp == g) {
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
+        for (int a = 0; a < MT; ++a)
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            float* p = red + (ti * 8 + a) * kTnPad + tj * 8 + c;
+          for (int c = 0; c < MT; ++c) {
+            float* p = red + (ti * MT + a) * kTnPad + tj * MT + c;
             *p = (g == 0) ? acc[a][c] : *p + acc[a][c];
           }
       }
@@ -323,49 +328,51 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
   PDBG(3);
   grid_barrier(bar, G);
   PDBG(4);
-  // ---- phase 3: A2_b -= Q1_b T ----
+  // ---- phase 3: A2_b -= Q1_b T  (all loads of a row issued before any store) ----
   {
-    float* Ts = &Qs[0][0];  // [h][64] (h <= 64)
-    for (int e = tid; e < h * 64; e += 256) {
-      const int i = e / 64, j = e % 64;
-      Ts[i * 64 + j] = (j < w2) ? __ldcg(T + i + (long long)j * h) : 0.f;
+    float* Ts = &Qs[0][0];  // [h][TD]
+    for (int e = tid; e < h * TD; e += 256) {
+      const int i = e / TD, j = e % TD;
+      Ts[i * TD + j] = (j < w2) ? __ldcg(T + i + (long long)j * h) : 0.f;
     }
     __syncthreads();
     for (long long row = r0 + tid; row < r1; row += 256) {
-      float acc[64];
+      float cold[TD];
 #pragma unroll
-      for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+      for (int j = 0; j < TD; ++j) cold[j] = (j < w2) ? A2[row + (long long)j * lda] : 0.f;
+      float acc[TD];
+#pragma unroll
+      for (int j = 0; j < TD; ++j) acc[j] = 0.f;
       for (int i0 = 0; i0 < h; i0 += 8) {
         float qb[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) qb[u] = (i0 + u < h) ? __ldg(Q1 + row + (long long)(i0 + u) * ldq) : 0.f;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          if (i0 + u < h) {
 #pragma unroll
-            for (int j = 0; j < 64; j += 4) {
-              const float4 tv = *reinterpret_cast<const float4*>(&Ts[(i0 + u) * 64 + j]);
-              acc[j] = fmaf(qb[u], tv.x, acc[j]);
-              acc[j + 1] = fmaf(qb[u], tv.y, acc[j + 1]);
-              acc[j + 2] = fmaf(qb[u], tv.z, acc[j + 2]);
-              acc[j + 3] = fmaf(qb[u], tv.w, acc[j + 3]);
-            }
+          for (int j = 0; j < TD; j += 4) {
+            const float4 tv = *reinterpret_cast<const float4*>(&Ts[(i0 + u) * TD + j]);
+            acc[j] = fmaf(qb[u], tv.x, acc[j]);
+            acc[j + 1] = fmaf(qb[u], tv.y, acc[j + 1]);
+            acc[j + 2] = fmaf(qb[u], tv.z, acc[j + 2]);
+            acc[j + 3] = fmaf(qb[u], tv.w, acc[j + 3]);
           }
         }
       }
 #pragma unroll
-      for (int j = 0; j < 64; ++j)
-        if (j < w2) A2[row + (long long)j * lda] -= acc[j];
+      for (int j = 0; j < TD; ++j)
+        if (j < w2) A2[row + (long long)j * lda] = cold[j] - acc[j];
     }
   }
   PDBG(5);
 #undef PDBG
 }
 
-int f32_project_capacity(int num_sms) {
+template <int TD>
+static int f32_project_capacity(int num_sms) {
   static int per_sm = -1;
   if (per_sm < 0 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f32_project_kernel, 256, 0) !=
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f32_project_kernel<TD>, 256, 0) !=
           cudaSuccess)
     per_sm = 0;
   return per_sm * num_sms;
@@ -376,8 +383,9 @@ cudaError_t f32_project(int m, int h, int w2, const float* Q1, long long ldq, fl
                         long long lda, float* Rblk, long long ldr, float* T, float* P,
                         long long p_cap, int* bar, int num_sms, cudaStream_t st) {
   if (h > 64 || w2 > 64) return cudaErrorNotSupported;
+  const bool small = (h <= 32 && w2 <= 32);
   int G = (m + 255) / 256;
-  const int cap = f32_project_capacity(num_sms);
+  const int cap = small ? f32_project_capacity<32>(num_sms) : f32_project_capacity<64>(num_sms);
   if (G > cap) G = cap;
   if ((long long)G * h * w2 > p_cap) G = (int)(p_cap / ((long long)h * w2));
   if (G < 1) return cudaErrorNotSupported;
@@ -391,8 +399,10 @@ cudaError_t f32_project(int m, int h, int w2, const float* Q1, long long ldq, fl
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, f32_project_kernel, m, h, w2, Q1, ldq, A2, lda, Rblk, ldr, P,
-                            T, bar, g_proj_dbg);
+  return small ? cudaLaunchKernelEx(&cfg, f32_project_kernel<32>, m, h, w2, Q1, ldq, A2, lda,
+                                    Rblk, ldr, P, T, bar, g_proj_dbg)
+               : cudaLaunchKernelEx(&cfg, f32_project_kernel<64>, m, h, w2, Q1, ldq, A2, lda,
+                                    Rblk, ldr, P, T, bar, g_proj_dbg);
 }
 
 }  // namespace tcqr
