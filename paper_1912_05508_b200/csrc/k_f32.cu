@@ -337,31 +337,34 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
     }
     __syncthreads();
     for (long long row = r0 + tid; row < r1; row += 256) {
-      float cold[TD];
+#pragma unroll 1
+      for (int jh = 0; jh < TD; jh += 32) {  // 32-column halves keep registers bounded
+        float cold[32];
 #pragma unroll
-      for (int j = 0; j < TD; ++j) cold[j] = (j < w2) ? A2[row + (long long)j * lda] : 0.f;
-      float acc[TD];
+        for (int j = 0; j < 32; ++j) cold[j] = (jh + j < w2) ? A2[row + (long long)(jh + j) * lda] : 0.f;
+        float acc[32];
 #pragma unroll
-      for (int j = 0; j < TD; ++j) acc[j] = 0.f;
-      for (int i0 = 0; i0 < h; i0 += 8) {
-        float qb[8];
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        for (int i0 = 0; i0 < h; i0 += 8) {
+          float qb[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) qb[u] = (i0 + u < h) ? __ldg(Q1 + row + (long long)(i0 + u) * ldq) : 0.f;
+          for (int u = 0; u < 8; ++u) qb[u] = (i0 + u < h) ? __ldg(Q1 + row + (long long)(i0 + u) * ldq) : 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < 8; ++u) {
 #pragma unroll
-          for (int j = 0; j < TD; j += 4) {
-            const float4 tv = *reinterpret_cast<const float4*>(&Ts[(i0 + u) * TD + j]);
-            acc[j] = fmaf(qb[u], tv.x, acc[j]);
-            acc[j + 1] = fmaf(qb[u], tv.y, acc[j + 1]);
-            acc[j + 2] = fmaf(qb[u], tv.z, acc[j + 2]);
-            acc[j + 3] = fmaf(qb[u], tv.w, acc[j + 3]);
+            for (int j = 0; j < 32; j += 4) {
+              const float4 tv = *reinterpret_cast<const float4*>(&Ts[(i0 + u) * TD + jh + j]);
+              acc[j] = fmaf(qb[u], tv.x, acc[j]);
+              acc[j + 1] = fmaf(qb[u], tv.y, acc[j + 1]);
+              acc[j + 2] = fmaf(qb[u], tv.z, acc[j + 2]);
+              acc[j + 3] = fmaf(qb[u], tv.w, acc[j + 3]);
+            }
           }
         }
-      }
 #pragma unroll
-      for (int j = 0; j < TD; ++j)
-        if (j < w2) A2[row + (long long)j * lda] = cold[j] - acc[j];
+        for (int j = 0; j < 32; ++j)
+          if (jh + j < w2) A2[row + (long long)(jh + j) * lda] = cold[j] - acc[j];
+      }
     }
   }
   PDBG(5);
