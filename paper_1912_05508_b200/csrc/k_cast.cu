@@ -64,11 +64,94 @@ __global__ void __launch_bounds__(kCastThreads) cast_scale_kernel(
   for (int i = m4 + threadIdx.x; i < m; i += kCastThreads) xh[i] = __float2half_rn(x[i] * s);
 }
 
+// Pass 1 of the parallel cast: per-(row chunk, column) max |x| folded into cmax[j] with an
+// integer atomicMax on the float bits (max is order-independent: deterministic).
+__global__ void __launch_bounds__(256) colmax_kernel(int m, const float* __restrict__ X,
+                                                     long long ldx, unsigned int* cmax,
+                                                     int* status, int col_base, int rows_per) {
+  __shared__ float red[32];
+  const int j = blockIdx.y;
+  const long long r0 = (long long)blockIdx.x * rows_per;
+  const long long r1 = min((long long)m, r0 + rows_per);
+  const float* x = X + (long long)j * ldx;
+  float mx = 0.f;
+  bool bad = false;
+  const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && ((r0 & 3) == 0);
+  long long i = r0;
+  if (vec) {
+    for (long long q = r0 + threadIdx.x * 4; q + 3 < r1; q += 256 * 4) {
+      const float4 v = *reinterpret_cast<const float4*>(x + q);
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+    }
+    i = r0 + ((r1 - r0) & ~3LL);
+  }
+  for (long long q = i + threadIdx.x; q < r1; q += 256) {
+    const float v = x[q];
+    mx = fmaxf(mx, fabsf(v));
+    bad |= !isfinite(v);
+  }
+  if (bad && status) atomicMin(status, col_base + j + 1);
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0 && mx > 0.f) atomicMax(cmax + j, __float_as_uint(mx));
+}
+
+// Pass 2: scaled RNE cast of a (row chunk, column) tile; inv_s written by chunk 0.
+__global__ void __launch_bounds__(256) cast_pass2_kernel(int m, const float* __restrict__ X,
+                                                         long long ldx, __half* __restrict__ Xh,
+                                                         long long ldh,
+                                                         const unsigned int* __restrict__ cmax,
+                                                         float* __restrict__ inv_s, int scaling,
+                                                         int rows_per) {
+  const int j = blockIdx.y;
+  const long long r0 = (long long)blockIdx.x * rows_per;
+  const long long r1 = min((long long)m, r0 + rows_per);
+  const float s = scaling ? pow2_scale_for(__uint_as_float(cmax[j])) : 1.f;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && inv_s) inv_s[j] = 1.f / s;
+  const float* x = X + (long long)j * ldx;
+  __half* xh = Xh + (long long)j * ldh;
+  const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
+                   ((ldh & 3) == 0) && ((reinterpret_cast<uintptr_t>(Xh) & 7) == 0) &&
+                   ((r0 & 3) == 0);
+  long long i = r0;
+  if (vec) {
+    for (long long q = r0 + threadIdx.x * 4; q + 3 < r1; q += 256 * 4) {
+      const float4 v = *reinterpret_cast<const float4*>(x + q);
+      __half2 lo = __floats2half2_rn(v.x * s, v.y * s);
+      __half2 hi = __floats2half2_rn(v.z * s, v.w * s);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(xh + q) = pk;
+    }
+    i = r0 + ((r1 - r0) & ~3LL);
+  }
+  for (long long q = i + threadIdx.x; q < r1; q += 256) xh[q] = __float2half_rn(x[q] * s);
+}
+
 cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
-                       float* inv_s, int scaling, int* status, int col_base, cudaStream_t st) {
+                       float* inv_s, int scaling, int* status, int col_base, unsigned int* cmax,
+                       cudaStream_t st) {
   if (m <= 0 || w <= 0) return cudaSuccess;
-  cast_scale_kernel<<<w, kCastThreads, 0, st>>>(m, X, ldx, Xh, ldh, inv_s, scaling, status,
-                                                 col_base);
+  // Few columns x many rows: split rows (2-D grid, pass 1 = column max via atomicMax).
+  // Many columns: one CTA per column already fills the GPU.
+  if (w >= 1024 || (!scaling && !status) || !cmax) {
+    if (!scaling && !status) {
+      const int rows_per = 8192;
+      dim3 g((m + rows_per - 1) / rows_per, w);
+      cast_pass2_kernel<<<g, 256, 0, st>>>(m, X, ldx, Xh, ldh, nullptr, inv_s, 0, rows_per);
+      return cudaGetLastError();
+    }
+    cast_scale_kernel<<<w, kCastThreads, 0, st>>>(m, X, ldx, Xh, ldh, inv_s, scaling, status,
+                                                   col_base);
+    return cudaGetLastError();
+  }
+  cudaError_t e = cudaMemsetAsync(cmax, 0, sizeof(unsigned int) * w, st);
+  if (e != cudaSuccess) return e;
+  const int rows_per = 8192;
+  dim3 g((m + rows_per - 1) / rows_per, w);
+  colmax_kernel<<<g, 256, 0, st>>>(m, X, ldx, cmax, status, col_base, rows_per);
+  cast_pass2_kernel<<<g, 256, 0, st>>>(m, X, ldx, Xh, ldh, cmax, inv_s, scaling, rows_per);
   return cudaGetLastError();
 }
 

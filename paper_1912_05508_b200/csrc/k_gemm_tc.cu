@@ -140,18 +140,29 @@ __global__ void __launch_bounds__(192, 1)
       const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n, s = w / (tiles_m * tiles_n);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      const int row = mb * BM + q * 32 + lane;
+      const bool rok = row < M;
+      // NN: the first chunk of the FP32 C tile is loaded BEFORE waiting for the accumulator
+      // (overlaps the mainloop); later chunks are prefetched one chunk ahead.
+      float cv[32];
+      if (MODE == kModeNN) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = nb * BN + j;
+          cv[j] = (rok && col < N) ? C[row + (long long)col * ldc] : 0.f;
+        }
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c, r);
-        tmem_ld_wait();
         const int col0 = nb * BN + c;
-        if (row < M) {
-          if (MODE == kModeTN) {
+        if (MODE == kModeTN) {
+          tmem_ld_wait();
+          if (rok) {
             float* out = C + (splits > 1 ? (long long)s * split_stride : 0LL) + row;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -162,12 +173,17 @@ __global__ void __launch_bounds__(192, 1)
                 out[(long long)col * ldc] = v;
               }
             }
-          } else {
-            float* out = C + row;
-            float cv[32];
+          }
+        } else {
+          float cn[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              cv[j] = (col0 + j < N) ? out[(long long)(col0 + j) * ldc] : 0.f;
+          for (int j = 0; j < 32; ++j) {
+            const int col = col0 + 32 + j;
+            cn[j] = (rok && c + 32 < BN && col < N) ? C[row + (long long)col * ldc] : 0.f;
+          }
+          tmem_ld_wait();
+          if (rok) {
+            float* out = C + row;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int col = col0 + j;
@@ -177,6 +193,8 @@ __global__ void __launch_bounds__(192, 1)
               }
             }
           }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) cv[j] = cn[j];
         }
       }
       tc_fence_before();
@@ -192,18 +210,44 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // Deterministic split-K reduction: C[i + j*ldc] = (sum_s P[s][i + j*ldp]) * col_mult[j].
-__global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, long long pstride,
-                                     int ldp, int M, int N, float* __restrict__ C, long long ldc,
-                                     const float* __restrict__ col_mult) {
+// 8 threads per output element (each sums a contiguous range of splits with all loads in
+// flight), combined in a fixed order through shared memory.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ P, int splits,
+                                                            long long pstride, int ldp, int M,
+                                                            int N, float* __restrict__ C,
+                                                            long long ldc,
+                                                            const float* __restrict__ col_mult) {
+  __shared__ float part[8][33];
   const long long total = (long long)M * N;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e % M), j = (int)(e / M);
-    const float* p = P + i + (long long)j * ldp;
+  const int el = threadIdx.x & 31, sg = threadIdx.x >> 5;  // 32 elements x 8 split groups
+  const int per = (splits + 7) / 8, s0 = sg * per, s1 = min(splits, s0 + per);
+  for (long long eb = (long long)blockIdx.x * 32; eb < total; eb += (long long)gridDim.x * 32) {
+    const long long e = eb + el;
     float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += p[(long long)s * pstride];
-    if (col_mult) acc *= col_mult[j];
-    C[i + (long long)j * ldc] = acc;
+    if (e < total) {
+      const int i = (int)(e % M), j = (int)(e / M);
+      const float* p = P + i + (long long)j * ldp;
+      int s = s0;
+      for (; s + 8 <= s1; s += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (long long)(s + u) * pstride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+      }
+      for (; s < s1; ++s) acc += __ldcg(p + (long long)s * pstride);
+    }
+    __syncthreads();
+    part[sg][el] = acc;
+    __syncthreads();
+    if (sg == 0 && e < total) {
+      float t = 0.f;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) t += part[g][el];
+      const int i = (int)(e % M), j = (int)(e / M);
+      if (col_mult) t *= col_mult[j];
+      C[i + (long long)j * ldc] = t;
+    }
   }
 }
 
@@ -277,7 +321,10 @@ cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, 
   int splits = 1;
   if (tiles < num_sms) {
     splits = num_sms / tiles;
-    if (splits > nkb) splits = nkb;
+    // keep >= 8 K-blocks per split: the partials (and their reduction) cost HBM traffic and a
+    // split that only fills the pipeline is latency, not throughput
+    if (splits > nkb / 8) splits = nkb / 8;
+    if (splits < 1) splits = 1;
     const long long per = (long long)h * w2;
     if (P == nullptr || per * splits > p_cap) splits = P ? (int)(p_cap / per) : 1;
     if (splits < 1) splits = 1;
@@ -295,8 +342,8 @@ cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, 
                                             num_sms, st);
   if (e != cudaSuccess) return e;
   const long long total = (long long)h * w2;
-  int grid = (int)((total + 255) / 256);
-  if (grid > 4 * num_sms) grid = 4 * num_sms;
+  int grid = (int)((total + 31) / 32);
+  if (grid > 8 * num_sms) grid = 8 * num_sms;
   splitk_reduce_kernel<<<grid, 256, 0, st>>>(P, splits, sstride, h, h, w2, C, ldc, col_mult);
   return cudaGetLastError();
 }

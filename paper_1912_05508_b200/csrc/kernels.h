@@ -19,8 +19,10 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
 
 // ---- K1 and friends (k_cast.cu) ----
 // Xh = fl16(X diag(s)); inv_s[j] = 1/s_j; status: atomicMin(1-based first non-finite column).
+// cmax: w uints of scratch for the split-row column max (may be null -> one CTA per column).
 cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
-                       float* inv_s, int scaling, int* status, int col_base, cudaStream_t st);
+                       float* inv_s, int scaling, int* status, int col_base, unsigned int* cmax,
+                       cudaStream_t st);
 // R12 finalize: T (h x w2, ldt) -> R block (ldr) and fl16(R12 diag(s')) (ldh2), inv_s2.
 cudaError_t r12_finalize(int h, int w2, const float* T, long long ldt, float* Rblk, long long ldr,
                          __half* R12h, long long ldh2, float* inv_s2, int scaling, cudaStream_t st);

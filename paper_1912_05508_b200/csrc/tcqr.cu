@@ -121,6 +121,7 @@ struct FactorWs {
   long long pws_cap = 0;
   int* iws = nullptr;       // fused panel arrival counters / flags (zero between launches)
   long long iws_cap = 0;
+  unsigned int* cmax = nullptr;  // column max scratch of the split-row cast (n)
 };
 
 static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, FactorWs& w) {
@@ -143,6 +144,7 @@ static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, Facto
   w.pws = a.take<float>((size_t)w.pws_cap);
   w.iws_cap = 4096 + m / 16;
   w.iws = a.take<int>((size_t)w.iws_cap);
+  w.cmax = a.take<unsigned int>((size_t)n + 64);
 }
 
 struct LlsWs {
@@ -428,7 +430,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
       __half* A2h = ws.Qh + (long long)(c0 + h) * ws.ldh;
       PROF(TCQR_K1_CAST, 0, 6.0 * m * w2,
            CK(cast_scale(m, w2, A2, J.ldq, A2h, ws.ldh, ws.inv_s + c0 + h, c.cfg.col_scaling,
-                         c.d_status, c0 + h, c.stream)));
+                         c.d_status, c0 + h, ws.cmax, c.stream)));
       PROF(TCQR_K3_TN, 2.0 * m * h * w2, 2.0 * m * (h + w2) + 4.0 * h * w2,
            CK(tc_gemm_tn(m, h, w2, A1h, ws.ldh, A2h, ws.ldh, ws.T, h, ws.inv_s + c0 + h, ws.P,
                          ws.p_cap, c.num_sms, c.stream)));
@@ -474,7 +476,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     // Q columns of this panel are final: emit their FP16 shadow for the GEMMs above.
     PROF(TCQR_K1_CAST, 0, 6.0 * m * w,
          CK(cast_scale(m, w, Qc, J.ldq, ws.Qh + (long long)c0 * ws.ldh, ws.ldh, nullptr, 0,
-                       nullptr, 0, c.stream)));
+                       nullptr, 0, nullptr, c.stream)));
   }
   return 0;
 }
@@ -909,8 +911,11 @@ int tcqr_cast_scale(int64_t m, int64_t w, const float* X, int64_t ldx, uint16_t*
   Context& c = g_ctx;
   begin_call();
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));
+  unsigned int* cmax = nullptr;
+  CK(cudaMallocAsync(&cmax, sizeof(unsigned int) * (size_t)w, c.stream));
   CK(cast_scale((int)m, (int)w, X, ldx, reinterpret_cast<__half*>(Xh), ldh, inv_s, scaling,
-                c.d_status, 0, c.stream));
+                c.d_status, 0, cmax, c.stream));
+  cudaFreeAsync(cmax, c.stream);
   return read_status();
 }
 
