@@ -63,6 +63,9 @@ typedef struct tcqr_config {
   int stag_window;   /* stagnation window W (default 10, R-A11)                                */
   double stag_floor; /* stagnation floor relative to pass 1's ||s0|| (default 1e-11, R-A11)    */
   int use_graphs;    /* 1: capture the factorization into a CUDA graph and replay (default 1)  */
+  int reorth;        /* 1: re-orthogonalize (NEXT-1): factor Q1 again,
+                        Q <- Q2, R <- R2 * R1; used by tcqr_factor and tcqr_lls_solve (default 0,
+                        i.e. Alg. 5 with the single RMGSQR R)                                  */
 } tcqr_config_t;
 
 /* Per-solve report (SPEC.md:296-299 CglsReport). */

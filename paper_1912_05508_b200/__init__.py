@@ -32,7 +32,8 @@ class TcqrConfig(ctypes.Structure):
     _fields_ = [("cutoff", ctypes.c_int), ("panel_rows", ctypes.c_int),
                 ("col_scaling", ctypes.c_int), ("restart", ctypes.c_int),
                 ("tol2", ctypes.c_double), ("stag_window", ctypes.c_int),
-                ("stag_floor", ctypes.c_double), ("use_graphs", ctypes.c_int)]
+                ("stag_floor", ctypes.c_double), ("use_graphs", ctypes.c_int),
+                ("reorth", ctypes.c_int)]
 
 
 class TcqrLlsInfo(ctypes.Structure):

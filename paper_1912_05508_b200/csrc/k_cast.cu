@@ -245,4 +245,63 @@ cudaError_t zero_lower(int n, float* R, long long ldr, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// C = A * B for upper-triangular n x n FP32 A, B (column-major, leading dims lda/ldb/ldc): the
+// re-orthogonalized R = R2 * R1 (NEXT-1).  64 x 64 tiles, 4 x 4 per thread,
+// only upper tiles; the k range of tile (I, J) is [I*64, (J+1)*64) (zeros elsewhere).
+__global__ void __launch_bounds__(256) trmm_upper_kernel(int n, const float* __restrict__ A,
+                                                         long long lda, const float* __restrict__ B,
+                                                         long long ldb, float* __restrict__ C,
+                                                         long long ldc) {
+  __shared__ float As[16][65];
+  __shared__ float Bs[16][65];
+  const int tI = blockIdx.x, tJ = blockIdx.y;
+  const int tid = threadIdx.x, ti = tid & 15, tj = tid >> 4;
+  const int i0 = tI * 64, j0 = tJ * 64;
+  if (tI > tJ) {
+    for (int e = tid; e < 64 * 64; e += 256) {
+      const int r = i0 + (e & 63), c = j0 + (e >> 6);
+      if (r < n && c < n) C[r + (long long)c * ldc] = 0.f;
+    }
+    return;
+  }
+  float acc[4][4] = {};
+  const int k_end = min(n, j0 + 64);
+  for (int k0 = i0; k0 < k_end; k0 += 16) {
+    __syncthreads();
+    for (int e = tid; e < 16 * 64; e += 256) {
+      const int kk = e >> 6, mm = e & 63;
+      const int k = k0 + kk;
+      As[kk][mm] = (i0 + mm < n && k < k_end) ? A[(i0 + mm) + (long long)k * lda] : 0.f;
+      Bs[kk][mm] = (j0 + mm < n && k < k_end) ? B[k + (long long)(j0 + mm) * ldb] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a[x] = As[kk][ti * 4 + x];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) b[y] = Bs[kk][tj * 4 + y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(a[x], b[y], acc[x][y]);
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int r = i0 + ti * 4 + x, c = j0 + tj * 4 + y;
+      if (r < n && c < n) C[r + (long long)c * ldc] = acc[x][y];
+    }
+}
+
+cudaError_t trmm_upper(int n, const float* A, long long lda, const float* B, long long ldb,
+                       float* C, long long ldc, cudaStream_t st) {
+  const int t = (n + 63) / 64;
+  trmm_upper_kernel<<<dim3(t, t), 256, 0, st>>>(n, A, lda, B, ldb, C, ldc);
+  return cudaGetLastError();
+}
+
 }  // namespace tcqr

@@ -122,9 +122,12 @@ struct FactorWs {
   int* iws = nullptr;       // fused panel arrival counters / flags (zero between launches)
   long long iws_cap = 0;
   unsigned int* cmax = nullptr;  // column max scratch of the split-row cast (n)
+  float* R2 = nullptr;           // re-orthogonalization: R of the second pass (n x n)
+  float* Rt = nullptr;           // re-orthogonalization: R2 * R1 staging (n x n)
 };
 
-static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, FactorWs& w) {
+static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, FactorWs& w,
+                           bool reorth = false) {
   w.ldh = round_up(std::max<long long>(m, 8), 8);
   w.Qh = a.take<__half>((size_t)w.ldh * n);
   w.inv_s = a.take<float>(n + 8);
@@ -145,6 +148,10 @@ static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, Facto
   w.iws_cap = 4096 + m / 16;
   w.iws = a.take<int>((size_t)w.iws_cap);
   w.cmax = a.take<unsigned int>((size_t)n + 64);
+  if (reorth) {
+    w.R2 = a.take<float>((size_t)n * n);
+    w.Rt = a.take<float>((size_t)n * n);
+  }
 }
 
 struct LlsWs {
@@ -194,14 +201,14 @@ static void plan_lls_ws(Arena& a, long long m, long long n, int nranks, int maxi
   w.hist_cap = std::max(maxit, 1) * 2 + 8;
   w.hist = a.take<double>((size_t)w.hist_cap);
   w.st = a.take<CgState>(1);
-  plan_factor_ws(a, m, n, nranks, w.f);
+  plan_factor_ws(a, m, n, nranks, w.f, g_ctx.cfg.reorth != 0);
 }
 
 static size_t ws_bytes(long long m, long long n, int op, int nranks, int maxit) {
   Arena a;
   if (op == 0) {
     FactorWs f;
-    plan_factor_ws(a, m, n, nranks, f);
+    plan_factor_ws(a, m, n, nranks, f, g_ctx.cfg.reorth != 0);
   } else {
     LlsWs l;
     plan_lls_ws(a, m, n, nranks, maxit, l);
@@ -493,6 +500,17 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
   const bool need_h = n > c.cfg.cutoff;
   CKR(rgs(J, 0, n, need_h));
   CK(zero_lower(n, R, n, c.stream));
+  if (c.cfg.reorth && ws.R2) {
+    // NEXT-1: a second QR of Q itself; Q <- Q2, R <- R2 R1.
+    CK(cudaMemsetAsync(ws.R2, 0, sizeof(float) * (size_t)n * n, c.stream));
+    FactorJob J2{m, n, Q, (long long)m, ws.R2, (long long)n, &ws};
+    CKR(rgs(J2, 0, n, need_h));
+    CK(zero_lower(n, ws.R2, n, c.stream));
+    PROF(TCQR_TRINV, (double)n * n * n / 3.0, 12.0 * n * n,
+         CK(trmm_upper(n, ws.R2, n, R, n, ws.Rt, n, c.stream)));
+    CK(cudaMemcpyAsync(R, ws.Rt, sizeof(float) * (size_t)n * n, cudaMemcpyDeviceToDevice,
+                       c.stream));
+  }
   CKR(allreduce_max_i32(c.d_status));
   return 0;
 }
@@ -514,7 +532,7 @@ static std::string graph_key(const char* tag, std::initializer_list<long long> v
     k += buf;
   }
   const tcqr_config_t& f = g_ctx.cfg;
-  snprintf(buf, sizeof buf, "|%d,%d,%d", f.cutoff, f.panel_rows, f.col_scaling);
+  snprintf(buf, sizeof buf, "|%d,%d,%d,%d", f.cutoff, f.panel_rows, f.col_scaling, f.reorth);
   k += buf;
   return k;
 }
@@ -590,6 +608,7 @@ void tcqr_default_config(tcqr_config_t* c) {
   c->stag_window = 10;
   c->stag_floor = 1e-11;
   c->use_graphs = 1;
+  c->reorth = 0;
 }
 
 int tcqr_set_config(const tcqr_config_t* cfg) {
@@ -598,6 +617,7 @@ int tcqr_set_config(const tcqr_config_t* cfg) {
   if (cfg->cutoff < 32 || cfg->cutoff > 128 || cfg->cutoff % 32) return -1;
   if (cfg->panel_rows < 64 || cfg->panel_rows > 1024 || cfg->panel_rows % 32) return -1;
   if (cfg->tol2 <= 0 || cfg->stag_window < 1 || cfg->stag_floor < 0) return -1;
+  if (cfg->reorth != 0 && cfg->reorth != 1) return -1;
   g_ctx.cfg = *cfg;
   return 0;
 }
@@ -706,7 +726,7 @@ int tcqr_factor(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, flo
   if (!base) return TCQR_ERR_OOM;
   Arena a{base, 0};
   FactorWs ws;
-  plan_factor_ws(a, m, n, c.nranks, ws);
+  plan_factor_ws(a, m, n, c.nranks, ws, c.cfg.reorth != 0);
   CKR(run_factor((int)m, (int)n, A, lda, Q, R, ws, base));
   return read_status();
 }

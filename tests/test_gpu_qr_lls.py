@@ -180,3 +180,36 @@ def test_lls_maxit_reports_not_converged(tq):
     x, info = tq.lls_solve(tq.to_device_colmajor(a), torch.from_numpy(b).cuda(), maxit=5)
     assert info["converged"] == 0 and info["stop_reason"] == 2
     assert np.all(np.isfinite(x.cpu().numpy()))
+
+
+# ---- NEXT-1: re-orthogonalization -------------------------------------------
+@pytest.mark.parametrize("kind,cond", [("geometric", 1e3), ("geometric", 1e4), ("gaussian", 1)])
+def test_reorth_factor(tq, kind, cond):
+    a = W.make_matrix(kind, 4096, 512, seed=17, cond=cond)
+    q1, r1 = _factor(tq, a)
+    q2, r2 = _factor(tq, a, reorth=1)
+    tq.set_config()
+    _, r_o = rgs(a.astype(np.float64))
+    # Q2 is orthogonal to working accuracy whatever kappa (the paper's remedy), A = Q2 (R2 R1)
+    assert orthogonality_f(q2) < 5e-4
+    assert orthogonality_f(q2) <= orthogonality_f(q1) + 1e-6
+    assert backward_error_f(a, q2, r2) < 5e-3
+    assert np.array_equal(r2, np.triu(r2)) and np.all(np.diag(r2) > 0)
+    if cond <= 1e3:
+        assert r_rel_error(r2, r_o) < 1e-2
+
+
+def test_reorth_lls_fewer_iterations(tq):
+    a = W.spectrum_matrix(4096, 1024, "geometric", 1e4, seed=23)
+    b, x_true = W.consistent_rhs(a, seed=24)
+    x_o, _ = oracle_lls(a.astype(np.float64), b)
+    A = tq.to_device_colmajor(a)
+    B = torch.from_numpy(b).cuda()
+    tq.set_config()
+    x1, i1 = tq.lls_solve(A, B, tol=1e-10, maxit=4000)
+    tq.set_config(reorth=1)
+    x2, i2 = tq.lls_solve(A, B, tol=1e-10, maxit=4000)
+    tq.set_config()
+    assert i2["converged"] == 1 and x_rel_error(x2.cpu().numpy(), x_o) <= 1e-10
+    assert x_rel_error(x1.cpu().numpy(), x_o) <= 1e-10
+    assert i2["iterations"] * 4 < i1["iterations"], (i1["iterations"], i2["iterations"])

@@ -13,6 +13,7 @@ A = W.spectrum_cuda(M, n, "geometric", kappa, 6)
 g = torch.Generator(device="cuda"); g.manual_seed(106)
 xt = torch.randn(n, generator=g, device="cuda", dtype=torch.float64)
 b = A.to(torch.float64) @ xt
+tq.set_config(reorth=int(os.environ.get("REORTH", 0)))
 for it in range(2):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
