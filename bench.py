@@ -335,19 +335,30 @@ def main():
         bl = b_full[l0:l1].contiguous()
         del Al_full, b_full
         torch.cuda.empty_cache()
-        barrier()
-        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        h0.record(stream)
-        x, info = tq.lls_solve(Al, bl, tol=1e-10, maxit=4000)
-        h1.record(stream)
-        torch.cuda.synchronize()
-        lms = h0.elapsed_time(h1)
-        xe = float(torch.linalg.norm(x - x_true) / torch.linalg.norm(x_true))
-        lls = {"workload": "LLS 32768x8192 geometric kappa=1e4, b = A x_true (BASELINE configs[3])",
-               "time_to_solution_ms": lms, "qr_ms": info["qr_ms"], "cgls_ms": info["cgls_ms"],
-               "iterations": info["iterations"], "iterations_pass1": info["iterations_pass1"],
-               "converged": bool(info["converged"]), "x_rel_err_vs_x_true": xe,
-               "fp64_accuracy_reached": bool(xe <= 1e-10)}
+        lls = {"workload": "LLS 32768x8192 geometric kappa=1e4, b = A x_true (BASELINE configs[3]), "
+                           "FP64 target (tol 1e-10, one restart), warm (graphs captured)"}
+        for label, reorth in (("paper_R", 0), ("reorth_R", 1)):
+            tq.set_config(cutoff=args.cutoff, reorth=reorth)
+            tq.lls_solve(Al, bl, tol=1e-10, maxit=4000)      # warm-up: builds the QR graph
+            barrier()
+            torch.cuda.synchronize()
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            x, info = tq.lls_solve(Al, bl, tol=1e-10, maxit=4000)
+            h1.record(stream)
+            torch.cuda.synchronize()
+            lt = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+            xe = float(torch.linalg.norm(x - x_true) / torch.linalg.norm(x_true))
+            lls[label] = {"time_to_solution_ms": float(lt.item()), "qr_ms": info["qr_ms"],
+                          "cgls_ms": info["cgls_ms"], "iterations": info["iterations"],
+                          "iterations_pass1": info["iterations_pass1"],
+                          "converged": bool(info["converged"]), "x_rel_err_vs_x_true": xe,
+                          "fp64_accuracy_reached": bool(xe <= 1e-10)}
+        lls["reorth_R"]["note"] = ("NEXT-1 (PAPER.md:622-627): R = R2 R1 from a second RGS of Q; "
+                                   "paper_R is Alg. 5 with the single RMGSQR R")
+        tq.set_config(cutoff=args.cutoff)
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ----
     cpu = None
