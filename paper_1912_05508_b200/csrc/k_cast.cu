@@ -297,10 +297,84 @@ __global__ void __launch_bounds__(256) trmm_upper_kernel(int n, const float* __r
     }
 }
 
+// 128 x 128 tiles, 8 x 8 register micro-tiles, register-prefetched double-buffered K-chunks.
+__global__ void __launch_bounds__(256, 1) trmm_upper_big(int n, const float* __restrict__ A,
+                                                         long long lda, const float* __restrict__ B,
+                                                         long long ldb, float* __restrict__ C,
+                                                         long long ldc) {
+  constexpr int TB = 128, KB = 16, NLD = KB * TB / 256;
+  __shared__ __align__(16) float As[2][KB][TB];
+  __shared__ __align__(16) float Bs[2][KB][TB];
+  const int tI = blockIdx.x, tJ = blockIdx.y;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int i0 = tI * TB, j0 = tJ * TB;
+  if (tI > tJ) {
+    for (int e = tid; e < TB * TB; e += 256) {
+      const int r = i0 + (e & (TB - 1)), c = j0 + e / TB;
+      if (r < n && c < n) C[r + (long long)c * ldc] = 0.f;
+    }
+    return;
+  }
+  const int kbeg = i0, kend = min(n, j0 + TB);
+  auto load = [&](int k0, float (&ra)[NLD], float (&rb)[NLD]) {
+#pragma unroll
+    for (int u = 0; u < NLD; ++u) {
+      const int e = tid + u * 256, kk = e >> 7, mm = e & 127;
+      const int k = k0 + kk;
+      ra[u] = (i0 + mm < n && k < kend) ? __ldg(A + (i0 + mm) + (long long)k * lda) : 0.f;
+      rb[u] = (j0 + mm < n && k < kend) ? __ldg(B + k + (long long)(j0 + mm) * ldb) : 0.f;
+    }
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int x = 0; x < 8; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) acc[x][y] = 0.f;
+  float ra[NLD], rb[NLD];
+  int buf = 0;
+  load(kbeg, ra, rb);
+  for (int k0 = kbeg; k0 < kend; k0 += KB) {
+#pragma unroll
+    for (int u = 0; u < NLD; ++u) {
+      const int e = tid + u * 256, kk = e >> 7, mm = e & 127;
+      As[buf][kk][mm] = ra[u];
+      Bs[buf][kk][mm] = rb[u];
+    }
+    __syncthreads();
+    if (k0 + KB < kend) load(k0 + KB, ra, rb);
+#pragma unroll
+    for (int kk = 0; kk < KB; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][tx * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][tx * 8 + 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][ty * 8]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][ty * 8 + 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) acc[x][y] = fmaf(a[x], bb[y], acc[x][y]);
+    }
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int x = 0; x < 8; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const int r = i0 + tx * 8 + x, c = j0 + ty * 8 + y;
+      if (r < n && c < n) C[r + (long long)c * ldc] = acc[x][y];
+    }
+}
+
 cudaError_t trmm_upper(int n, const float* A, long long lda, const float* B, long long ldb,
                        float* C, long long ldc, cudaStream_t st) {
-  const int t = (n + 63) / 64;
-  trmm_upper_kernel<<<dim3(t, t), 256, 0, st>>>(n, A, lda, B, ldb, C, ldc);
+  if (n >= 512) {
+    const int t = (n + 127) / 128;
+    trmm_upper_big<<<dim3(t, t), 256, 0, st>>>(n, A, lda, B, ldb, C, ldc);
+  } else {
+    const int t = (n + 63) / 64;
+    trmm_upper_kernel<<<dim3(t, t), 256, 0, st>>>(n, A, lda, B, ldb, C, ldc);
+  }
   return cudaGetLastError();
 }
 

@@ -123,6 +123,120 @@ __global__ void __launch_bounds__(256) trinv_pair_gemm_kernel(int n, int b, int 
     }
 }
 
+// Large-tile FP64 pair GEMM (b >= 128): 128 x 128 output tile per CTA, 256 threads with 8 x 8
+// register micro-tiles, K-chunks of 16 staged through shared memory with a register prefetch of
+// the next chunk; the triangular factor's zero blocks are skipped (mode 0: k < (J+1)*128,
+// mode 1: k >= I*128).
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) trinv_pair_gemm_big(int n, int b,
+                                                              const float* __restrict__ R,
+                                                              long long ldr,
+                                                              double* __restrict__ M,
+                                                              long long ldm,
+                                                              double* __restrict__ W) {
+  constexpr int TB = 128, KB = 8, NLD = KB * TB / 256;
+  __shared__ __align__(16) double As[2][KB][TB];
+  __shared__ __align__(16) double Bs[2][KB][TB];
+  const int p = blockIdx.z;
+  const int i0 = p * 2 * b;
+  const int b1 = b;
+  const int b2 = min(b, n - (i0 + b));
+  if (b2 <= 0) return;
+  const int tm = blockIdx.x * TB, tn = blockIdx.y * TB;
+  if (tm >= b1 || tn >= b2) return;
+  double* Wp = W + (long long)p * b * b;  // ld = b
+  const int K = (MODE == 0) ? b2 : b1;
+  const int kbeg = (MODE == 0) ? 0 : tm;
+  const int kend = (MODE == 0) ? min(K, tn + TB) : K;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // rows tx*8.., cols ty*8..
+  // loader mapping: KB x 128 tile, NLD doubles per thread: kk = e >> 7, mm = e & 127
+  auto loadA = [&](int k0, double (&ra)[NLD]) {
+#pragma unroll
+    for (int u = 0; u < NLD; ++u) {
+      const int e = tid + u * 256, kk = e >> 7, mm = e & 127;
+      const int r = tm + mm, k = k0 + kk;
+      double v = 0.0;
+      if (r < b1 && k < kend) {
+        if (MODE == 0)
+          v = (double)__ldg(R + (i0 + r) + (long long)(i0 + b1 + k) * ldr);
+        else
+          v = M[(i0 + r) + (long long)(i0 + k) * ldm];
+      }
+      ra[u] = v;
+    }
+  };
+  auto loadB = [&](int k0, double (&rb)[NLD]) {
+#pragma unroll
+    for (int u = 0; u < NLD; ++u) {
+      const int e = tid + u * 256, kk = e >> 7, mm = e & 127;
+      const int c = tn + mm, k = k0 + kk;
+      double v = 0.0;
+      if (c < b2 && k < kend) {
+        if (MODE == 0)
+          v = M[(i0 + b1 + k) + (long long)(i0 + b1 + c) * ldm];
+        else
+          v = Wp[k + (long long)c * b];
+      }
+      rb[u] = v;
+    }
+  };
+  double acc[8][8];
+#pragma unroll
+  for (int x = 0; x < 8; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) acc[x][y] = 0.0;
+  double ra[NLD], rb[NLD];
+  int buf = 0;
+  loadA(kbeg, ra);
+  loadB(kbeg, rb);
+  for (int k0 = kbeg; k0 < kend; k0 += KB) {
+#pragma unroll
+    for (int u = 0; u < NLD; ++u) {
+      const int e = tid + u * 256, kk = e >> 7, mm = e & 127;
+      As[buf][kk][mm] = ra[u];
+      Bs[buf][kk][mm] = rb[u];
+    }
+    __syncthreads();
+    if (k0 + KB < kend) {
+      loadA(k0 + KB, ra);
+      loadB(k0 + KB, rb);
+    }
+#pragma unroll
+    for (int kk = 0; kk < KB; ++kk) {
+      double a[8], bb[8];
+#pragma unroll
+      for (int x = 0; x < 8; x += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(&As[buf][kk][tx * 8 + x]);
+        a[x] = v.x;
+        a[x + 1] = v.y;
+      }
+#pragma unroll
+      for (int y = 0; y < 8; y += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][kk][ty * 8 + y]);
+        bb[y] = v.x;
+        bb[y + 1] = v.y;
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) acc[x][y] = fma(a[x], bb[y], acc[x][y]);
+    }
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int x = 0; x < 8; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const int r = tm + tx * 8 + x, c = tn + ty * 8 + y;
+      if (r < b1 && c < b2) {
+        if (MODE == 0)
+          Wp[r + (long long)c * b] = acc[x][y];
+        else
+          M[(i0 + r) + (long long)(i0 + b1 + c) * ldm] = -acc[x][y];
+      }
+    }
+}
+
 cudaError_t trinv_f64(int n, const float* R, long long ldr, double* M, long long ldm, double* W,
                       int num_sms, cudaStream_t st) {
   (void)num_sms;
@@ -133,9 +247,15 @@ cudaError_t trinv_f64(int n, const float* R, long long ldr, double* M, long long
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   for (int b = kInvBlk; b < n; b *= 2) {
     const int pairs = (n + 2 * b - 1) / (2 * b);
-    dim3 grid((b + 63) / 64, (b + 63) / 64, pairs);
-    trinv_pair_gemm_kernel<<<grid, 256, 0, st>>>(n, b, 0, R, ldr, M, ldm, W);
-    trinv_pair_gemm_kernel<<<grid, 256, 0, st>>>(n, b, 1, R, ldr, M, ldm, W);
+    if (b >= 128) {
+      dim3 grid((b + 127) / 128, (b + 127) / 128, pairs);
+      trinv_pair_gemm_big<0><<<grid, 256, 0, st>>>(n, b, R, ldr, M, ldm, W);
+      trinv_pair_gemm_big<1><<<grid, 256, 0, st>>>(n, b, R, ldr, M, ldm, W);
+    } else {
+      dim3 grid((b + 63) / 64, (b + 63) / 64, pairs);
+      trinv_pair_gemm_kernel<<<grid, 256, 0, st>>>(n, b, 0, R, ldr, M, ldm, W);
+      trinv_pair_gemm_kernel<<<grid, 256, 0, st>>>(n, b, 1, R, ldr, M, ldm, W);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -146,3 +146,27 @@ def test_trinv_and_gemv(tq):
     u = rng.standard_normal(1000)
     z = tq.gemv(A, torch.from_numpy(u).cuda(), trans=True).cpu().numpy()
     assert np.allclose(z, a.astype(np.float64).T @ u, rtol=1e-12, atol=1e-10)
+
+
+@pytest.mark.parametrize("n", [300, 1000, 2100])
+def test_trinv_large_tiles(tq, n):
+    # the 128 x 128 FP64 pair-GEMM path (b >= 128) against the FP64 residual R M - I
+    rng = np.random.default_rng(n)
+    r = np.linalg.qr(rng.standard_normal((2 * n, n)))[1]
+    r = (r * np.sign(np.diag(r))[:, None]).astype(np.float32)
+    M = tq.trinv(tq.to_device_colmajor(r)).cpu().numpy()
+    assert np.array_equal(M, np.triu(M))
+    assert np.linalg.norm(r.astype(np.float64) @ M - np.eye(n)) / np.sqrt(n) < 1e-12
+
+
+def test_reorth_product_is_r2_r1(tq):
+    # tcqr_factor with reorth: A = Q2 (R2 R1); R2 R1 upper triangular (trmm kernel), n >= 512 path
+    a = W.gaussian(2048, 640, seed=3)
+    tq.set_config(reorth=1)
+    A = tq.to_device_colmajor(a)
+    Q, R = tq.factor(A)
+    tq.set_config()
+    q, r = Q.cpu().numpy().astype(np.float64), R.cpu().numpy().astype(np.float64)
+    assert np.array_equal(r, np.triu(r))
+    assert np.linalg.norm(a - q @ r) / np.linalg.norm(a) < 5e-3
+    assert orthogonality_f(q) < 1e-5
