@@ -69,6 +69,8 @@ struct Context {
   size_t user_ws_bytes = 0;
   void* own_ws = nullptr;
   size_t own_ws_bytes = 0;
+  void* hstage = nullptr;   // device staging of the host-pointer entry points (grow-only, so
+  size_t hstage_bytes = 0;  // pointers stay stable and the factorization graph is reused)
   int* d_status = nullptr;  // [0] factor status, [1] scratch
   int* h_status = nullptr;  // pinned
   std::map<std::string, GraphEntry> graphs;
@@ -214,6 +216,21 @@ static size_t ws_bytes(long long m, long long n, int op, int nranks, int maxit) 
     plan_lls_ws(a, m, n, nranks, maxit, l);
   }
   return a.off + 256;
+}
+
+static char* get_hstage(size_t bytes) {
+  Context& c = g_ctx;
+  if (c.hstage_bytes < bytes) {
+    if (c.hstage) {
+      cudaStreamSynchronize(c.stream);
+      cudaFree(c.hstage);
+    }
+    c.hstage = nullptr;
+    c.hstage_bytes = 0;
+    if (cudaMalloc(&c.hstage, bytes) != cudaSuccess) return nullptr;
+    c.hstage_bytes = bytes;
+  }
+  return static_cast<char*>(c.hstage);
 }
 
 static char* get_ws(size_t bytes) {
@@ -643,6 +660,9 @@ int tcqr_finalize(void) {
   if (c.own_ws) cudaFree(c.own_ws);
   c.own_ws = nullptr;
   c.own_ws_bytes = 0;
+  if (c.hstage) cudaFree(c.hstage);
+  c.hstage = nullptr;
+  c.hstage_bytes = 0;
   if (c.d_status) cudaFree(c.d_status);
   if (c.h_status) cudaFreeHost(c.h_status);
   c.d_status = nullptr;
@@ -873,9 +893,11 @@ int tcqr_factor_host(int64_t m, int64_t n, const float* A, int64_t lda, float* Q
   Context& c = g_ctx;
   begin_call();
   cudaSetDevice(c.device);
-  float *dQ = nullptr, *dR = nullptr;
-  if (cudaMallocAsync(&dQ, sizeof(float) * m * n, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
-  if (cudaMallocAsync(&dR, sizeof(float) * n * n, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
+  const size_t qbytes = (size_t)round_up(sizeof(float) * m * n, 256);
+  char* stage = get_hstage(qbytes + sizeof(float) * n * n);
+  if (!stage) return TCQR_ERR_OOM;
+  float* dQ = reinterpret_cast<float*>(stage);
+  float* dR = reinterpret_cast<float*>(stage + qbytes);
   CK(cudaMemcpy2DAsync(dQ, sizeof(float) * m, A, sizeof(float) * lda, sizeof(float) * m, n,
                        cudaMemcpyHostToDevice, c.stream));
   int rc = tcqr_factor(m, n, dQ, m, dQ, dR);
@@ -883,8 +905,6 @@ int tcqr_factor_host(int64_t m, int64_t n, const float* A, int64_t lda, float* Q
     CK(cudaMemcpyAsync(Q, dQ, sizeof(float) * m * n, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaMemcpyAsync(R, dR, sizeof(float) * n * n, cudaMemcpyDeviceToHost, c.stream));
   }
-  cudaFreeAsync(dQ, c.stream);
-  cudaFreeAsync(dR, c.stream);
   CK(cudaStreamSynchronize(c.stream));
   return rc;
 }
@@ -901,19 +921,18 @@ int tcqr_lls_solve_host(int64_t m, int64_t n, const float* A, int64_t lda, const
   Context& c = g_ctx;
   begin_call();
   cudaSetDevice(c.device);
-  float* dA = nullptr;
-  double *db = nullptr, *dx = nullptr;
-  if (cudaMallocAsync(&dA, sizeof(float) * m * n, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
-  if (cudaMallocAsync(&db, sizeof(double) * m, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
-  if (cudaMallocAsync(&dx, sizeof(double) * n, c.stream) != cudaSuccess) return TCQR_ERR_OOM;
+  const size_t abytes = (size_t)round_up(sizeof(float) * m * n, 256);
+  const size_t bbytes = (size_t)round_up(sizeof(double) * m, 256);
+  char* stage = get_hstage(abytes + bbytes + sizeof(double) * n);
+  if (!stage) return TCQR_ERR_OOM;
+  float* dA = reinterpret_cast<float*>(stage);
+  double* db = reinterpret_cast<double*>(stage + abytes);
+  double* dx = reinterpret_cast<double*>(stage + abytes + bbytes);
   CK(cudaMemcpy2DAsync(dA, sizeof(float) * m, A, sizeof(float) * lda, sizeof(float) * m, n,
                        cudaMemcpyHostToDevice, c.stream));
   CK(cudaMemcpyAsync(db, b, sizeof(double) * m, cudaMemcpyHostToDevice, c.stream));
   int rc = tcqr_lls_solve(m, n, dA, m, db, dx, tol, maxit, info);
   if (rc == 0) CK(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
-  cudaFreeAsync(dA, c.stream);
-  cudaFreeAsync(db, c.stream);
-  cudaFreeAsync(dx, c.stream);
   CK(cudaStreamSynchronize(c.stream));
   return rc;
 }
