@@ -230,6 +230,27 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
 }
 
 // Alg. 4 on the rows held in x (thread t owns rows t + r*NT): Q columns -> qs, R rows -> Rdst.
+// One step k with the reduction width chosen from the active column count.
+template <int NT, int RPT>
+__device__ __forceinline__ void mgs_step_any(float (&x)[RPT][32], int nrows, int w, int k,
+                                             float* const (&qp)[RPT], int qstride, float* Rdst,
+                                             long long rs, long long cs, bool check, int* status,
+                                             int col0, float* red, int& buf) {
+  const int act = w - k;
+  if (act > 16)
+    mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+  else if (act > 8)
+    mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+  else if (act > 4)
+    mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+  else if (act > 2)
+    mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+  else if (act > 1)
+    mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+  else
+    mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+}
+
 template <int NT, int RPT>
 __device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int w,
                                              const QSink& qs, float* Rdst, long long rs,
@@ -532,6 +553,173 @@ cudaError_t panel_mgs_level(int rows, int w, float* X, long long ldx, int br, in
   panel_mgs_kernel<<<nb, kLvlNT, smem, st>>>(rows, w, X, ldx, br, nb, S, lds, Rout, ldr, top,
                                              status, col0);
   return cudaGetLastError();
+}
+
+// ==========================================================================================
+// Pipelined single-level panel (nb <= F row blocks, one root): the stacked node is a stack of
+// upper triangles, so the root's MGS step k only touches rows (b, i <= k), which child b produced
+// at ITS step k (R_b(k, k:)).  The root therefore runs one step behind the children instead of
+// after them.  Likewise the final Q column j of block b is Q_b * S_b(:, j), and S_b(:, j) (rows of
+// the root's Q column j) is final after root step j: the children apply it column by column
+// while the root is still running.  Every R / S value doubles as its own ready flag: the
+// scratch is NaN-initialized, producers store plain values, consumers poll until non-NaN and
+// reset the slot to NaN after use (no fences on the critical path).
+// ==========================================================================================
+struct PipeArgs {
+  float* X;
+  long long ldx;
+  __half* Xh;  // may be null
+  long long ldh;
+  int m, w, nb;
+  float* Rb;   // nb row-major w x w child R's (NaN between uses)
+  float* S;    // nb column-major w x w slices of the root Q (NaN between uses)
+  float* Rout;
+  long long ldr;
+  int root_is_global;
+  int* status;
+  int col0;
+};
+
+__device__ __forceinline__ float ld_relaxed_f(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int NT, int RPT>
+__global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
+  extern __shared__ float fsm[];
+  float* qA = fsm;                                      // child: Q_b [CAP][33]
+  float* sj = fsm + ((NT * RPT * 33 + 3) & ~3);         // child: [2][32] current S column
+  float* red = sj + 64;                                 // [2][NT/32][32]
+  const int w = a.w, b = blockIdx.x;
+  const float qnan = __int_as_float(0x7fffffff);
+  if (b < a.nb) {
+    // ----------------------------- child: row block b -----------------------------------------
+    const int row0 = blk_row(b, a.m, a.nb);
+    const int nrows = blk_row(b + 1, a.m, a.nb) - row0;
+    float x[RPT][32];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = threadIdx.x + r * NT;
+      const bool ok = i < nrows;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        x[r][j] = (ok && j < w) ? a.X[(long long)(row0 + i) + (long long)j * a.ldx] : 0.f;
+    }
+    mgs_rotating<NT, RPT>(x, nrows, w, QSink{qA, nullptr, w}, a.Rb + (long long)b * w * w, w, 1,
+                          false, a.status, a.col0, red);
+    __syncthreads();
+    const float* Sb = a.S + (long long)b * w * w;
+    for (int j = 0; j < w; ++j) {
+      float* sbuf = sj + (j & 1) * 32;
+      if (threadIdx.x < 32) {
+        const int i = threadIdx.x;
+        float v = 0.f;
+        if (i <= j) {
+          float* src = const_cast<float*>(Sb) + i + j * w;
+          v = ld_relaxed_f(src);
+          while (isnan(v)) {
+            __nanosleep(20);
+            v = ld_relaxed_f(src);
+          }
+          *src = qnan;  // consumed: reset for the next panel
+        }
+        sbuf[i] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = threadIdx.x + r * NT;
+        if (i < nrows) {
+          float y = 0.f;
+          for (int l = 0; l <= j; ++l) y = fmaf(qA[i * 33 + l], sbuf[l], y);
+          const long long gi = (long long)(row0 + i) + (long long)j * a.ldx;
+          a.X[gi] = y;
+          if (a.Xh) a.Xh[(long long)(row0 + i) + (long long)j * a.ldh] = __float2half_rn(y);
+        }
+      }
+    }
+  } else {
+    // ----------------------------- root: the stack of child R's -------------------------------
+    const int srows = a.nb * w;
+    float x[RPT][32];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[r][j] = 0.f;
+    float* qp[RPT];
+    int cb[RPT], ci[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int sr = threadIdx.x + r * NT;
+      const int s0 = sr < srows ? sr : 0;
+      cb[r] = sr < srows ? s0 / w : -1;
+      ci[r] = s0 - (s0 / w) * w;
+      qp[r] = a.S + (long long)(s0 / w) * w * w + ci[r];
+    }
+    int buf = 0;
+    for (int k = 0; k < w; ++k) {
+      // lazily load stack rows (b, k): R_b(k, k:w) is ready once child b finished its step k
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        if (cb[r] >= 0 && ci[r] == k) {
+          float* src = a.Rb + (long long)cb[r] * w * w + (long long)k * w;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            if (k + c < w) {
+              float v = ld_relaxed_f(src + k + c);
+              while (isnan(v)) {
+                __nanosleep(20);
+                v = ld_relaxed_f(src + k + c);
+              }
+              x[r][c] = v;
+              src[k + c] = qnan;
+            }
+          }
+        }
+      }
+      mgs_step_any<NT, RPT>(x, srows, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
+                            a.status, a.col0, red, buf);
+    }
+  }
+}
+
+template <int NT, int RPT>
+static int pipe_capacity(int num_sms) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    const int smem = (int)sizeof(float) * (((NT * RPT * 33 + 3) & ~3) + 64 + 2 * (NT / 32) * 32);
+    cudaFuncSetAttribute(panel_pipe_kernel<NT, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_pipe_kernel<NT, RPT>, NT,
+                                                      smem) != cudaSuccess)
+      per_sm = 0;
+  }
+  return per_sm * num_sms;
+}
+
+// m rows in nb = ceil(m / 1024) <= 1024 / w blocks + one root CTA; Rb, S: NaN-initialized scratch
+// of 32 * 32 * 32 floats each.  cudaErrorNotSupported when the shape does not qualify.
+cudaError_t panel_pipe(int m, int w, float* X, long long ldx, __half* Xh, long long ldh, int br,
+                       float* Rout, long long ldr, int root_is_global, int* status, int col0,
+                       float* Rb, float* S, int num_sms, cudaStream_t st) {
+  if (w < 1 || w > 32 || br != 1024) return cudaErrorNotSupported;
+  const int nb = (m + br - 1) / br;
+  if (nb < 2 || nb * w > 1024 || nb > 32) return cudaErrorNotSupported;
+  if (nb + 1 > pipe_capacity<256, 4>(num_sms)) return cudaErrorNotSupported;
+  PipeArgs a{X, ldx, Xh, ldh, m, w, nb, Rb, S, Rout, ldr, root_is_global, status, col0};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nb + 1);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = (int)sizeof(float) * (((256 * 4 * 33 + 3) & ~3) + 64 + 2 * 8 * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, panel_pipe_kernel<256, 4>, a);
 }
 
 unsigned long long* g_panel_dbg = nullptr;

@@ -54,6 +54,11 @@ cudaError_t panel_fused(int m, int w, float* X, long long ldx, __half* Xh, long 
                         float* ws, long long ws_cap, int* iws, long long iws_cap, int num_sms,
                         cudaStream_t st);
 int fused_panel_capacity(int num_sms);
+// Pipelined single-level panel (root runs one MGS step behind the row blocks); Rb, S: NaN-filled
+// scratch (32*32*32 floats each), left NaN-filled.  cudaErrorNotSupported -> panel_fused.
+cudaError_t panel_pipe(int m, int w, float* X, long long ldx, __half* Xh, long long ldh, int br,
+                       float* Rout, long long ldr, int root_is_global, int* status, int col0,
+                       float* Rb, float* S, int num_sms, cudaStream_t st);
 int fused_panel_smem_bytes();
 int fused_panel_max_rows();
 extern unsigned long long* g_panel_dbg;

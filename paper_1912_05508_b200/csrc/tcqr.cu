@@ -124,6 +124,8 @@ struct FactorWs {
   int* iws = nullptr;       // fused panel arrival counters / flags (zero between launches)
   long long iws_cap = 0;
   unsigned int* cmax = nullptr;  // column max scratch of the split-row cast (n)
+  float* pipeR = nullptr;        // pipelined panel: child R's (NaN between uses)
+  float* pipeS = nullptr;        // pipelined panel: root Q slices (NaN between uses)
   float* R2 = nullptr;           // re-orthogonalization: R of the second pass (n x n)
   float* Rt = nullptr;           // re-orthogonalization: R2 * R1 staging (n x n)
 };
@@ -150,6 +152,8 @@ static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, Facto
   w.iws_cap = 4096 + m / 16;
   w.iws = a.take<int>((size_t)w.iws_cap);
   w.cmax = a.take<unsigned int>((size_t)n + 64);
+  w.pipeR = a.take<float>(32 * 32 * 32);
+  w.pipeS = a.take<float>(32 * 32 * 32);
   if (reorth) {
     w.R2 = a.take<float>((size_t)n * n);
     w.Rt = a.take<float>((size_t)n * n);
@@ -392,6 +396,15 @@ static int panel(FactorWs& ws, int m, int w, float* X, long long ldx, float* Rou
   if (c.nranks <= 1) {
     cudaError_t e = cudaErrorNotSupported;
     PROF(TCQR_K2_MGS, 4.0 * m * w * w, 8.0 * m * w + (Xh ? 2.0 * m * w : 0.0),
+         e = panel_pipe(m, w, X, ldx, Xh, ws.ldh, c.cfg.panel_rows, Rout, ldr, 1, c.d_status,
+                        col0, ws.pipeR, ws.pipeS, c.num_sms, c.stream));
+    if (e == cudaSuccess) {
+      *wrote_h = Xh != nullptr;
+      return 0;
+    }
+    if (e != cudaErrorNotSupported) CK(e);
+    cudaGetLastError();
+    PROF(TCQR_K2_MGS, 4.0 * m * w * w, 8.0 * m * w + (Xh ? 2.0 * m * w : 0.0),
          e = panel_fused(m, w, X, ldx, Xh, ws.ldh, c.cfg.panel_rows, Rout, ldr, 1, c.d_status,
                          col0, ws.pws, ws.pws_cap, ws.iws, ws.iws_cap, c.num_sms, c.stream));
     if (e == cudaSuccess) {
@@ -512,6 +525,7 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));  // INT_MAX-ish = OK
   CK(cudaMemsetAsync(R, 0, sizeof(float) * (size_t)n * n, c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
+  CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   PROF(TCQR_COPY, 0, 8.0 * m * n, CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream)));
   FactorJob J{m, n, Q, (long long)m, R, (long long)n, &ws};
   const bool need_h = n > c.cfg.cutoff;
@@ -1028,6 +1042,7 @@ int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t
   plan_factor_ws(a, m, 32, 1, ws);
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
+  CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   bool wrote_h = false;
   int rc = panel(ws, (int)m, (int)w, X, ldx, R, ldr, 0, nullptr, &wrote_h);
   c.cfg.panel_rows = saved;
