@@ -555,6 +555,8 @@ cudaError_t panel_mgs_level(int rows, int w, float* X, long long ldx, int br, in
   return cudaGetLastError();
 }
 
+unsigned long long* g_panel_dbg = nullptr;
+
 // ==========================================================================================
 // Pipelined single-level panel (nb <= F row blocks, one root): the stacked node is a stack of
 // upper triangles, so the root's MGS step k only touches rows (b, i <= k), which child b produced
@@ -578,6 +580,7 @@ struct PipeArgs {
   int root_is_global;
   int* status;
   int col0;
+  unsigned long long* dbg;  // optional timestamps: child 0 [0..1], apply columns [32+j], root [64+k]
 };
 
 __device__ __forceinline__ float ld_relaxed_f(const float* p) {
@@ -596,6 +599,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
   const float qnan = __int_as_float(0x7fffffff);
   if (b < a.nb) {
     // ----------------------------- child: row block b -----------------------------------------
+    if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[0] = gtimer();
     const int row0 = blk_row(b, a.m, a.nb);
     const int nrows = blk_row(b + 1, a.m, a.nb) - row0;
     float x[RPT][32];
@@ -610,6 +614,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     mgs_rotating<NT, RPT>(x, nrows, w, QSink{qA, nullptr, w}, a.Rb + (long long)b * w * w, w, 1,
                           false, a.status, a.col0, red);
     __syncthreads();
+    if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[1] = gtimer();
     const float* Sb = a.S + (long long)b * w * w;
     for (int j = 0; j < w; ++j) {
       float* sbuf = sj + (j & 1) * 32;
@@ -628,6 +633,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
         sbuf[i] = v;
       }
       __syncthreads();
+      if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[32 + j] = gtimer();
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         const int i = threadIdx.x + r * NT;
@@ -660,6 +666,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     }
     int buf = 0;
     for (int k = 0; k < w; ++k) {
+      if (a.dbg && threadIdx.x == 0) a.dbg[64 + k] = gtimer();
       // lazily load stack rows (b, k): R_b(k, k:w) is ready once child b finished its step k
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
@@ -708,7 +715,8 @@ cudaError_t panel_pipe(int m, int w, float* X, long long ldx, __half* Xh, long l
   const int nb = (m + br - 1) / br;
   if (nb < 2 || nb * w > 1024 || nb > 32) return cudaErrorNotSupported;
   if (nb + 1 > pipe_capacity<256, 4>(num_sms)) return cudaErrorNotSupported;
-  PipeArgs a{X, ldx, Xh, ldh, m, w, nb, Rb, S, Rout, ldr, root_is_global, status, col0};
+  PipeArgs a{X, ldx, Xh, ldh, m, w, nb, Rb, S, Rout, ldr, root_is_global, status, col0,
+             g_panel_dbg};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nb + 1);
   cfg.blockDim = dim3(256);
@@ -722,7 +730,6 @@ cudaError_t panel_pipe(int m, int w, float* X, long long ldx, __half* Xh, long l
   return cudaLaunchKernelEx(&cfg, panel_pipe_kernel<256, 4>, a);
 }
 
-unsigned long long* g_panel_dbg = nullptr;
 
 template <int NT, int RPT>
 static int fused_capacity(int num_sms) {
