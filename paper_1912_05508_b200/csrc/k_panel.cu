@@ -671,19 +671,24 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         if (cb[r] >= 0 && ci[r] == k) {
-          float* src = a.Rb + (long long)cb[r] * w * w + (long long)k * w;
+          float* src = a.Rb + (long long)cb[r] * w * w + (long long)k * w + k;
+          const int cnt = w - k;
+          // all loads in flight at once (a per-value spin would serialize 32 L2 round trips)
+          bool ready = false;
+          while (!ready) {
+            ready = true;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            if (k + c < w) {
-              float v = ld_relaxed_f(src + k + c);
-              while (isnan(v)) {
-                __nanosleep(20);
-                v = ld_relaxed_f(src + k + c);
+            for (int c = 0; c < 32; ++c) {
+              if (c < cnt) {
+                x[r][c] = ld_relaxed_f(src + c);
+                ready &= !isnan(x[r][c]);
               }
-              x[r][c] = v;
-              src[k + c] = qnan;
             }
+            if (!ready) __nanosleep(20);
           }
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (c < cnt) src[c] = qnan;
         }
       }
       mgs_step_any<NT, RPT>(x, srows, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
