@@ -181,7 +181,8 @@ template <int NT, int RPT, int W>
 __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, int k,
                                          float* const (&qp)[RPT], int qstride, float* Rdst,
                                          long long rs, long long cs, bool check, int* status,
-                                         int col0, float* red, int& buf) {
+                                         int col0, float* red, int& buf,
+                                         bool write_lower = true) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float p[32];
@@ -210,7 +211,7 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
   const float rkj = zero ? 0.f : (jl == 0 ? rkk : tot * inv);
   if (warp == 0) {  // R(k, j) at Rdst[k*rs + j*cs]
     if (lane < w - k && lane < W) Rdst[k * rs + (long long)(k + lane) * cs] = rkj;
-    if (lane < k) Rdst[k * rs + (long long)lane * cs] = 0.f;
+    if (write_lower && lane < k) Rdst[k * rs + (long long)lane * cs] = 0.f;
   }
   float q[RPT];
 #pragma unroll
@@ -255,7 +256,8 @@ template <int NT, int RPT>
 __device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int w,
                                              const QSink& qs, float* Rdst, long long rs,
                                              long long cs, bool check, int* status, int col0,
-                                             float* red, unsigned long long* dbg = nullptr) {
+                                             float* red, unsigned long long* dbg = nullptr,
+                                             bool write_lower = true) {
   float* qp[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -268,17 +270,17 @@ __device__ __forceinline__ void mgs_rotating(float (&x)[RPT][32], int nrows, int
     if (dbg && threadIdx.x == 0) dbg[k] = gtimer();
     const int act = w - k;
     if (act > 16)
-      mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, write_lower);
     else if (act > 8)
-      mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, write_lower);
     else if (act > 4)
-      mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, write_lower);
     else if (act > 2)
-      mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, write_lower);
     else if (act > 1)
-      mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, write_lower);
     else
-      mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+      mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, write_lower);
   }
 }
 
@@ -611,8 +613,10 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
       for (int j = 0; j < 32; ++j)
         x[r][j] = (ok && j < w) ? a.X[(long long)(row0 + i) + (long long)j * a.ldx] : 0.f;
     }
+    // only the slots the root consumes are written (no zero lower triangle): a stale value in a
+    // never-consumed slot could alias a polled slot of a later panel with another width
     mgs_rotating<NT, RPT>(x, nrows, w, QSink{qA, nullptr, w}, a.Rb + (long long)b * w * w, w, 1,
-                          false, a.status, a.col0, red);
+                          false, a.status, a.col0, red, nullptr, false);
     __syncthreads();
     if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[1] = gtimer();
     const float* Sb = a.S + (long long)b * w * w;
@@ -648,52 +652,62 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     }
   } else {
     // ----------------------------- root: the stack of child R's -------------------------------
+    // Stack row (b, i) lives in thread 8b + i/4, slot r = i%4, so the nb rows (b, k) needed at
+    // step k are held by nb different threads and loaded in one round trip.  Until a row is
+    // loaded its Q store goes to a private dummy slot (S slots are written only when consumed).
+    __shared__ float dummy[NT * RPT];
     const int srows = a.nb * w;
     float x[RPT][32];
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[r][j] = 0.f;
+    const int tb = threadIdx.x >> 3;          // child block of this thread's rows
+    const int ti0 = (threadIdx.x & 7) * 4;    // first in-block row index
+    const bool tvalid = tb < a.nb;
     float* qp[RPT];
-    int cb[RPT], ci[RPT];
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const int sr = threadIdx.x + r * NT;
-      const int s0 = sr < srows ? sr : 0;
-      cb[r] = sr < srows ? s0 / w : -1;
-      ci[r] = s0 - (s0 / w) * w;
-      qp[r] = a.S + (long long)(s0 / w) * w * w + ci[r];
-    }
+    for (int r = 0; r < RPT; ++r) qp[r] = dummy + threadIdx.x * RPT + r;
     int buf = 0;
     for (int k = 0; k < w; ++k) {
       if (a.dbg && threadIdx.x == 0) a.dbg[64 + k] = gtimer();
-      // lazily load stack rows (b, k): R_b(k, k:w) is ready once child b finished its step k
+      // lazily load stack row (b, k): R_b(k, k:w) is ready once child b finished its step k
+      if (tvalid && k >= ti0 && k < ti0 + RPT) {
+        const int r = k - ti0;
+        float* src = a.Rb + (long long)tb * w * w + (long long)k * w + k;
+        const int cnt = w - k;
+        float v[32];
+        bool ready = false;
+        while (!ready) {
+          ready = true;
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        if (cb[r] >= 0 && ci[r] == k) {
-          float* src = a.Rb + (long long)cb[r] * w * w + (long long)k * w + k;
-          const int cnt = w - k;
-          // all loads in flight at once (a per-value spin would serialize 32 L2 round trips)
-          bool ready = false;
-          while (!ready) {
-            ready = true;
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              if (c < cnt) {
-                x[r][c] = ld_relaxed_f(src + c);
-                ready &= !isnan(x[r][c]);
-              }
+          for (int c = 0; c < 32; ++c) {
+            if (c < cnt) {
+              v[c] = ld_relaxed_f(src + c);
+              ready &= !isnan(v[c]);
+            } else {
+              v[c] = 0.f;
             }
-            if (!ready) __nanosleep(20);
           }
+          if (!ready) __nanosleep(20);
+        }
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (c < cnt) src[c] = qnan;
+        for (int c = 0; c < 32; ++c)
+          if (c < cnt) src[c] = qnan;
+        // place into slot r (compile-time indices via a select chain over RPT)
+#pragma unroll
+        for (int rr = 0; rr < RPT; ++rr) {
+          if (rr == r) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) x[rr][c] = v[c];
+            qp[rr] = a.S + (long long)tb * w * w + k;  // element (row (b,k), col j) at + j*w
+          }
         }
       }
-      mgs_step_any<NT, RPT>(x, srows, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
+      mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
                             a.status, a.col0, red, buf);
     }
+    (void)srows;
   }
 }
 
