@@ -704,6 +704,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
           }
         }
       }
+      if (a.dbg && threadIdx.x == 0) a.dbg[96 + k] = gtimer();
       mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
                             a.status, a.col0, red, buf);
     }

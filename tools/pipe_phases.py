@@ -22,6 +22,7 @@ for m in (32768, 4100):
     print(m, "child0 mgs end", f(d[1]))
     print("  apply cols", [f(v) for v in d[32:64]])
     print("  root steps", [f(v) for v in d[64:96]])
+    print("  root load->step us", [round((int(b_) - int(a_)) / 1000, 2) for a_, b_ in zip(d[64:96], d[96:128])])
     q = Xq.cpu().numpy().astype(np.float64); r = R.cpu().numpy().astype(np.float64)
     a = X.cpu().numpy().astype(np.float64)
     print("  backward", np.linalg.norm(a - q @ r) / np.linalg.norm(a), "orth", np.linalg.norm(q.T @ q - np.eye(32)))
