@@ -591,6 +591,13 @@ __device__ __forceinline__ float ld_relaxed_f(const float* p) {
   return v;
 }
 
+// same load without a memory clobber, so consecutive polls are issued back to back
+__device__ __forceinline__ float ld_relaxed_nc(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
 template <int NT, int RPT>
 __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
   extern __shared__ float fsm[];
@@ -615,9 +622,11 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     }
     // only the slots the root consumes are written (no zero lower triangle): a stale value in a
     // never-consumed slot could alias a polled slot of a later panel with another width
+    
     mgs_rotating<NT, RPT>(x, nrows, w, QSink{qA, nullptr, w}, a.Rb + (long long)b * w * w, w, 1,
                           false, a.status, a.col0, red, nullptr, false);
     __syncthreads();
+    
     if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[1] = gtimer();
     const float* Sb = a.S + (long long)b * w * w;
     for (int j = 0; j < w; ++j) {
@@ -655,7 +664,9 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     // Stack row (b, i) lives in thread 8b + i/4, slot r = i%4, so the nb rows (b, k) needed at
     // step k are held by nb different threads and loaded in one round trip.  Until a row is
     // loaded its Q store goes to a private dummy slot (S slots are written only when consumed).
-    __shared__ float dummy[NT * RPT];
+    // dummy sinks are written at + k * w like real Q rows: sized for the largest offset (the
+    // write-only slots may overlap between threads)
+    __shared__ float dummy[NT * RPT + 32 * 32];
     const int srows = a.nb * w;
     float x[RPT][32];
 #pragma unroll
@@ -669,6 +680,21 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
 #pragma unroll
     for (int r = 0; r < RPT; ++r) qp[r] = dummy + threadIdx.x * RPT + r;
     int buf = 0;
+    // Prefetch: the owner of stack row (b, k+1) copies it into shared memory (cp.async, L2 only)
+    // while step k runs; at step k+1 only a row that was not complete yet is polled again.
+    // Rows start 16-byte aligned when w % 4 == 0 (row k of block b at b*w*w + k*w).
+    const bool pf = (w & 3) == 0;
+    float* stg = fsm + threadIdx.x * 72;  // [2][36] per thread; the child region is unused here
+    auto prefetch = [&](int kk) {
+      const float* src = a.Rb + (long long)tb * w * w + (long long)kk * w;
+      float* dst = stg + (kk & 1) * 36;
+      for (int c = 0; c < w; c += 4) {
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + c));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (pf && tvalid && ti0 == 0) prefetch(0);
     for (int k = 0; k < w; ++k) {
       if (a.dbg && threadIdx.x == 0) a.dbg[64 + k] = gtimer();
       // lazily load stack row (b, k): R_b(k, k:w) is ready once child b finished its step k
@@ -678,22 +704,27 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
         const int cnt = w - k;
         float v[32];
         bool ready = false;
-        while (!ready) {
+        if (pf) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          const float* st = stg + (k & 1) * 36 + k;
           ready = true;
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
-            if (c < cnt) {
-              v[c] = ld_relaxed_f(src + c);
-              ready &= !isnan(v[c]);
-            } else {
-              v[c] = 0.f;
-            }
+            v[c] = c < cnt ? st[c] : 0.f;
+            ready &= !isnan(v[c]);
           }
+
+        }
+        while (!ready) {
+          // all loads issued before any is consumed: one round trip per row, not 32
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c] = c < cnt ? ld_relaxed_nc(src + c) : 0.f;
+          ready = true;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) ready &= !isnan(v[c]);
           if (!ready) __nanosleep(20);
         }
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (c < cnt) src[c] = qnan;
+        if (pf && k + 1 < w && k + 1 < ti0 + RPT) prefetch(k + 1);
         // place into slot r (compile-time indices via a select chain over RPT)
 #pragma unroll
         for (int rr = 0; rr < RPT; ++rr) {
@@ -704,11 +735,21 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
           }
         }
       }
+      if (pf && tvalid && ti0 == k + 1 && k + 1 < w) prefetch(k + 1);
       if (a.dbg && threadIdx.x == 0) a.dbg[96 + k] = gtimer();
       mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
                             a.status, a.col0, red, buf);
     }
-    (void)srows;
+    // every stack row has been consumed: reset the slots to NaN for the next panel in bulk (off
+    // the per-step critical path; the children are still applying the last columns)
+    const long long tot = (long long)srows * w;
+    if ((w & 3) == 0) {
+      float4* p4 = reinterpret_cast<float4*>(a.Rb);
+      const float4 n4 = make_float4(qnan, qnan, qnan, qnan);
+      for (long long i = threadIdx.x; i < tot / 4; i += NT) p4[i] = n4;
+    } else {
+      for (long long i = threadIdx.x; i < tot; i += NT) a.Rb[i] = qnan;
+    }
   }
 }
 

@@ -9,7 +9,7 @@ tq.init(0)
 L = tq.lib()
 L.tcqr_debug_panel_timestamps.argtypes = [ctypes.c_void_p]
 for m in (32768, 4100):
-    dbg = torch.zeros(128, dtype=torch.int64, device="cuda")
+    dbg = torch.zeros(256, dtype=torch.int64, device="cuda")
     L.tcqr_debug_panel_timestamps(ctypes.c_void_p(dbg.data_ptr()))
     X = W.gaussian_cuda(m, 32, 3)
     for _ in range(2):
