@@ -375,10 +375,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16xf32", "data": "synthetic",
             "config": {"workload": wl["name"], "M": M, "n": n, "local_rows": m,
-                       "cutoff": args.cutoff, "panel_rows": 256,
+                       "cutoff": args.cutoff, "panel_rows": tq.default_config().panel_rows,
                        "flops_convention": "2Mn^2-2/3n^3",
                        "l2": "inputs larger than L2 (A 2 GiB fp32 per step; no flush needed)",
                        "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU",

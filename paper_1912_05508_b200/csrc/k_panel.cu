@@ -598,6 +598,32 @@ __device__ __forceinline__ float ld_relaxed_nc(const float* p) {
   return v;
 }
 
+// Root of the pipelined panel: stack row R_b(k, k:w) into a register slot (window column c =
+// global column k + c).  The cp.async-prefetched copy is used when complete; otherwise the row
+// is polled until no NaN sentinel is left.
+__device__ __forceinline__ void pipe_acquire_row(float (&xr)[32], const float* st, const float* src,
+                                                 int cnt, bool pf) {
+  bool ready = false;
+  if (pf) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    ready = true;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      xr[c] = c < cnt ? st[c] : 0.f;
+      ready &= !isnan(xr[c]);
+    }
+  }
+  while (!ready) {
+    // all loads issued before any is consumed: one round trip per row
+#pragma unroll
+    for (int c = 0; c < 32; ++c) xr[c] = c < cnt ? ld_relaxed_nc(src + c) : 0.f;
+    ready = true;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) ready &= !isnan(xr[c]);
+    if (!ready) __nanosleep(20);
+  }
+}
+
 template <int NT, int RPT>
 __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
   extern __shared__ float fsm[];
@@ -624,7 +650,8 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     // never-consumed slot could alias a polled slot of a later panel with another width
     
     mgs_rotating<NT, RPT>(x, nrows, w, QSink{qA, nullptr, w}, a.Rb + (long long)b * w * w, w, 1,
-                          false, a.status, a.col0, red, nullptr, false);
+                          false, a.status, a.col0, red,
+                          nullptr, false);
     __syncthreads();
     
     if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[1] = gtimer();
@@ -697,42 +724,26 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     if (pf && tvalid && ti0 == 0) prefetch(0);
     for (int k = 0; k < w; ++k) {
       if (a.dbg && threadIdx.x == 0) a.dbg[64 + k] = gtimer();
-      // lazily load stack row (b, k): R_b(k, k:w) is ready once child b finished its step k
+      // lazily load stack row (b, k): R_b(k, k:w) is ready once child b finished its step k.
+      // The slot k - ti0 = k % 4 is block-uniform, so the switch is a uniform branch and each
+      // case writes its register slot directly.
       if (tvalid && k >= ti0 && k < ti0 + RPT) {
-        const int r = k - ti0;
         float* src = a.Rb + (long long)tb * w * w + (long long)k * w + k;
-        const int cnt = w - k;
-        float v[32];
-        bool ready = false;
-        if (pf) {
-          asm volatile("cp.async.wait_all;" ::: "memory");
-          const float* st = stg + (k & 1) * 36 + k;
-          ready = true;
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            v[c] = c < cnt ? st[c] : 0.f;
-            ready &= !isnan(v[c]);
-          }
-
-        }
-        while (!ready) {
-          // all loads issued before any is consumed: one round trip per row, not 32
-#pragma unroll
-          for (int c = 0; c < 32; ++c) v[c] = c < cnt ? ld_relaxed_nc(src + c) : 0.f;
-          ready = true;
-#pragma unroll
-          for (int c = 0; c < 32; ++c) ready &= !isnan(v[c]);
-          if (!ready) __nanosleep(20);
+        const float* st = stg + (k & 1) * 36 + k;
+        static_assert(RPT == 4, "slot switch assumes four rows per thread");
+        switch (k & 3) {
+          case 0: pipe_acquire_row(x[0], st, src, w - k, pf); break;
+          case 1: pipe_acquire_row(x[1], st, src, w - k, pf); break;
+          case 2: pipe_acquire_row(x[2], st, src, w - k, pf); break;
+          default: pipe_acquire_row(x[3], st, src, w - k, pf); break;
         }
         if (pf && k + 1 < w && k + 1 < ti0 + RPT) prefetch(k + 1);
-        // place into slot r (compile-time indices via a select chain over RPT)
-#pragma unroll
-        for (int rr = 0; rr < RPT; ++rr) {
-          if (rr == r) {
-#pragma unroll
-            for (int c = 0; c < 32; ++c) x[rr][c] = v[c];
-            qp[rr] = a.S + (long long)tb * w * w + k;  // element (row (b,k), col j) at + j*w
-          }
+        float* const qrow = a.S + (long long)tb * w * w + k;  // (row (b,k), col j) at + j*w
+        switch (k & 3) {
+          case 0: qp[0] = qrow; break;
+          case 1: qp[1] = qrow; break;
+          case 2: qp[2] = qrow; break;
+          default: qp[3] = qrow; break;
         }
       }
       if (pf && tvalid && ti0 == k + 1 && k + 1 < w) prefetch(k + 1);
