@@ -1,6 +1,9 @@
 // k_f32.cu -- K2b: FP32 products of the recursion below the tensor-core cutoff (reading R-A1:
 // the leaf panelQR is single precision, so Alg. 2 lines 8-9 run in FP32 for
 // nodes with w <= cutoff).  Deterministic split-K for R12 = Q1' A2; a row-parallel update.
+#include <algorithm>
+#include <cstdint>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -8,6 +11,7 @@ namespace tcqr {
 
 constexpr int kTnRows = 64;   // rows per shared-memory chunk
 constexpr int kTnPad = 68;    // row stride (floats) of the staged tiles, 16-byte aligned
+constexpr int kResSmemMax = 220 * 1024;  // dynamic shared memory cap of the resident projection
 
 // P_s (h x w2, ld h) = sum over rows [r0_s, r1_s) of Q1(r, :)' A2(r, :).  h, w2 <= 64.
 // 256 threads = 4 row groups x (8 x 8 threads) each owning an 8 x 8 output micro-tile.
@@ -208,6 +212,43 @@ __device__ __forceinline__ unsigned long long gtimer_f() {
 }
 unsigned long long* g_proj_dbg = nullptr;
 
+// Phase 2 of the fused projection: CTA b sums its slice of the h*w2 entries over all G partials
+// in a fixed order (8 partial-groups x 32 entries per pass, all loads of a thread in flight, then
+// a fixed-order combine in shared memory `part` [8][32]); writes T and the R block.
+__device__ __forceinline__ void proj_phase2(const float* P, float* T, float* Rblk, long long ldr,
+                                            int h, int hw, int G, int b, float* part) {
+  const int tid = threadIdx.x;
+  const int e0 = (int)((long long)b * hw / G), e1 = (int)((long long)(b + 1) * hw / G);
+  const int el = tid & 31, pg = tid >> 5;
+  const int gper = (G + 7) / 8, g0 = pg * gper, g1 = min(G, g0 + gper);
+  for (int eb = e0; eb < e1; eb += 32) {
+    const int e = eb + el;
+    float s = 0.f;
+    if (e < e1) {
+      int g = g0;
+      for (; g + 8 <= g1; g += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(P + (long long)(g + u) * hw + e);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      for (; g < g1; ++g) s += __ldcg(P + (long long)g * hw + e);
+    }
+    __syncthreads();
+    part[pg * 32 + el] = s;
+    __syncthreads();
+    if (pg == 0 && e < e1) {
+      float tot = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) tot += part[q * 32 + el];
+      T[e] = tot;
+      const int i = e % h, j = e / h;
+      Rblk[i + (long long)j * ldr] = tot;
+    }
+  }
+}
+
 template <int TD>  // TD = 32 or 64: h, w2 <= TD
 __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w2,
                                                              const float* __restrict__ Q1,
@@ -291,40 +332,7 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
   PDBG(1);
   grid_barrier(bar, G);
   PDBG(2);
-  // ---- phase 2: fixed-order sum of this CTA's slice of entries: 8 partial-groups x 32 entries
-  // per pass, all loads of a thread in flight, then a fixed-order combine in shared memory ----
-  {
-    const int e0 = (int)((long long)b * hw / G), e1 = (int)((long long)(b + 1) * hw / G);
-    float* part = &As[0][0];  // [8][32]
-    const int el = tid & 31, pg = tid >> 5;
-    const int gper = (G + 7) / 8, g0 = pg * gper, g1 = min(G, g0 + gper);
-    for (int eb = e0; eb < e1; eb += 32) {
-      const int e = eb + el;
-      float s = 0.f;
-      if (e < e1) {
-        int g = g0;
-        for (; g + 8 <= g1; g += 8) {
-          float v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = __ldcg(P + (long long)(g + u) * hw + e);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) s += v[u];
-        }
-        for (; g < g1; ++g) s += __ldcg(P + (long long)g * hw + e);
-      }
-      __syncthreads();
-      part[pg * 32 + el] = s;
-      __syncthreads();
-      if (pg == 0 && e < e1) {
-        float tot = 0.f;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) tot += part[q * 32 + el];
-        T[e] = tot;
-        const int i = e % h, j = e / h;
-        Rblk[i + (long long)j * ldr] = tot;
-      }
-    }
-  }
+  proj_phase2(P, T, Rblk, ldr, h, hw, G, b, &As[0][0]);
   PDBG(3);
   grid_barrier(bar, G);
   PDBG(4);
@@ -371,6 +379,179 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
 #undef PDBG
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Resident fused projection: CTA b owns rows [b RB, (b+1) RB) (RB a multiple of 4) and keeps its
+// rows of Q1 and A2 in shared memory from one cp.async round trip to the update, so Q1 and A2
+// are read from HBM once and A2 written once.  Same three phases and the same fixed
+// accumulation orders per entry as f32_project_kernel (rows in increasing order inside a
+// thread, row groups combined 0..3, partials 0..G-1, T columns l = 0..h-1).
+// Shared layout: column c of Q1 / A2 at c*RBp + skew(c), skew = ((c / MT) & 7) * 4 floats, so the
+// eight micro-tile column groups of a warp hit distinct banks with 16-byte row-quad loads.
+// ------------------------------------------------------------------------------------------
+template <int TD>
+__device__ __forceinline__ int res_col(int c, int RBp) {
+  return c * RBp + ((c / (TD / 8)) & 7) * 4;
+}
+
+template <int TD>
+__host__ __device__ constexpr int res_smem_floats(int RBp) {
+  return 2 * (TD * RBp + 32) + TD * TD + TD * TD;
+}
+
+template <int TD>
+__global__ void __launch_bounds__(256, 1) f32_project_res_kernel(
+    int m, int h, int w2, int RB, int RBp, const float* __restrict__ Q1, long long ldq, float* A2,
+    long long lda, float* Rblk, long long ldr, float* P, float* T, int* bar, int vec,
+    unsigned long long* dbg) {
+#define PDBG(i) if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[i] = gtimer_f();
+  constexpr int MT = TD / 8;
+  PDBG(0);
+  extern __shared__ __align__(16) float dsm[];
+  float* Qs = dsm;
+  float* As = Qs + TD * RBp + 32;
+  float* red = As + TD * RBp + 32;  // [TD][TD] row-group combine
+  float* Ts = red + TD * TD;        // [h][TD] R12 for the update; phase-2 scratch before that
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const long long r0 = (long long)b * RB;
+  const int nrows = (int)min((long long)RB, (long long)m - r0);
+  const int nq = RB / 4, hw = h * w2;
+  // ---- load: Q1_b, A2_b -> shared (rows >= nrows and columns >= h / w2 are zero) ----
+  if (vec) {
+    for (int e = tid; e < (h + w2) * nq; e += 256) {
+      const int c = e / nq, q = e - c * nq;
+      const bool isq = c < h;
+      const int cc = isq ? c : c - h;
+      const float* col = isq ? Q1 + r0 + (long long)cc * ldq : A2 + r0 + (long long)cc * lda;
+      const int valid = max(0, min(4, nrows - 4 * q));
+      const float* src = valid > 0 ? col + 4 * q : col;
+      const unsigned dst = static_cast<unsigned>(
+          __cvta_generic_to_shared((isq ? Qs : As) + res_col<TD>(cc, RBp) + 4 * q));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                   "r"(valid * 4) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else {
+    for (int e = tid; e < (h + w2) * RB; e += 256) {
+      const int c = e / RB, r = e - c * RB;
+      const bool isq = c < h;
+      const int cc = isq ? c : c - h;
+      const float v = r < nrows ? (isq ? Q1[r0 + r + (long long)cc * ldq]
+                                       : A2[r0 + r + (long long)cc * lda])
+                                : 0.f;
+      (isq ? Qs : As)[res_col<TD>(cc, RBp) + r] = v;
+    }
+  }
+  for (int e = tid; e < (TD - h) * RB; e += 256) Qs[res_col<TD>(h + e / RB, RBp) + e % RB] = 0.f;
+  for (int e = tid; e < (TD - w2) * RB; e += 256) As[res_col<TD>(w2 + e / RB, RBp) + e % RB] = 0.f;
+  if (vec) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  // ---- phase 1: P_b = Q1_b' A2_b; 4 row groups x (8 x 8 threads) with MT x MT micro-tiles ----
+  {
+    const int grp = tid >> 6, t = tid & 63, ti = t & 7, tj = t >> 3;
+    const float* qb = Qs + res_col<TD>(ti * MT, RBp);  // column ti*MT + a at qb + a*RBp
+    const float* ab = As + res_col<TD>(tj * MT, RBp);
+    float acc[MT][MT];
+#pragma unroll
+    for (int a = 0; a < MT; ++a)
+#pragma unroll
+      for (int c = 0; c < MT; ++c) acc[a][c] = 0.f;
+    for (int q = grp; q < nq; q += 4) {
+      float4 qv[MT], av[MT];
+#pragma unroll
+      for (int a = 0; a < MT; ++a) qv[a] = *reinterpret_cast<const float4*>(qb + a * RBp + 4 * q);
+#pragma unroll
+      for (int c = 0; c < MT; ++c) av[c] = *reinterpret_cast<const float4*>(ab + c * RBp + 4 * q);
+#pragma unroll
+      for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int c = 0; c < MT; ++c) {
+          acc[a][c] = fmaf(qv[a].x, av[c].x, acc[a][c]);
+          acc[a][c] = fmaf(qv[a].y, av[c].y, acc[a][c]);
+          acc[a][c] = fmaf(qv[a].z, av[c].z, acc[a][c]);
+          acc[a][c] = fmaf(qv[a].w, av[c].w, acc[a][c]);
+        }
+    }
+    for (int g = 0; g < 4; ++g) {
+      if (grp == g) {
+#pragma unroll
+        for (int a = 0; a < MT; ++a)
+#pragma unroll
+          for (int c = 0; c < MT; ++c) {
+            float* p = red + (ti * MT + a) * TD + tj * MT + c;
+            *p = (g == 0) ? acc[a][c] : *p + acc[a][c];
+          }
+      }
+      __syncthreads();
+    }
+    float* out = P + (long long)b * hw;
+    for (int e = tid; e < hw; e += 256) {
+      const int i = e % h, j = e / h;
+      out[e] = red[i * TD + j];
+    }
+  }
+  PDBG(1);
+  grid_barrier(bar, G);
+  PDBG(2);
+  proj_phase2(P, T, Rblk, ldr, h, hw, G, b, Ts);
+  PDBG(3);
+  grid_barrier(bar, G);
+  PDBG(4);
+  // ---- phase 3: A2_b -= Q1_b T from shared memory; task = (row quad, TD/4-column group) ----
+  {
+    for (int e = tid; e < h * TD; e += 256) {
+      const int i = e / TD, j = e % TD;
+      Ts[e] = (j < w2) ? __ldcg(T + i + (long long)j * h) : 0.f;
+    }
+    __syncthreads();
+    constexpr int CW = TD / 4;
+    for (int task = tid; task < nq * 4; task += 256) {
+      const int q = task % nq, cg = task / nq;
+      if (4 * q >= nrows || cg * CW >= w2) continue;
+      float acc[4][CW];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int j = 0; j < CW; ++j) acc[r][j] = 0.f;
+      for (int l = 0; l < h; ++l) {
+        const float4 qv = *reinterpret_cast<const float4*>(Qs + res_col<TD>(l, RBp) + 4 * q);
+        const float* tr = Ts + l * TD + cg * CW;
+#pragma unroll
+        for (int j = 0; j < CW; j += 4) {
+          const float4 tv = *reinterpret_cast<const float4*>(tr + j);
+          const float tj4[4] = {tv.x, tv.y, tv.z, tv.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc[0][j + u] = fmaf(qv.x, tj4[u], acc[0][j + u]);
+            acc[1][j + u] = fmaf(qv.y, tj4[u], acc[1][j + u]);
+            acc[2][j + u] = fmaf(qv.z, tj4[u], acc[2][j + u]);
+            acc[3][j + u] = fmaf(qv.w, tj4[u], acc[3][j + u]);
+          }
+        }
+      }
+      const bool full = vec && 4 * q + 4 <= nrows;
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const int col = cg * CW + j;
+        if (col < w2) {
+          const float4 a4 = *reinterpret_cast<const float4*>(As + res_col<TD>(col, RBp) + 4 * q);
+          const float4 o = make_float4(a4.x - acc[0][j], a4.y - acc[1][j], a4.z - acc[2][j],
+                                       a4.w - acc[3][j]);
+          float* dst = A2 + r0 + 4 * q + (long long)col * lda;
+          if (full) {
+            *reinterpret_cast<float4*>(dst) = o;
+          } else {
+            const float ov[4] = {o.x, o.y, o.z, o.w};
+            for (int r = 0; r < 4 && 4 * q + r < nrows; ++r) dst[r] = ov[r];
+          }
+        }
+      }
+    }
+  }
+  PDBG(5);
+#undef PDBG
+}
+
 template <int TD>
 static int f32_project_capacity(int num_sms) {
   static int per_sm = -1;
@@ -381,27 +562,70 @@ static int f32_project_capacity(int num_sms) {
   return per_sm * num_sms;
 }
 
-// One cooperative launch; cudaErrorNotSupported when it cannot be made co-resident.
+template <int TD>
+static int f32_project_res_capacity(int num_sms, int smem) {
+  static int set = 0;
+  if (!set) {
+    cudaFuncSetAttribute(f32_project_res_kernel<TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kResSmemMax);
+    set = 1;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f32_project_res_kernel<TD>, 256,
+                                                    smem) != cudaSuccess)
+    per_sm = 0;
+  return per_sm * num_sms;
+}
+
+static cudaLaunchConfig_t coop_cfg(int G, int smem, cudaStream_t st, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+// One cooperative launch; cudaErrorNotSupported when it cannot be made co-resident.  The
+// resident variant (one CTA per SM, rows kept in shared memory) is used whenever a CTA's rows
+// fit; otherwise the streaming variant re-reads Q1 and A2 in the update.
 cudaError_t f32_project(int m, int h, int w2, const float* Q1, long long ldq, float* A2,
                         long long lda, float* Rblk, long long ldr, float* T, float* P,
                         long long p_cap, int* bar, int num_sms, cudaStream_t st) {
   if (h > 64 || w2 > 64) return cudaErrorNotSupported;
   const bool small = (h <= 32 && w2 <= 32);
+  const int TD = small ? 32 : 64;
+  cudaLaunchAttribute attr[1];
+  {
+    int G = std::min(num_sms, std::max(1, m / 64));
+    int RB = ((m + G - 1) / G + 3) / 4 * 4;
+    G = (m + RB - 1) / RB;
+    const int RBp = (RB + 31) / 32 * 32;
+    const int smem = (int)sizeof(float) * (small ? res_smem_floats<32>(RBp) : res_smem_floats<64>(RBp));
+    const int cap = smem > kResSmemMax ? 0
+                    : small ? f32_project_res_capacity<32>(num_sms, smem)
+                            : f32_project_res_capacity<64>(num_sms, smem);
+    if (smem <= kResSmemMax && G <= cap && (long long)G * h * w2 <= p_cap) {
+      const int vec = ((reinterpret_cast<uintptr_t>(Q1) | reinterpret_cast<uintptr_t>(A2)) % 16 == 0) &&
+                      ldq % 4 == 0 && lda % 4 == 0;
+      cudaLaunchConfig_t cfg = coop_cfg(G, smem, st, attr);
+      return small ? cudaLaunchKernelEx(&cfg, f32_project_res_kernel<32>, m, h, w2, RB, RBp, Q1,
+                                        ldq, A2, lda, Rblk, ldr, P, T, bar, vec, g_proj_dbg)
+                   : cudaLaunchKernelEx(&cfg, f32_project_res_kernel<64>, m, h, w2, RB, RBp, Q1,
+                                        ldq, A2, lda, Rblk, ldr, P, T, bar, vec, g_proj_dbg);
+    }
+  }
+  (void)TD;
   int G = (m + 255) / 256;
   const int cap = small ? f32_project_capacity<32>(num_sms) : f32_project_capacity<64>(num_sms);
   if (G > cap) G = cap;
   if ((long long)G * h * w2 > p_cap) G = (int)(p_cap / ((long long)h * w2));
   if (G < 1) return cudaErrorNotSupported;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(G);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cudaLaunchConfig_t cfg = coop_cfg(G, 0, st, attr);
   return small ? cudaLaunchKernelEx(&cfg, f32_project_kernel<32>, m, h, w2, Q1, ldq, A2, lda,
                                     Rblk, ldr, P, T, bar, g_proj_dbg)
                : cudaLaunchKernelEx(&cfg, f32_project_kernel<64>, m, h, w2, Q1, ldq, A2, lda,
