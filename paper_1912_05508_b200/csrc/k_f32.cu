@@ -187,20 +187,26 @@ __device__ __forceinline__ int ld_relaxed_i(const int* p) {
 __device__ __forceinline__ void st_release_i(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// Sense-free grid barrier: bar[0] arrival counter (returns to 0), bar[1] generation.
+// Sense-free grid barrier: bar[0] arrival counter (returns to 0), bar[1] generation.  Release /
+// acquire at gpu scope instead of sequentially consistent fences: the CTA barrier orders every
+// thread's writes before thread 0's release (cumulativity), thread 0's acquire before every
+// thread's reads after the closing CTA barrier.  Data written before the barrier is read with
+// L1-bypassing loads after it.
 __device__ __forceinline__ void grid_barrier(int* bar, int nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const int g = ld_relaxed_i(bar + 1);
-    __threadfence();
-    if (atomicAdd(bar, 1) == nblocks - 1) {
-      bar[0] = 0;
-      __threadfence();
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == nblocks - 1) {
+      asm volatile("st.relaxed.gpu.global.b32 [%0], 0;" ::"l"(bar) : "memory");
       st_release_i(bar + 1, g + 1);
     } else {
-      while (ld_relaxed_i(bar + 1) == g) __nanosleep(32);
+      int cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+      } while (cur == g);
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -225,15 +231,23 @@ __device__ __forceinline__ void proj_phase2(const float* P, float* T, float* Rbl
     const int e = eb + el;
     float s = 0.f;
     if (e < e1) {
+      // up to 24 partials per thread: all loads in flight, then the fixed-order sum
       int g = g0;
-      for (; g + 8 <= g1; g += 8) {
-        float v[8];
+      for (; g + 24 <= g1; g += 24) {
+        float v[24];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(P + (long long)(g + u) * hw + e);
+        for (int u = 0; u < 24; ++u) v[u] = __ldcg(P + (long long)(g + u) * hw + e);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
+        for (int u = 0; u < 24; ++u) s += v[u];
       }
-      for (; g < g1; ++g) s += __ldcg(P + (long long)g * hw + e);
+      if (g < g1) {
+        float v[24];
+#pragma unroll
+        for (int u = 0; u < 24; ++u) v[u] = g + u < g1 ? __ldcg(P + (long long)(g + u) * hw + e) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 24; ++u)
+          if (g + u < g1) s += v[u];
+      }
     }
     __syncthreads();
     part[pg * 32 + el] = s;
@@ -339,9 +353,23 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
   // ---- phase 3: A2_b -= Q1_b T  (all loads of a row issued before any store) ----
   {
     float* Ts = &Qs[0][0];  // [h][TD]
-    for (int e = tid; e < h * TD; e += 256) {
-      const int i = e / TD, j = e % TD;
-      Ts[i * TD + j] = (j < w2) ? __ldcg(T + i + (long long)j * h) : 0.f;
+    {
+      // coalesced read of T (h x w2, column-major) with all loads of a thread in flight; the
+      // transpose into Ts [h][TD] happens in shared memory
+      constexpr int NL = TD * TD / 256;
+      float tv[NL];
+#pragma unroll
+      for (int u = 0; u < NL; ++u) {
+        const int e = tid + u * 256;
+        tv[u] = e < hw ? __ldcg(T + e) : 0.f;
+      }
+      for (int e = tid; e < h * TD; e += 256) Ts[e] = 0.f;
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < NL; ++u) {
+        const int e = tid + u * 256;
+        if (e < hw) Ts[(e % h) * TD + e / h] = tv[u];
+      }
     }
     __syncthreads();
     for (long long row = r0 + tid; row < r1; row += 256) {
@@ -396,7 +424,7 @@ __device__ __forceinline__ int res_col(int c, int RBp) {
 
 template <int TD>
 __host__ __device__ constexpr int res_smem_floats(int RBp) {
-  return 2 * (TD * RBp + 32) + TD * TD + TD * TD;
+  return 2 * (TD * RBp + 32) + TD * (TD + 1) + TD * TD;
 }
 
 template <int TD>
@@ -410,8 +438,8 @@ __global__ void __launch_bounds__(256, 1) f32_project_res_kernel(
   extern __shared__ __align__(16) float dsm[];
   float* Qs = dsm;
   float* As = Qs + TD * RBp + 32;
-  float* red = As + TD * RBp + 32;  // [TD][TD] row-group combine
-  float* Ts = red + TD * TD;        // [h][TD] R12 for the update; phase-2 scratch before that
+  float* red = As + TD * RBp + 32;  // [TD][TD + 1] row-group combine
+  float* Ts = red + TD * (TD + 1);  // [h][TD] R12 for the update; phase-2 scratch before that
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
   const long long r0 = (long long)b * RB;
   const int nrows = (int)min((long long)RB, (long long)m - r0);
@@ -446,6 +474,7 @@ __global__ void __launch_bounds__(256, 1) f32_project_res_kernel(
   for (int e = tid; e < (TD - w2) * RB; e += 256) As[res_col<TD>(w2 + e / RB, RBp) + e % RB] = 0.f;
   if (vec) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  PDBG(6);
   // ---- phase 1: P_b = Q1_b' A2_b; 4 row groups x (8 x 8 threads) with MT x MT micro-tiles ----
   {
     const int grp = tid >> 6, t = tid & 63, ti = t & 7, tj = t >> 3;
@@ -472,13 +501,15 @@ __global__ void __launch_bounds__(256, 1) f32_project_res_kernel(
           acc[a][c] = fmaf(qv[a].w, av[c].w, acc[a][c]);
         }
     }
+    PDBG(7);
     for (int g = 0; g < 4; ++g) {
       if (grp == g) {
 #pragma unroll
         for (int a = 0; a < MT; ++a)
 #pragma unroll
           for (int c = 0; c < MT; ++c) {
-            float* p = red + (ti * MT + a) * TD + tj * MT + c;
+            float* p = red + (tj * MT + c) * (TD + 1) + ti * MT + a;  // [j][i]: P reads below
+                                                                       // are conflict-free
             *p = (g == 0) ? acc[a][c] : *p + acc[a][c];
           }
       }
@@ -487,7 +518,7 @@ __global__ void __launch_bounds__(256, 1) f32_project_res_kernel(
     float* out = P + (long long)b * hw;
     for (int e = tid; e < hw; e += 256) {
       const int i = e % h, j = e / h;
-      out[e] = red[i * TD + j];
+      out[e] = red[j * (TD + 1) + i];
     }
   }
   PDBG(1);
@@ -499,11 +530,26 @@ __global__ void __launch_bounds__(256, 1) f32_project_res_kernel(
   PDBG(4);
   // ---- phase 3: A2_b -= Q1_b T from shared memory; task = (row quad, TD/4-column group) ----
   {
-    for (int e = tid; e < h * TD; e += 256) {
-      const int i = e / TD, j = e % TD;
-      Ts[e] = (j < w2) ? __ldcg(T + i + (long long)j * h) : 0.f;
+    {
+      // coalesced read of T (h x w2, column-major) with all loads of a thread in flight; the
+      // transpose into Ts [h][TD] happens in shared memory
+      constexpr int NL = TD * TD / 256;
+      float tv[NL];
+#pragma unroll
+      for (int u = 0; u < NL; ++u) {
+        const int e = tid + u * 256;
+        tv[u] = e < hw ? __ldcg(T + e) : 0.f;
+      }
+      for (int e = tid; e < h * TD; e += 256) Ts[e] = 0.f;
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < NL; ++u) {
+        const int e = tid + u * 256;
+        if (e < hw) Ts[(e % h) * TD + e / h] = tv[u];
+      }
     }
     __syncthreads();
+    PDBG(8);
     constexpr int CW = TD / 4;
     for (int task = tid; task < nq * 4; task += 256) {
       const int q = task % nq, cg = task / nq;

@@ -17,11 +17,11 @@ for m in (32768, 8192):
         tq.factor(A)
     torch.cuda.synchronize()
     d = dbg.cpu().numpy()
-    print(m, "w=64", [round((int(v) - int(d[0])) / 1000, 2) for v in d[:6]])
+    print(m, "w=64", [round((int(v) - int(d[0])) / 1000, 2) for v in d[:9]])
     A = W.gaussian_cuda(m, 128, 3)   # last projection of a 128 leaf is 32x32; the middle one 64x64
     for _ in range(2):
         tq.factor(A)
     torch.cuda.synchronize()
     d = dbg.cpu().numpy()
-    print(m, "w=128(last)", [round((int(v) - int(d[0])) / 1000, 2) for v in d[:6]])
+    print(m, "w=128(last)", [round((int(v) - int(d[0])) / 1000, 2) for v in d[:9]])
 L.tcqr_debug_proj_timestamps(None)
