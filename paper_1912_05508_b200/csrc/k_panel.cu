@@ -182,20 +182,29 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
                                          float* const (&qp)[RPT], int qstride, float* Rdst,
                                          long long rs, long long cs, bool check, int* status,
                                          int col0, float* red, int& buf,
-                                         bool write_lower = true) {
+                                         bool write_lower = true, bool idle = false) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float p[32];
+  // idle (warp-uniform): every row of this warp is zero and stays zero in this step; the warp
+  // only contributes a zero partial (x + 0 = x: the sums are unchanged) and meets the barrier
+  float part = 0.f;
+  if (!idle) {
+    float p[32];
 #pragma unroll
-  for (int j = 0; j < W; ++j) {
-    float acc = 0.f;
+    for (int j = 0; j < W; ++j) {
+      float acc = 0.f;
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) acc = fmaf(x[r][0], x[r][j], acc);
-    p[j] = acc;
+      for (int r = 0; r < RPT; ++r) acc = fmaf(x[r][0], x[r][j], acc);
+      p[j] = acc;
+    }
+    part = tr_reduce<W>(p);  // lane j: warp sum of a_k' a_{k+(j%W)}
   }
-  const float part = tr_reduce<W>(p);  // lane j: warp sum of a_k' a_{k+(j%W)}
   red[(buf * NW + warp) * 32 + lane] = part;
   __syncthreads();
+  if (idle) {
+    buf ^= 1;
+    return;
+  }
   float tot = 0.f;
 #pragma unroll
   for (int v = 0; v < NW; ++v) tot += red[(buf * NW + v) * 32 + lane];
@@ -236,20 +245,21 @@ template <int NT, int RPT>
 __device__ __forceinline__ void mgs_step_any(float (&x)[RPT][32], int nrows, int w, int k,
                                              float* const (&qp)[RPT], int qstride, float* Rdst,
                                              long long rs, long long cs, bool check, int* status,
-                                             int col0, float* red, int& buf) {
+                                             int col0, float* red, int& buf,
+                                             bool idle = false) {
   const int act = w - k;
   if (act > 16)
-    mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+    mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
   else if (act > 8)
-    mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+    mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
   else if (act > 4)
-    mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+    mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
   else if (act > 2)
-    mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+    mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
   else if (act > 1)
-    mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+    mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
   else
-    mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf);
+    mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
 }
 
 template <int NT, int RPT>
@@ -655,101 +665,158 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     __syncthreads();
     
     if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[1] = gtimer();
-    const float* Sb = a.S + (long long)b * w * w;
-    for (int j = 0; j < w; ++j) {
-      float* sbuf = sj + (j & 1) * 32;
-      if (threadIdx.x < 32) {
-        const int i = threadIdx.x;
-        float v = 0.f;
-        if (i <= j) {
-          float* src = const_cast<float*>(Sb) + i + j * w;
-          v = ld_relaxed_f(src);
-          while (isnan(v)) {
-            __nanosleep(20);
-            v = ld_relaxed_f(src);
-          }
-          *src = qnan;  // consumed: reset for the next panel
+    // ---- apply: X_b(:, c) = Q_b S(:, c) (S = the root's Q slice of this block, upper
+    // triangular), column groups of 8 as the root publishes them.  Q_b's rows stay in registers
+    // (x is dead after the MGS) and S(l, c) = 0 for l > c, so each output is a full 32-term dot
+    // product in the order l = 0..31 (the zero terms add exactly nothing). ----
+    float qr[RPT][32];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = threadIdx.x + r * NT;
+#pragma unroll
+      for (int l = 0; l < 32; ++l) qr[r][l] = (i < nrows && l < w) ? qA[i * 33 + l] : 0.f;
+    }
+    __syncthreads();                 // qA is free from here on
+    float* Ss = qA;                  // S block, column-major [32][32]
+    float* Sb = a.S + (long long)b * w * w;
+    const int si = threadIdx.x;      // warp 0 lane l = row l of S
+    for (int c0 = 0; c0 < w; c0 += 8) {
+      if (si < 32) {
+        // the group's columns: all loads in flight, then re-poll what the root has not written
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + u;
+          v[u] = (c < w && si <= c) ? ld_relaxed_nc(Sb + si + c * w) : 0.f;
         }
-        sbuf[i] = v;
+        bool ready = true;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) ready &= !isnan(v[u]);
+        while (!ready) {
+          __nanosleep(20);
+          ready = true;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (isnan(v[u])) v[u] = ld_relaxed_nc(Sb + si + (c0 + u) * w);
+            ready &= !isnan(v[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + u;
+          Ss[c * 32 + si] = v[u];
+          if (c < w && si <= c) Sb[si + c * w] = qnan;  // consumed: reset for the next panel
+        }
       }
       __syncthreads();
-      if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[32 + j] = gtimer();
+      if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[32 + min(c0 + 7, w - 1)] = gtimer();
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const int i = threadIdx.x + r * NT;
-        if (i < nrows) {
-          float y = 0.f;
-          for (int l = 0; l <= j; ++l) y = fmaf(qA[i * 33 + l], sbuf[l], y);
-          const long long gi = (long long)(row0 + i) + (long long)j * a.ldx;
-          a.X[gi] = y;
-          if (a.Xh) a.Xh[(long long)(row0 + i) + (long long)j * a.ldh] = __float2half_rn(y);
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u;
+        if (c < w) {
+          const float4* sc = reinterpret_cast<const float4*>(Ss + c * 32);
+          float y[RPT];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) y[r] = 0.f;
+#pragma unroll
+          for (int l4 = 0; l4 < 8; ++l4) {
+            const float4 sv = sc[l4];
+            const float s4[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+#pragma unroll
+              for (int r = 0; r < RPT; ++r) y[r] = fmaf(qr[r][l4 * 4 + e], s4[e], y[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int i = threadIdx.x + r * NT;
+            if (i < nrows) {
+              a.X[(long long)(row0 + i) + (long long)c * a.ldx] = y[r];
+              if (a.Xh) a.Xh[(long long)(row0 + i) + (long long)c * a.ldh] = __float2half_rn(y[r]);
+            }
+          }
         }
       }
     }
   } else {
     // ----------------------------- root: the stack of child R's -------------------------------
-    // Stack row (b, i) lives in thread 8b + i/4, slot r = i%4, so the nb rows (b, k) needed at
-    // step k are held by nb different threads and loaded in one round trip.  Until a row is
-    // loaded its Q store goes to a private dummy slot (S slots are written only when consumed).
-    // dummy sinks are written at + k * w like real Q rows: sized for the largest offset (the
-    // write-only slots may overlap between threads)
+    // Stack row (b, i) lives in warp i/4, lane b, register slot i%4.  A warp whose rows are all
+    // still zero (4*warp > k) is idle in step k; it loads its four rows while idle (loads issued
+    // after the barrier of step 4w-2, checked after the barrier of step 4w-1), so no stack-row
+    // load is on the step chain.  Row i = 4w + r is placed shifted for the window of step 4w:
+    // x[r][c] = R_b(i, 4w + c), zero for c < r -- the steps 4w..i-1 see a zero leading column in
+    // it, which is exactly MGS on a row that starts at column i.  Until step i its Q store goes to
+    // a private dummy slot (S slots are written only when consumed); dummy sinks are written at
+    // + k * w like real Q rows, so they are sized for the largest offset (the write-only slots
+    // may overlap between threads).
     __shared__ float dummy[NT * RPT + 32 * 32];
+    static_assert(NT == 256 && RPT == 4, "root mapping: 8 warps x 4 rows cover 32 stack rows");
     const int srows = a.nb * w;
     float x[RPT][32];
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[r][j] = 0.f;
-    const int tb = threadIdx.x >> 3;          // child block of this thread's rows
-    const int ti0 = (threadIdx.x & 7) * 4;    // first in-block row index
+    const int tb = threadIdx.x & 31;          // child block of this thread's rows
+    const int i0 = (threadIdx.x >> 5) * 4;    // first in-block row index (warp-uniform)
     const bool tvalid = tb < a.nb;
+    const float* rb = a.Rb + (long long)tb * w * w;
     float* qp[RPT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) qp[r] = dummy + threadIdx.x * RPT + r;
-    int buf = 0;
-    // Prefetch: the owner of stack row (b, k+1) copies it into shared memory (cp.async, L2 only)
-    // while step k runs; at step k+1 only a row that was not complete yet is polled again.
-    // Rows start 16-byte aligned when w % 4 == 0 (row k of block b at b*w*w + k*w).
-    const bool pf = (w & 3) == 0;
-    float* stg = fsm + threadIdx.x * 72;  // [2][36] per thread; the child region is unused here
-    auto prefetch = [&](int kk) {
-      const float* src = a.Rb + (long long)tb * w * w + (long long)kk * w;
-      float* dst = stg + (kk & 1) * 36;
-      for (int c = 0; c < w; c += 4) {
-        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + c));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c) : "memory");
+    // issue the loads of this thread's four rows (all in flight; NaN where not yet written)
+    auto load_rows = [&]() {
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = i0 + r;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int e = c - r;  // element (i, i + e)
+          x[r][c] = (tvalid && c >= r && e < w - i) ? ld_relaxed_nc(rb + (long long)i * w + i + e)
+                                                    : 0.f;
+        }
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (pf && tvalid && ti0 == 0) prefetch(0);
+    // wait until no NaN sentinel is left, re-polling only the missing elements
+    auto settle_rows = [&]() {
+      while (true) {
+        bool ready = true;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+#pragma unroll
+          for (int c = 0; c < 32; ++c) ready &= !isnan(x[r][c]);
+        if (__all_sync(0xffffffffu, ready)) break;
+        __nanosleep(20);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int i = i0 + r;
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (isnan(x[r][c])) x[r][c] = ld_relaxed_nc(rb + (long long)i * w + i + (c - r));
+        }
+      }
+    };
+    int buf = 0;
+    if (i0 == 0) {
+      load_rows();
+      settle_rows();
+    }
     for (int k = 0; k < w; ++k) {
       if (a.dbg && threadIdx.x == 0) a.dbg[64 + k] = gtimer();
-      // lazily load stack row (b, k): R_b(k, k:w) is ready once child b finished its step k.
-      // The slot k - ti0 = k % 4 is block-uniform, so the switch is a uniform branch and each
-      // case writes its register slot directly.
-      if (tvalid && k >= ti0 && k < ti0 + RPT) {
-        float* src = a.Rb + (long long)tb * w * w + (long long)k * w + k;
-        const float* st = stg + (k & 1) * 36 + k;
-        static_assert(RPT == 4, "slot switch assumes four rows per thread");
-        switch (k & 3) {
-          case 0: pipe_acquire_row(x[0], st, src, w - k, pf); break;
-          case 1: pipe_acquire_row(x[1], st, src, w - k, pf); break;
-          case 2: pipe_acquire_row(x[2], st, src, w - k, pf); break;
-          default: pipe_acquire_row(x[3], st, src, w - k, pf); break;
-        }
-        if (pf && k + 1 < w && k + 1 < ti0 + RPT) prefetch(k + 1);
+      if (tvalid && k >= i0 && k < i0 + RPT) {
         float* const qrow = a.S + (long long)tb * w * w + k;  // (row (b,k), col j) at + j*w
-        switch (k & 3) {
+        switch (k & 3) {  // uniform: k - i0 = k % 4
           case 0: qp[0] = qrow; break;
           case 1: qp[1] = qrow; break;
           case 2: qp[2] = qrow; break;
           default: qp[3] = qrow; break;
         }
       }
-      if (pf && tvalid && ti0 == k + 1 && k + 1 < w) prefetch(k + 1);
-      if (a.dbg && threadIdx.x == 0) a.dbg[96 + k] = gtimer();
       mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
-                            a.status, a.col0, red, buf);
+                            a.status, a.col0, red, buf, i0 > k);
+      // idle warps (past the step's barrier): prefetch / settle their rows for step i0
+      if (k == i0 - 2 && i0 < w) load_rows();
+      if (k == i0 - 1 && i0 < w) settle_rows();
     }
     // every stack row has been consumed: reset the slots to NaN for the next panel in bulk (off
     // the per-step critical path; the children are still applying the last columns)
