@@ -182,7 +182,8 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
                                          float* const (&qp)[RPT], int qstride, float* Rdst,
                                          long long rs, long long cs, bool check, int* status,
                                          int col0, float* red, int& buf,
-                                         bool write_lower = true, bool idle = false) {
+                                         bool write_lower = true, bool idle = false,
+                                         int bar_cnt = NT) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // idle (warp-uniform): every row of this warp is zero and stays zero in this step; the warp
@@ -200,7 +201,9 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
     part = tr_reduce<W>(p);  // lane j: warp sum of a_k' a_{k+(j%W)}
   }
   red[(buf * NW + warp) * 32 + lane] = part;
-  __syncthreads();
+  // named barrier 1 over the bar_cnt participating threads (all NT unless the caller grows the
+  // participating warp set step by step, as the pipelined root does)
+  asm volatile("bar.sync 1, %0;" ::"r"(bar_cnt) : "memory");
   if (idle) {
     buf ^= 1;
     return;
@@ -246,20 +249,20 @@ __device__ __forceinline__ void mgs_step_any(float (&x)[RPT][32], int nrows, int
                                              float* const (&qp)[RPT], int qstride, float* Rdst,
                                              long long rs, long long cs, bool check, int* status,
                                              int col0, float* red, int& buf,
-                                             bool idle = false) {
+                                             bool idle = false, int bar_cnt = NT) {
   const int act = w - k;
   if (act > 16)
-    mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
+    mgs_step<NT, RPT, 32>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle, bar_cnt);
   else if (act > 8)
-    mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
+    mgs_step<NT, RPT, 16>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle, bar_cnt);
   else if (act > 4)
-    mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
+    mgs_step<NT, RPT, 8>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle, bar_cnt);
   else if (act > 2)
-    mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
+    mgs_step<NT, RPT, 4>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle, bar_cnt);
   else if (act > 1)
-    mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
+    mgs_step<NT, RPT, 2>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle, bar_cnt);
   else
-    mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle);
+    mgs_step<NT, RPT, 1>(x, nrows, w, k, qp, qstride, Rdst, rs, cs, check, status, col0, red, buf, true, idle, bar_cnt);
 }
 
 template <int NT, int RPT>
@@ -740,45 +743,77 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     }
   } else {
     // ----------------------------- root: the stack of child R's -------------------------------
-    // Stack row (b, i) lives in warp i/4, lane b, register slot i%4.  A warp whose rows are all
-    // still zero (4*warp > k) is idle in step k; it loads its four rows while idle (loads issued
-    // after the barrier of step 4w-2, checked after the barrier of step 4w-1), so no stack-row
-    // load is on the step chain.  Row i = 4w + r is placed shifted for the window of step 4w:
-    // x[r][c] = R_b(i, 4w + c), zero for c < r -- the steps 4w..i-1 see a zero leading column in
-    // it, which is exactly MGS on a row that starts at column i.  Until step i its Q store goes to
-    // a private dummy slot (S slots are written only when consumed); dummy sinks are written at
-    // + k * w like real Q rows, so they are sized for the largest offset (the write-only slots
-    // may overlap between threads).
+    // Stack row (b, i) lives in warp i/4, lane b, register slot i%4.  Warp w's rows are all zero
+    // before step 4w, so it stays out of the steps until then: it polls its four rows in the
+    // meantime (off the step chain), joins the step barrier at step 4w-1 (idle: a zero partial)
+    // and computes from step 4w on.  The barrier count grows with the joined warps.  Row
+    // i = 4w + r is placed for the window of step 4w: x[r][c] = R_b(i, 4w + c), zero for c < r --
+    // steps 4w..i-1 see a zero leading column in it, which is exactly MGS on a row that starts at
+    // column i.  Until step i its Q store goes to a private dummy slot (S slots are written only
+    // when consumed); dummy sinks are written at + k * w like real Q rows, so they are sized for
+    // the largest offset (the write-only slots may overlap between threads).
     __shared__ float dummy[NT * RPT + 32 * 32];
     static_assert(NT == 256 && RPT == 4, "root mapping: 8 warps x 4 rows cover 32 stack rows");
+    constexpr int NW = NT / 32;
     const int srows = a.nb * w;
-    float x[RPT][32];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r)
-#pragma unroll
-      for (int j = 0; j < 32; ++j) x[r][j] = 0.f;
+    const int wid = threadIdx.x >> 5;
     const int tb = threadIdx.x & 31;          // child block of this thread's rows
-    const int i0 = (threadIdx.x >> 5) * 4;    // first in-block row index (warp-uniform)
+    const int i0 = wid * 4;                   // first in-block row index (warp-uniform)
     const bool tvalid = tb < a.nb;
-    const float* rb = a.Rb + (long long)tb * w * w;
-    float* qp[RPT];
+    const int nwa = min(NW, (w + 3) / 4);     // warps that hold rows
+    // partial slots of warps that have not joined read as zero
+    __shared__ int s_step;                    // last step whose barrier warp 0 has passed
+    for (int e = threadIdx.x; e < 2 * NW * 32; e += NT) red[e] = 0.f;
+    if (threadIdx.x == 0) s_step = -1;
+    __syncthreads();
+    if (wid < nwa) {
+      const float* rb = a.Rb + (long long)tb * w * w;
+      float x[RPT][32];
+      float* qp[RPT];
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) qp[r] = dummy + threadIdx.x * RPT + r;
-    // issue the loads of this thread's four rows (all in flight; NaN where not yet written)
-    auto load_rows = [&]() {
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const int i = i0 + r;
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int e = c - r;  // element (i, i + e)
-          x[r][c] = (tvalid && c >= r && e < w - i) ? ld_relaxed_nc(rb + (long long)i * w + i + e)
-                                                    : 0.f;
-        }
+      for (int r = 0; r < RPT; ++r) qp[r] = dummy + threadIdx.x * RPT + r;
+      // wait (one load per lane per round) until the last element of this warp's last row is
+      // written -- the child writes the rows in order -- then fetch the four rows with 16-byte
+      // loads from column i0 (x[r][c] = R_b(i0 + r, i0 + c); the lower part c < r is never
+      // written and is zeroed), re-polling elements still NaN.  16-byte loads: the load count,
+      // not the latency, bounds this fetch (~28 cycles per load instruction and warp).
+      {
+        const int il = min(i0 + RPT, w) - 1;
+        const float* sent = rb + (long long)il * w + (w - 1);
+        if (tvalid)
+          while (isnan(ld_relaxed_nc(sent))) __nanosleep(wid == 0 ? 32 : 256);
+        __syncwarp();
       }
-    };
-    // wait until no NaN sentinel is left, re-polling only the missing elements
-    auto settle_rows = [&]() {
+      const bool vec = (w & 3) == 0;
+      auto fetch = [&]() {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int i = i0 + r;
+          const float* src = rb + (long long)i * w + i0;
+          const bool ok = tvalid && i < w;
+          if (vec) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (ok && 4 * q < w - i0)
+                asm volatile("ld.relaxed.gpu.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                             : "l"(src + 4 * q));
+              x[r][4 * q] = v.x;
+              x[r][4 * q + 1] = v.y;
+              x[r][4 * q + 2] = v.z;
+              x[r][4 * q + 3] = v.w;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) x[r][c] = (ok && c < w - i0) ? ld_relaxed_nc(src + c) : 0.f;
+          }
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (c < r) x[r][c] = 0.f;  // below the diagonal: never written
+        }
+      };
+      fetch();
       while (true) {
         bool ready = true;
 #pragma unroll
@@ -786,38 +821,36 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
 #pragma unroll
           for (int c = 0; c < 32; ++c) ready &= !isnan(x[r][c]);
         if (__all_sync(0xffffffffu, ready)) break;
-        __nanosleep(20);
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const int i = i0 + r;
-#pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (isnan(x[r][c])) x[r][c] = ld_relaxed_nc(rb + (long long)i * w + i + (c - r));
-        }
+        __nanosleep(wid == 0 ? 20 : 200);
+        fetch();
       }
-    };
-    int buf = 0;
-    if (i0 == 0) {
-      load_rows();
-      settle_rows();
-    }
-    for (int k = 0; k < w; ++k) {
-      if (a.dbg && threadIdx.x == 0) a.dbg[64 + k] = gtimer();
-      if (tvalid && k >= i0 && k < i0 + RPT) {
-        float* const qrow = a.S + (long long)tb * w * w + k;  // (row (b,k), col j) at + j*w
-        switch (k & 3) {  // uniform: k - i0 = k % 4
-          case 0: qp[0] = qrow; break;
-          case 1: qp[1] = qrow; break;
-          case 2: qp[2] = qrow; break;
-          default: qp[3] = qrow; break;
-        }
+      const int kfirst = wid == 0 ? 0 : i0 - 1;
+      int buf = kfirst & 1;
+      // a joining warp may only arrive at the step barrier once the previous step's barrier has
+      // completed (a named barrier must not see arrivals of two generations with different counts)
+      if (wid > 0) {
+        if (tb == 0)
+          while (*reinterpret_cast<volatile int*>(&s_step) < kfirst - 1) __nanosleep(20);
+        __syncwarp();
       }
-      mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
-                            a.status, a.col0, red, buf, i0 > k);
-      // idle warps (past the step's barrier): prefetch / settle their rows for step i0
-      if (k == i0 - 2 && i0 < w) load_rows();
-      if (k == i0 - 1 && i0 < w) settle_rows();
+      for (int k = kfirst; k < w; ++k) {
+        if (a.dbg && threadIdx.x == 0) a.dbg[64 + k] = gtimer();
+        if (tvalid && k >= i0 && k < i0 + RPT) {
+          float* const qrow = a.S + (long long)tb * w * w + k;  // (row (b,k), col j) at + j*w
+          switch (k & 3) {  // uniform: k - i0 = k % 4
+            case 0: qp[0] = qrow; break;
+            case 1: qp[1] = qrow; break;
+            case 2: qp[2] = qrow; break;
+            default: qp[3] = qrow; break;
+          }
+        }
+        const int cnt = 32 * min(nwa, (k + 1) / 4 + 1);  // warps joined at step k
+        mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
+                              a.status, a.col0, red, buf, k < i0, cnt);
+        if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(&s_step) = k;  // barrier k passed
+      }
     }
+    __syncthreads();
     // every stack row has been consumed: reset the slots to NaN for the next panel in bulk (off
     // the per-step critical path; the children are still applying the last columns)
     const long long tot = (long long)srows * w;
