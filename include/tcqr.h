@@ -66,6 +66,9 @@ typedef struct tcqr_config {
   int reorth;        /* 1: re-orthogonalize (NEXT-1): factor Q1 again,
                         Q <- Q2, R <- R2 * R1; used by tcqr_factor and tcqr_lls_solve (default 0,
                         i.e. Alg. 5 with the single RMGSQR R)                                  */
+  int warm_start;    /* 1: tcqr_lls_solve starts CGLS from the direct QR solution
+                        x0 = R^-1 Q' b (Alg. 1; NEXT-2) instead of x0 = 0
+                        (Alg. 5 line 4); pass 1 then iterates on r0 = b - A x0 (default 0)      */
 } tcqr_config_t;
 
 /* Per-solve report (SPEC.md:296-299 CglsReport). */
@@ -128,6 +131,18 @@ int tcqr_factor(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, flo
  */
 int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const double* b, double* x,
                    double tol, int maxit, tcqr_lls_info_t* info);
+
+/*
+ * tcqr_qr_solve -- the direct QR solve x = R^-1 (Q' b) of Alg. 1 lines 3-4 (PAPER.md:187-198,
+ * Eq. (4); NEXT-2), with Q and R from tcqr_factor (or any thin QR).
+ *   Q : FP32 m x n (ldq >= m; this rank's rows);  R : FP32 n x n upper triangular (ldr >= n);
+ *   b : FP64 m (this rank's rows);  x : FP64 n output (replicated).  Device pointers.
+ * Q' b is an FP64-accumulated GEMV (allreduced over ranks); R^-1 is applied as the FP64
+ * explicit inverse of tcqr_trinv (reading R-A13).  Errors: -1 m, -2 n, -3 Q, -4 ldq, -5 R,
+ * -6 ldr, -7 b, -8 x; +k if R(k,k) is zero or not finite.
+ */
+int tcqr_qr_solve(int64_t m, int64_t n, const float* Q, int64_t ldq, const float* R, int64_t ldr,
+                  const double* b, double* x);
 
 /* Host-pointer variants (end-to-end: the H2D copy of A, b and the D2H copy of the result happen
  * inside the call; A, b, Q, R, x are HOST pointers; pinned memory is used if the caller's is). */

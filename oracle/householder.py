@@ -52,10 +52,17 @@ def back_substitution(r: np.ndarray, y: np.ndarray) -> np.ndarray:
     return x
 
 
+def qr_solve(q: np.ndarray, r: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Alg. 1 lines 3-4 (Eq. (4)): x = R^-1 (Q' b) for any
+    thin QR (Q m x n, R n x n upper triangular), in FP64 -- the direct QR solve of NEXT-2."""
+    q = np.asarray(q, dtype=np.float64)
+    return back_substitution(np.asarray(r, dtype=np.float64), q.T @ np.asarray(b, dtype=np.float64))
+
+
 def householder_lls(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     """Alg. 1 with Householder factors: x = R^-1 (Q' b)."""
     q, r = householder_qr(a)
-    return back_substitution(r, q.T @ np.asarray(b, dtype=np.float64))
+    return qr_solve(q, r, b)
 
 
 def normal_equations_lls(a: np.ndarray, b: np.ndarray) -> np.ndarray:

@@ -33,7 +33,7 @@ class TcqrConfig(ctypes.Structure):
                 ("col_scaling", ctypes.c_int), ("restart", ctypes.c_int),
                 ("tol2", ctypes.c_double), ("stag_window", ctypes.c_int),
                 ("stag_floor", ctypes.c_double), ("use_graphs", ctypes.c_int),
-                ("reorth", ctypes.c_int)]
+                ("reorth", ctypes.c_int), ("warm_start", ctypes.c_int)]
 
 
 class TcqrLlsInfo(ctypes.Structure):
@@ -68,6 +68,7 @@ _SIGS = {
     "tcqr_gemm_nn_update": (ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
     "tcqr_panel_qr": (ctypes.c_int, [_I64, _I64, _P, _I64, _P, _I64, ctypes.c_int]),
     "tcqr_trinv": (ctypes.c_int, [_I64, _P, _I64, _P, _I64]),
+    "tcqr_qr_solve": (ctypes.c_int, [_I64, _I64, _P, _I64, _P, _I64, _P, _P]),
     "tcqr_gemv": (ctypes.c_int, [ctypes.c_int, _I64, _I64, _P, _I64, _P, _P]),
     "tcqr_version": (ctypes.c_char_p, []),
     "tcqr_profile_enable": (ctypes.c_int, [ctypes.c_int]),
@@ -242,6 +243,19 @@ def lls_solve(A, b, tol=1e-10, maxit=200, x=None):
     _check("tcqr_lls_solve", lib().tcqr_lls_solve(m, n, _ptr(A), _ld(A), _ptr(b), _ptr(x),
                                                   float(tol), int(maxit), ctypes.byref(info)))
     return x, info.as_dict()
+
+
+def qr_solve(Q, R, b, x=None):
+    """NEXT-2, Alg. 1 lines 3-4: x = R^-1 (Q' b) (tcqr_qr_solve). Q CUDA
+    float32 m x n column-major, R float32 n x n column-major, b float64 (m,). Returns x (n,)."""
+    torch = _torch()
+    _ensure()
+    m, n = Q.shape
+    if x is None:
+        x = torch.empty(n, dtype=torch.float64, device=Q.device)
+    _check("tcqr_qr_solve", lib().tcqr_qr_solve(m, n, _ptr(Q), _ld(Q), _ptr(R), _ld(R), _ptr(b),
+                                                _ptr(x)))
+    return x
 
 
 def factor_host(A_np):

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <map>
+#include <cmath>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -640,6 +641,7 @@ void tcqr_default_config(tcqr_config_t* c) {
   c->stag_floor = 1e-11;
   c->use_graphs = 1;
   c->reorth = 0;
+  c->warm_start = 0;
 }
 
 int tcqr_set_config(const tcqr_config_t* cfg) {
@@ -649,6 +651,7 @@ int tcqr_set_config(const tcqr_config_t* cfg) {
   if (cfg->panel_rows < 64 || cfg->panel_rows > 1024 || cfg->panel_rows % 32) return -1;
   if (cfg->tol2 <= 0 || cfg->stag_window < 1 || cfg->stag_floor < 0) return -1;
   if (cfg->reorth != 0 && cfg->reorth != 1) return -1;
+  if (cfg->warm_start != 0 && cfg->warm_start != 1) return -1;
   g_ctx.cfg = *cfg;
   return 0;
 }
@@ -821,6 +824,19 @@ static int lls_pass(LlsWs& w, int m, int n, const float* A, long long lda, doubl
   return 0;
 }
 
+// x = M (Q' b): Alg. 1 lines 3-4 with the explicit FP64 inverse M = R^-1 (reading R-A13).  t: n
+// doubles; part: cg_tri_chunks(n) * n doubles; st: a CgState whose `done` flag is cleared here
+// (the CGLS kernels reused below return early while it is set).
+static int direct_solve(int m, int n, const float* Q, long long ldq, const double* M, long long ldm,
+                        const double* b, double* x, double* t, double* part, CgState* st) {
+  Context& c = g_ctx;
+  CK(cudaMemsetAsync(&st->done, 0, sizeof(int), c.stream));
+  CK(gemv_f32_t(m, n, Q, ldq, b, t, c.stream));
+  CKR(allreduce_f64(t, n));
+  CK(cg_launch_tri_n(n, M, ldm, t, x, part, &st->done, c.stream));
+  return 0;
+}
+
 int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const double* b, double* x,
                    double tol, int maxit, tcqr_lls_info_t* info) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -857,13 +873,22 @@ int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const doub
   // K6 set-up: M = inv(R) in FP64 (reading R-A13).
   PROF(TCQR_TRINV, (double)n * n * n / 3.0, 12.0 * n * n,
        CK(trinv_f64((int)n, w.R, n, w.M, n, w.W, c.num_sms, c.stream)));
-  // pass 1: r = b, x = 0
-  CK(cudaMemcpyAsync(w.r, b, sizeof(double) * m, cudaMemcpyDeviceToDevice, c.stream));
   int it1 = 0, reason1 = 0, it2 = 0, reason2 = -1;
   double s01 = 0, fr1 = 0, s02 = 0, fr2 = 0;
+  if (c.cfg.warm_start) {
+    // NEXT-2: x0 = R^-1 Q' b (Alg. 1 lines 3-4) from the factorization's own Q (the working
+    // copy) and M = R^-1; pass 1 then iterates on r0 = b - A x0 and x = x0 + dx.
+    CKR(direct_solve((int)m, (int)n, w.Aw, m, w.M, n, b, w.x1, w.t, w.part, w.st));
+    CK(gemv_f32_n((int)m, (int)n, A, lda, w.x1, w.q, w.part, w.part_cap, c.stream));
+    CK(cg_launch_residual((int)m, b, w.q, w.r, c.stream));
+  } else {
+    // pass 1: r = b, x = 0 (Alg. 5 line 4)
+    CK(cudaMemcpyAsync(w.r, b, sizeof(double) * m, cudaMemcpyDeviceToDevice, c.stream));
+  }
   CKR(lls_pass(w, (int)m, (int)n, A, lda, tol, maxit, 0.0, &it1, &reason1, &s01, &fr1));
   int passes = 1;
   CK(cudaMemcpyAsync(x, w.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  if (c.cfg.warm_start) CK(cg_launch_axpy((int)n, 1.0, w.x1, x, c.stream));
   if (c.cfg.restart && reason1 != 3) {
     // pass 2 (reading R-A12): restart from the true FP64 residual r = b - A x1, tol2, floor
     // relative to pass 1's ||s0||.
@@ -1048,6 +1073,46 @@ int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t
   c.cfg.panel_rows = saved;
   if (rc) return rc;
   return read_status();
+}
+
+int tcqr_qr_solve(int64_t m, int64_t n, const float* Q, int64_t ldq, const float* R, int64_t ldr,
+                  const double* b, double* x) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  if (!Q) return -3;
+  if (ldq < m) return -4;
+  if (!R) return -5;
+  if (ldr < n) return -6;
+  if (!b) return -7;
+  if (!x) return -8;
+  Context& c = g_ctx;
+  begin_call();
+  cudaSetDevice(c.device);
+  // diag(R): a zero or non-finite pivot is a breakdown at that column (status +k)
+  std::vector<float> d((size_t)n);
+  CK(cudaMemcpy2DAsync(d.data(), sizeof(float), R, sizeof(float) * (ldr + 1), sizeof(float), n,
+                       cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  for (int64_t k = 0; k < n; ++k)
+    if (!(d[k] != 0.f) || !std::isfinite(d[k])) return (int)(k + 1);
+  double *M = nullptr, *W = nullptr, *t = nullptr, *part = nullptr;
+  CgState* st = nullptr;
+  CK(cudaMallocAsync(&M, sizeof(double) * n * n, c.stream));
+  CK(cudaMallocAsync(&W, sizeof(double) * trinv_w_count(n), c.stream));
+  CK(cudaMallocAsync(&t, sizeof(double) * n, c.stream));
+  CK(cudaMallocAsync(&part, sizeof(double) * cg_tri_chunks((int)n) * n, c.stream));
+  CK(cudaMallocAsync(&st, sizeof(CgState), c.stream));
+  CK(trinv_f64((int)n, R, ldr, M, n, W, c.num_sms, c.stream));
+  const int rc = direct_solve((int)m, (int)n, Q, ldq, M, n, b, x, t, part, st);
+  cudaFreeAsync(M, c.stream);
+  cudaFreeAsync(W, c.stream);
+  cudaFreeAsync(t, c.stream);
+  cudaFreeAsync(part, c.stream);
+  cudaFreeAsync(st, c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  return rc;
 }
 
 int tcqr_trinv(int64_t n, const float* R, int64_t ldr, double* Minv, int64_t ldm) {

@@ -131,3 +131,34 @@ def test_uniform_few_iterations():
     x, infos = lls_refine(a, b, r, tol=1e-10, maxit=200, target="fp64")
     assert sum(i.iterations for i in infos) <= 20
     assert x_rel_error(x, x_true) < 1e-10
+
+
+# ---- NEXT-2: direct QR solve x = R^-1 Q' b (Alg. 1 lines 3-4) ----
+@pytest.mark.parametrize("m,n,cond", [(60, 12, 1.0), (200, 40, 1e3)])
+def test_oracle_qr_solve_is_the_least_squares_solution(m, n, cond):
+    # any exact thin QR gives the LS solution (Eq. (4)): pinned against
+    # numpy's SVD-based lstsq (a different algorithm) and against the normal equations' optimality
+    # condition A'(b - A x) = 0.
+    from oracle.householder import qr_solve
+    from oracle.qr import rgs
+    a = W.make_matrix("geometric" if cond > 1 else "gaussian", m, n, seed=m + n, cond=cond)
+    a = a.astype(np.float64)
+    b = W.random_rhs(m, seed=m)
+    x_ls = np.linalg.lstsq(a, b, rcond=None)[0]
+    q, r = householder_qr(a)
+    x = qr_solve(q, r, b)
+    assert x_rel_error(x, x_ls) < 1e-13 * cond ** 2
+    g = a.T @ (b - a @ x)
+    assert np.linalg.norm(g) <= 1e-12 * cond * np.linalg.norm(a) * np.linalg.norm(b)
+    # the recursive Gram-Schmidt factors in FP64 give the same solution (Q'Q = I to ~cond*u)
+    q2, r2 = rgs(a, cutoff=32, gemm="fp64")
+    assert x_rel_error(qr_solve(q2, r2, b), x_ls) < 1e-12 * cond ** 2
+
+
+def test_oracle_qr_solve_upper_triangular_hand_example():
+    # R = [[2, 1], [0, 4]], Q = I (3 x 2 slice), b = [4, 8, 5]: Q'b = [4, 8], x2 = 2, x1 = 1
+    from oracle.householder import qr_solve
+    q = np.eye(3)[:, :2]
+    r = np.array([[2.0, 1.0], [0.0, 4.0]])
+    x = qr_solve(q, r, np.array([4.0, 8.0, 5.0]))
+    assert np.array_equal(x, np.array([1.0, 2.0]))
