@@ -230,7 +230,7 @@ __device__ __forceinline__ void mgs_step(float (&x)[RPT][32], int nrows, int w, 
   for (int r = 0; r < RPT; ++r) {
     q[r] = x[r][0] * inv;
     const int row = threadIdx.x + r * NT;
-    if (row < nrows) qp[r][k * qstride] = q[r];
+    if (row < nrows && qp[r]) qp[r][k * qstride] = q[r];  // null sink: the row is not stored
   }
 #pragma unroll
   for (int j = 1; j < W; ++j) {
@@ -681,7 +681,9 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     }
     __syncthreads();                 // qA is free from here on
     float* Ss = qA;                  // S block, column-major [32][32]
-    float* Sb = a.S + (long long)b * w * w;
+    // S element (l, c) of block b at S[(c*w + l)*32 + b]: the root writes one 128-byte line per
+    // step and stack row, the children read with a 128-byte lane stride
+    float* Sb = a.S + b;
     const int si = threadIdx.x;      // warp 0 lane l = row l of S
     for (int c0 = 0; c0 < w; c0 += 8) {
       if (si < 32) {
@@ -690,7 +692,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int c = c0 + u;
-          v[u] = (c < w && si <= c) ? ld_relaxed_nc(Sb + si + c * w) : 0.f;
+          v[u] = (c < w && si <= c) ? ld_relaxed_nc(Sb + (c * w + si) * 32) : 0.f;
         }
         bool ready = true;
 #pragma unroll
@@ -700,7 +702,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
           ready = true;
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            if (isnan(v[u])) v[u] = ld_relaxed_nc(Sb + si + (c0 + u) * w);
+            if (isnan(v[u])) v[u] = ld_relaxed_nc(Sb + ((c0 + u) * w + si) * 32);
             ready &= !isnan(v[u]);
           }
         }
@@ -708,7 +710,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
         for (int u = 0; u < 8; ++u) {
           const int c = c0 + u;
           Ss[c * 32 + si] = v[u];
-          if (c < w && si <= c) Sb[si + c * w] = qnan;  // consumed: reset for the next panel
+          if (c < w && si <= c) Sb[(c * w + si) * 32] = qnan;  // consumed: reset for the next panel
         }
       }
       __syncthreads();
@@ -749,10 +751,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     // and computes from step 4w on.  The barrier count grows with the joined warps.  Row
     // i = 4w + r is placed for the window of step 4w: x[r][c] = R_b(i, 4w + c), zero for c < r --
     // steps 4w..i-1 see a zero leading column in it, which is exactly MGS on a row that starts at
-    // column i.  Until step i its Q store goes to a private dummy slot (S slots are written only
-    // when consumed); dummy sinks are written at + k * w like real Q rows, so they are sized for
-    // the largest offset (the write-only slots may overlap between threads).
-    __shared__ float dummy[NT * RPT + 32 * 32];
+    // column i.  Until step i its Q sink is null (S slots are written only when consumed).
     static_assert(NT == 256 && RPT == 4, "root mapping: 8 warps x 4 rows cover 32 stack rows");
     constexpr int NW = NT / 32;
     const int srows = a.nb * w;
@@ -766,12 +765,49 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     for (int e = threadIdx.x; e < 2 * NW * 32; e += NT) red[e] = 0.f;
     if (threadIdx.x == 0) s_step = -1;
     __syncthreads();
+    // Warp 0's rows (rows 0..3 of every block) gate the first step: all warps fetch them together
+    // (coalesced, one 128-byte row per load instruction, polled until no NaN is left) into
+    // shared memory [block][129] (row r at r*32 + column).
+    float* st0 = fsm;
+    {
+      float v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int t = wid + NW * u, r = t & 3, bb = t >> 2;
+        const bool ok = bb < a.nb && r < w && tb >= r && tb < w;
+        v[u] = ok ? ld_relaxed_nc(a.Rb + (long long)bb * w * w + (long long)r * w + tb) : 0.f;
+      }
+      while (true) {
+        bool ready = true;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) ready &= !isnan(v[u]);
+        if (__all_sync(0xffffffffu, ready)) break;
+        __nanosleep(20);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int t = wid + NW * u, r = t & 3, bb = t >> 2;
+          if (isnan(v[u])) v[u] = ld_relaxed_nc(a.Rb + (long long)bb * w * w + (long long)r * w + tb);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int t = wid + NW * u, r = t & 3, bb = t >> 2;
+        if (bb < a.nb) st0[bb * 129 + r * 32 + tb] = v[u];
+      }
+    }
+    __syncthreads();
     if (wid < nwa) {
       const float* rb = a.Rb + (long long)tb * w * w;
       float x[RPT][32];
       float* qp[RPT];
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) qp[r] = dummy + threadIdx.x * RPT + r;
+      for (int r = 0; r < RPT; ++r) qp[r] = nullptr;
+      if (wid == 0) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+#pragma unroll
+          for (int c = 0; c < 32; ++c) x[r][c] = (tvalid && c >= r) ? st0[tb * 129 + r * 32 + c] : 0.f;
+      } else {
       // wait (one load per lane per round) until the last element of this warp's last row is
       // written -- the child writes the rows in order -- then fetch the four rows with 16-byte
       // loads from column i0 (x[r][c] = R_b(i0 + r, i0 + c); the lower part c < r is never
@@ -781,7 +817,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
         const int il = min(i0 + RPT, w) - 1;
         const float* sent = rb + (long long)il * w + (w - 1);
         if (tvalid)
-          while (isnan(ld_relaxed_nc(sent))) __nanosleep(wid == 0 ? 32 : 256);
+          while (isnan(ld_relaxed_nc(sent))) __nanosleep(256);
         __syncwarp();
       }
       const bool vec = (w & 3) == 0;
@@ -821,8 +857,9 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
 #pragma unroll
           for (int c = 0; c < 32; ++c) ready &= !isnan(x[r][c]);
         if (__all_sync(0xffffffffu, ready)) break;
-        __nanosleep(wid == 0 ? 20 : 200);
+        __nanosleep(200);
         fetch();
+      }
       }
       const int kfirst = wid == 0 ? 0 : i0 - 1;
       int buf = kfirst & 1;
@@ -836,7 +873,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
       for (int k = kfirst; k < w; ++k) {
         if (a.dbg && threadIdx.x == 0) a.dbg[64 + k] = gtimer();
         if (tvalid && k >= i0 && k < i0 + RPT) {
-          float* const qrow = a.S + (long long)tb * w * w + k;  // (row (b,k), col j) at + j*w
+          float* const qrow = a.S + k * 32 + tb;  // (block tb, row k, col j) at + j*w*32
           switch (k & 3) {  // uniform: k - i0 = k % 4
             case 0: qp[0] = qrow; break;
             case 1: qp[1] = qrow; break;
@@ -845,8 +882,8 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
           }
         }
         const int cnt = 32 * min(nwa, (k + 1) / 4 + 1);  // warps joined at step k
-        mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, w, a.Rout, 1, a.ldr, a.root_is_global != 0,
-                              a.status, a.col0, red, buf, k < i0, cnt);
+        mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, 32 * w, a.Rout, 1, a.ldr,
+                              a.root_is_global != 0, a.status, a.col0, red, buf, k < i0, cnt);
         if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(&s_step) = k;  // barrier k passed
       }
     }
