@@ -18,32 +18,38 @@
 
 namespace tcqr {
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool TMAC = false>
 struct TcCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int ST = (BN == 128) ? 6 : 4;
+  // NN keeps four 128 x 32 FP32 C chunks (16 KB each) for the TMA epilogue; its K = h is short,
+  // so fewer mainloop stages suffice
+  static constexpr int CBUF = TMAC ? 4 * 16384 : 0;
+  static constexpr int ST = TMAC ? ((BN == 128) ? 4 : 3) : ((BN == 128) ? 6 : 4);
   static constexpr uint32_t TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = ST * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = ST * STAGE + CBUF + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool TMAC>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   int M, int N, int K, int splits, float* __restrict__ C, long long ldc,
-                   long long split_stride, const float* __restrict__ col_mult) {
-  using Cfg = TcCfg<BN, MODE>;
+                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int splits,
+                   float* __restrict__ C, long long ldc, long long split_stride,
+                   const float* __restrict__ col_mult) {
+  using Cfg = TcCfg<BN, MODE, TMAC>;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, ST = Cfg::ST, STAGE = Cfg::STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * STAGE);
+  float* cbuf = reinterpret_cast<float*>(smem + ST * STAGE);  // NN: [4][32 cols][128 rows]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * STAGE + Cfg::CBUF);
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* cfull = tempty + 2;  // NN: C chunk loaded (4)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
@@ -61,6 +67,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&cfull[i], 1);
+    if (TMAC) tma_prefetch_desc(&tmC);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
@@ -133,6 +141,65 @@ __global__ void __launch_bounds__(192, 1)
         mma_commit(&tfull[acc]);
       }
     }
+  } else if (TMAC) {
+    // ---------------- NN epilogue through TMA (warps 2..5) ----------------
+    // 128 x 32 FP32 chunks of C: TMA-loaded up to three chunks ahead into four shared buffers,
+    // updated in place (C - D diag(col_mult)), TMA-stored back.  One elected thread issues the
+    // copies; the buffers are [col][row] (row fastest), so thread (row) accesses are conflict-free.
+    const int q = warp & 3;
+    const int rt = q * 32 + lane;  // row within the tile (= TMEM lane)
+    const bool issuer = (warp == 2 && lane == 0);
+    uint32_t cph = 0;
+    int it = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+      const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int ncol = min(BN, N - nb * BN), nch = (ncol + 31) / 32;
+      if (issuer) {
+        bulk_wait_read<0>();  // the previous tile's stores have read their buffers
+        for (int c = 0; c < 3 && c < nch; ++c) {
+          mbar_arrive_expect_tx(&cfull[c], 16384);
+          tma_load_2d(cbuf + c * 4096, &tmC, &cfull[c], mb * BM, nb * BN + 32 * c);
+        }
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < nch; ++c) {
+        const int buf = c & 3;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + 32 * c, r);
+        mbar_wait(&cfull[buf], (cph >> buf) & 1);
+        cph ^= 1u << buf;
+        tmem_ld_wait();
+        float* cb = cbuf + buf * 4096;
+        const int col0 = nb * BN + 32 * c;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = col0 + j;
+          const float mlt = col_mult ? (col < N ? __ldg(col_mult + col) : 0.f) : 1.f;
+          cb[j * 128 + rt] = cb[j * 128 + rt] - __uint_as_float(r[j]) * mlt;
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA store
+        named_bar_sync(1, 128);
+        if (issuer) {
+          tma_store_2d(&tmC, cb, mb * BM, col0);
+          bulk_commit();
+          if (c + 3 < nch) {
+            const int nbuf = (c + 3) & 3;  // last used by chunk c-1, whose store must have read it
+            bulk_wait_read<1>();
+            mbar_arrive_expect_tx(&cfull[nbuf], 16384);
+            tma_load_2d(cbuf + nbuf * 4096, &tmC, &cfull[nbuf], mb * BM, nb * BN + 32 * (c + 3));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if (issuer) bulk_wait<0>();
   } else {  // ---------------- epilogue warps 2..5 ----------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int it = 0;
@@ -287,22 +354,37 @@ static bool make_map_f16(CUtensorMap* map, const void* base, uint64_t inner, uin
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int MODE>
-static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
-                             int splits, float* C, long long ldc, long long sstride,
-                             const float* mult, int num_sms, cudaStream_t st) {
-  using Cfg = TcCfg<BN, MODE>;
+// 2-D FP32 map (no swizzle) for the NN epilogue's C chunks: 128 rows x 32 columns.
+static bool make_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                         uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int MODE, bool TMAC = false>
+static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
+                             int M, int N, int K, int splits, float* C, long long ldc,
+                             long long sstride, const float* mult, int num_sms, cudaStream_t st) {
+  using Cfg = TcCfg<BN, MODE, TMAC>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE, TMAC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int tiles = ((M + 127) / 128) * ((N + BN - 1) / BN) * splits;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  tc_gemm_kernel<BN, MODE><<<grid, 192, Cfg::SMEM, st>>>(a, b, M, N, K, splits, C, ldc, sstride,
-                                                         mult);
+  tc_gemm_kernel<BN, MODE, TMAC><<<grid, 192, Cfg::SMEM, st>>>(a, b, cm, M, N, K, splits, C, ldc,
+                                                               sstride, mult);
   return cudaGetLastError();
 }
 
@@ -331,15 +413,16 @@ cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, 
   }
   cudaError_t e;
   if (splits == 1) {
-    e = (BN == 256) ? launch_tc<256, kModeTN>(ma, mb, h, w2, m, 1, C, ldc, 0, col_mult, num_sms, st)
-                    : launch_tc<128, kModeTN>(ma, mb, h, w2, m, 1, C, ldc, 0, col_mult, num_sms, st);
+    e = (BN == 256)
+            ? launch_tc<256, kModeTN>(ma, mb, ma, h, w2, m, 1, C, ldc, 0, col_mult, num_sms, st)
+            : launch_tc<128, kModeTN>(ma, mb, ma, h, w2, m, 1, C, ldc, 0, col_mult, num_sms, st);
     return e;
   }
   const long long sstride = (long long)h * w2;
-  e = (BN == 256) ? launch_tc<256, kModeTN>(ma, mb, h, w2, m, splits, P, h, sstride, nullptr,
-                                            num_sms, st)
-                  : launch_tc<128, kModeTN>(ma, mb, h, w2, m, splits, P, h, sstride, nullptr,
-                                            num_sms, st);
+  e = (BN == 256) ? launch_tc<256, kModeTN>(ma, mb, ma, h, w2, m, splits, P, h, sstride,
+                                            nullptr, num_sms, st)
+                  : launch_tc<128, kModeTN>(ma, mb, ma, h, w2, m, splits, P, h, sstride,
+                                            nullptr, num_sms, st);
   if (e != cudaSuccess) return e;
   const long long total = (long long)h * w2;
   int grid = (int)((total + 31) / 32);
@@ -357,9 +440,21 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
   const int BN = (w2 > 128) ? 256 : 128;
   if (!make_map_f16(&ma, Qh, m, h, ldq, 64, 64)) return cudaErrorInvalidValue;
   if (!make_map_f16(&mb, Bh, h, w2, ldb, 64, BN)) return cudaErrorInvalidValue;
-  return (BN == 256)
-             ? launch_tc<256, kModeNN>(ma, mb, m, w2, h, 1, C, ldc, 0, col_mult, num_sms, st)
-             : launch_tc<128, kModeNN>(ma, mb, m, w2, h, 1, C, ldc, 0, col_mult, num_sms, st);
+  // TMA epilogue (C chunks through shared memory) when the update is epilogue-bound (short K = h)
+  // and C's columns are 16-byte aligned; the direct-load epilogue with deeper mainloop pipelining
+  // otherwise
+  CUtensorMap mc;
+  const bool tmac = h <= 2048 && (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0) &&
+                    make_map_f32(&mc, C, m, w2, ldc, 128, 32);
+  if (tmac)
+    return (BN == 256) ? launch_tc<256, kModeNN, true>(ma, mb, mc, m, w2, h, 1, C, ldc, 0, col_mult,
+                                                       num_sms, st)
+                       : launch_tc<128, kModeNN, true>(ma, mb, mc, m, w2, h, 1, C, ldc, 0, col_mult,
+                                                       num_sms, st);
+  return (BN == 256) ? launch_tc<256, kModeNN>(ma, mb, ma, m, w2, h, 1, C, ldc, 0, col_mult, num_sms,
+                                               st)
+                     : launch_tc<128, kModeNN>(ma, mb, ma, m, w2, h, 1, C, ldc, 0, col_mult, num_sms,
+                                               st);
 }
 
 }  // namespace tcqr
