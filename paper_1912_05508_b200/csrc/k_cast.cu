@@ -191,7 +191,7 @@ cudaError_t r12_finalize(int h, int w2, const float* T, long long ldt, float* Rb
 }
 
 __global__ void copy_validate_kernel(int m, const float* __restrict__ A, long long lda,
-                                     float* __restrict__ Q, long long ldq, int* status) {
+                                     float* __restrict__ Q, long long ldq, int* status, int col0) {
   const int j = blockIdx.y;
   const float* a = A + (long long)j * lda;
   float* q = Q + (long long)j * ldq;
@@ -201,16 +201,16 @@ __global__ void copy_validate_kernel(int m, const float* __restrict__ A, long lo
     bad |= !isfinite(v);
     if (q != a) q[i] = v;
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMin(status, j + 1);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMin(status, col0 + j + 1);
 }
 
 cudaError_t copy_validate(int m, int n, const float* A, long long lda, float* Q, long long ldq,
-                          int* status, cudaStream_t st) {
+                          int* status, cudaStream_t st, int col0) {
   if (m <= 0 || n <= 0) return cudaSuccess;
   int gx = (m + 1023) / 1024;
   if (gx > 64) gx = 64;
   dim3 grid(gx, n);
-  copy_validate_kernel<<<grid, 256, 0, st>>>(m, A, lda, Q, ldq, status);
+  copy_validate_kernel<<<grid, 256, 0, st>>>(m, A, lda, Q, ldq, status, col0);
   return cudaGetLastError();
 }
 

@@ -611,31 +611,12 @@ __device__ __forceinline__ float ld_relaxed_nc(const float* p) {
   return v;
 }
 
-// Root of the pipelined panel: stack row R_b(k, k:w) into a register slot (window column c =
-// global column k + c).  The cp.async-prefetched copy is used when complete; otherwise the row
-// is polled until no NaN sentinel is left.
-__device__ __forceinline__ void pipe_acquire_row(float (&xr)[32], const float* st, const float* src,
-                                                 int cnt, bool pf) {
-  bool ready = false;
-  if (pf) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    ready = true;
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      xr[c] = c < cnt ? st[c] : 0.f;
-      ready &= !isnan(xr[c]);
-    }
-  }
-  while (!ready) {
-    // all loads issued before any is consumed: one round trip per row
-#pragma unroll
-    for (int c = 0; c < 32; ++c) xr[c] = c < cnt ? ld_relaxed_nc(src + c) : 0.f;
-    ready = true;
-#pragma unroll
-    for (int c = 0; c < 32; ++c) ready &= !isnan(xr[c]);
-    if (!ready) __nanosleep(20);
-  }
-}
+// Hand-off sentinel of the pipelined panel: the all-ones bit pattern (a negative quiet NaN) that
+// the workspace memset (0xff bytes) and the consumers' resets write.  Arithmetic never produces
+// it -- the GPU's NaN results are the canonical 0x7fffffff and every published value is an
+// arithmetic result -- so a NaN in the data (non-finite input) cannot be mistaken for "not yet
+// written" and stall the pipeline.
+__device__ __forceinline__ bool pending(float v) { return __float_as_uint(v) == 0xffffffffu; }
 
 template <int NT, int RPT>
 __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
@@ -644,7 +625,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
   float* sj = fsm + ((NT * RPT * 33 + 3) & ~3);         // child: [2][32] current S column
   float* red = sj + 64;                                 // [2][NT/32][32]
   const int w = a.w, b = blockIdx.x;
-  const float qnan = __int_as_float(0x7fffffff);
+  const float qnan = __uint_as_float(0xffffffffu);  // the hand-off sentinel
   if (b < a.nb) {
     // ----------------------------- child: row block b -----------------------------------------
     if (a.dbg && b == 0 && threadIdx.x == 0) a.dbg[0] = gtimer();
@@ -696,14 +677,14 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
         }
         bool ready = true;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) ready &= !isnan(v[u]);
+        for (int u = 0; u < 8; ++u) ready &= !pending(v[u]);
         while (!ready) {
           __nanosleep(20);
           ready = true;
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            if (isnan(v[u])) v[u] = ld_relaxed_nc(Sb + ((c0 + u) * w + si) * 32);
-            ready &= !isnan(v[u]);
+            if (pending(v[u])) v[u] = ld_relaxed_nc(Sb + ((c0 + u) * w + si) * 32);
+            ready &= !pending(v[u]);
           }
         }
 #pragma unroll
@@ -780,13 +761,13 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
       while (true) {
         bool ready = true;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) ready &= !isnan(v[u]);
+        for (int u = 0; u < 16; ++u) ready &= !pending(v[u]);
         if (__all_sync(0xffffffffu, ready)) break;
         __nanosleep(20);
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const int t = wid + NW * u, r = t & 3, bb = t >> 2;
-          if (isnan(v[u])) v[u] = ld_relaxed_nc(a.Rb + (long long)bb * w * w + (long long)r * w + tb);
+          if (pending(v[u])) v[u] = ld_relaxed_nc(a.Rb + (long long)bb * w * w + (long long)r * w + tb);
         }
       }
 #pragma unroll
@@ -817,7 +798,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
         const int il = min(i0 + RPT, w) - 1;
         const float* sent = rb + (long long)il * w + (w - 1);
         if (tvalid)
-          while (isnan(ld_relaxed_nc(sent))) __nanosleep(256);
+          while (pending(ld_relaxed_nc(sent))) __nanosleep(256);
         __syncwarp();
       }
       const bool vec = (w & 3) == 0;
@@ -855,7 +836,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
 #pragma unroll
-          for (int c = 0; c < 32; ++c) ready &= !isnan(x[r][c]);
+          for (int c = 0; c < 32; ++c) ready &= !pending(x[r][c]);
         if (__all_sync(0xffffffffu, ready)) break;
         __nanosleep(200);
         fetch();

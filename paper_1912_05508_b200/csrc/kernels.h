@@ -28,7 +28,7 @@ cudaError_t r12_finalize(int h, int w2, const float* T, long long ldt, float* Rb
                          __half* R12h, long long ldh2, float* inv_s2, int scaling, cudaStream_t st);
 // Copy A -> Q (ld m) and flag the first non-finite column in status.
 cudaError_t copy_validate(int m, int n, const float* A, long long lda, float* Q, long long ldq,
-                          int* status, cudaStream_t st);
+                          int* status, cudaStream_t st, int col0 = 0);
 // Copy an h x w block (ld src / dst).
 cudaError_t copy_block(int h, int w, const float* S, long long lds, float* D, long long ldd,
                        cudaStream_t st);

@@ -61,6 +61,7 @@ struct Context {
   cudaStream_t stream = nullptr;       // internal non-blocking stream (capturable)
   cudaStream_t user_stream = nullptr;  // the caller's stream (may be the legacy NULL stream)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // copy streams of the streamed host factor
   int num_sms = 148;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
@@ -437,6 +438,18 @@ static int panel(FactorWs& ws, int m, int w, float* X, long long ldx, float* Rou
 // ------------------------------------------------------------------------------------------
 // Alg. 2 recursion on columns [c0, c0+w) of the working matrix Q (m x n, ldq), R (ldr).
 // ------------------------------------------------------------------------------------------
+// Streamed host factorization (tcqr_factor_host): the columns arrive in chunks (the subtrees at a
+// fixed recursion depth) on an H2D stream, and each chunk's Q columns and R columns go back on a
+// D2H stream as soon as its subtree is done, overlapping the PCIe transfers with the recursion.
+struct StreamPlan {
+  std::vector<int> a, b;             // chunk j = columns [a[j], b[j])
+  std::vector<cudaEvent_t> ev_in;    // chunk j resident (and validated) on the device
+  std::vector<char> waited;          // the compute stream already waits on ev_in[j]
+  std::vector<cudaEvent_t> ev_fin;   // chunk j final
+  float* hQ = nullptr;               // host outputs (ld m and ld n)
+  float* hR = nullptr;
+};
+
 struct FactorJob {
   int m, n;
   float* Q;
@@ -444,7 +457,37 @@ struct FactorJob {
   float* R;
   long long ldr;
   FactorWs* ws;
+  StreamPlan* sp = nullptr;
 };
+
+// The compute stream waits for every chunk overlapping columns [c0, c1).
+static void need_cols(FactorJob& J, int c0, int c1) {
+  StreamPlan* sp = J.sp;
+  if (!sp) return;
+  for (size_t j = 0; j < sp->a.size(); ++j)
+    if (!sp->waited[j] && sp->a[j] < c1 && c0 < sp->b[j]) {
+      cudaStreamWaitEvent(g_ctx.stream, sp->ev_in[j], 0);
+      sp->waited[j] = 1;
+    }
+}
+
+// After the subtree on [c0, c0+w): if it is a chunk, ship its Q columns and R columns (all n rows:
+// R(0:c0, cols) came from ancestors' R12 blocks, the rest of the column is this subtree's or zero).
+static int chunk_done(FactorJob& J, int c0, int w) {
+  StreamPlan* sp = J.sp;
+  if (!sp) return 0;
+  Context& c = g_ctx;
+  for (size_t j = 0; j < sp->a.size(); ++j)
+    if (sp->a[j] == c0 && sp->b[j] == c0 + w) {
+      CK(cudaEventRecord(sp->ev_fin[j], c.stream));
+      CK(cudaStreamWaitEvent(c.s_d2h, sp->ev_fin[j], 0));
+      CK(cudaMemcpyAsync(sp->hQ + (long long)c0 * J.m, J.Q + (long long)c0 * J.ldq,
+                         sizeof(float) * (size_t)J.m * w, cudaMemcpyDeviceToHost, c.s_d2h));
+      CK(cudaMemcpyAsync(sp->hR + (long long)c0 * J.n, J.R + (long long)c0 * J.ldr,
+                         sizeof(float) * (size_t)J.n * w, cudaMemcpyDeviceToHost, c.s_d2h));
+    }
+  return 0;
+}
 
 static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   Context& c = g_ctx;
@@ -453,15 +496,17 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   float* Qc = J.Q + (long long)c0 * J.ldq;
   if (w <= 32) {
     bool wrote_h = false;
+    need_cols(J, c0, c0 + w);
     CKR(panel(ws, m, w, Qc, J.ldq, J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0,
               need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, &wrote_h));
-    if (wrote_h) return 0;
+    if (wrote_h) return chunk_done(J, c0, w);
   } else {
     const int h = split_point(w), w2 = w - h;
     const bool tc = w > c.cfg.cutoff;
     CKR(rgs(J, c0, h, tc || need_h));  // Alg. 2 line 7
     float* A2 = J.Q + (long long)(c0 + h) * J.ldq;
     float* Rblk = J.R + c0 + (long long)(c0 + h) * J.ldr;
+    need_cols(J, c0 + h, c0 + w);
     if (tc) {
       // Alg. 2 line 8 on tensor cores: K1 cast of A2, K3 split-K TN, [allreduce], finalize.
       __half* A1h = ws.Qh + (long long)c0 * ws.ldh;
@@ -508,7 +553,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
            CK(f32_nn_update(m, h, w2, Qc, J.ldq, ws.T, A2, J.ldq, c.stream)));
     }
     CKR(rgs(J, c0 + h, w2, need_h));  // Alg. 2 line 9
-    return 0;
+    return chunk_done(J, c0, w);
   }
   if (need_h) {
     // Q columns of this panel are final: emit their FP16 shadow for the GEMMs above.
@@ -516,7 +561,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
          CK(cast_scale(m, w, Qc, J.ldq, ws.Qh + (long long)c0 * ws.ldh, ws.ldh, nullptr, 0,
                        nullptr, 0, nullptr, c.stream)));
   }
-  return 0;
+  return chunk_done(J, c0, w);
 }
 
 // Enqueue the whole factorization (no host synchronization inside: graph-capturable).
@@ -689,6 +734,9 @@ int tcqr_finalize(void) {
   if (c.ev_in) cudaEventDestroy(c.ev_in);
   if (c.ev_out) cudaEventDestroy(c.ev_out);
   if (c.stream) cudaStreamDestroy(c.stream);
+  if (c.s_h2d) cudaStreamDestroy(c.s_h2d);
+  if (c.s_d2h) cudaStreamDestroy(c.s_d2h);
+  c.s_h2d = c.s_d2h = nullptr;
   c.ev_in = c.ev_out = nullptr;
   c.stream = nullptr;
   c.user_ws = nullptr;
@@ -717,6 +765,9 @@ int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int ran
     return TCQR_ERR_CUDA;
   cudaEventCreateWithFlags(&c.ev_in, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c.ev_out, cudaEventDisableTiming);
+  if (cudaStreamCreateWithFlags(&c.s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c.s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+    return TCQR_ERR_CUDA;
   c.num_sms = prop.multiProcessorCount;
   c.rank = rank;
   c.nranks = nranks;
@@ -921,6 +972,75 @@ int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const doub
   return 0;
 }
 
+static void plan_chunks(int c0, int w, int target, int cutoff, StreamPlan& sp) {
+  if (w <= target || w <= 2 * cutoff) {
+    sp.a.push_back(c0);
+    sp.b.push_back(c0 + w);
+    return;
+  }
+  const int h = split_point(w);
+  plan_chunks(c0, h, target, cutoff, sp);
+  plan_chunks(c0 + h, w - h, target, cutoff, sp);
+}
+
+// Streamed variant of tcqr_factor_host (one rank, no re-orthogonalization): H2D of column chunks
+// on s_h2d, the recursion on the compute stream waiting per chunk, D2H of each finished chunk's
+// Q and R columns on s_d2h.  No CUDA graph (the chunk events order the replay).
+static int factor_host_streamed(int m, int n, const float* A, long long lda, float* Q, float* R,
+                                float* dQ, float* dR) {
+  Context& c = g_ctx;
+  const size_t need = ws_bytes(m, n, 0, c.nranks, 0);
+  char* base = get_ws(need);
+  if (!base) return TCQR_ERR_OOM;
+  Arena ar{base, 0};
+  FactorWs ws;
+  plan_factor_ws(ar, m, n, c.nranks, ws, false);
+  StreamPlan sp;
+  plan_chunks(0, n, std::max(n / 8, 1), c.cfg.cutoff, sp);
+  const size_t nc = sp.a.size();
+  sp.ev_in.resize(nc);
+  sp.ev_fin.resize(nc);
+  sp.waited.assign(nc, 0);
+  sp.hQ = Q;
+  sp.hR = R;
+  for (size_t j = 0; j < nc; ++j) {
+    cudaEventCreateWithFlags(&sp.ev_in[j], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&sp.ev_fin[j], cudaEventDisableTiming);
+  }
+  int rc = 0;
+  // H2D stream: status reset, then each chunk copied and validated in place (status +k global)
+  cudaStreamWaitEvent(c.s_h2d, c.ev_in, 0);
+  cudaStreamWaitEvent(c.s_d2h, c.ev_in, 0);
+  CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.s_h2d));
+  for (size_t j = 0; j < nc; ++j) {
+    const int a = sp.a[j], w = sp.b[j] - sp.a[j];
+    CK(cudaMemcpy2DAsync(dQ + (long long)a * m, sizeof(float) * m, A + (long long)a * lda,
+                         sizeof(float) * lda, sizeof(float) * m, w, cudaMemcpyHostToDevice,
+                         c.s_h2d));
+    CK(copy_validate(m, w, dQ + (long long)a * m, m, dQ + (long long)a * m, m, c.d_status,
+                     c.s_h2d, a));
+    CK(cudaEventRecord(sp.ev_in[j], c.s_h2d));
+  }
+  // compute stream
+  CK(cudaMemsetAsync(dR, 0, sizeof(float) * (size_t)n * n, c.stream));
+  CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
+  CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
+  FactorJob J{m, n, dQ, (long long)m, dR, (long long)n, &ws, &sp};
+  rc = rgs(J, 0, n, n > c.cfg.cutoff);
+  if (rc == 0) {
+    need_cols(J, 0, n);  // every validation has finished before the status is read
+    CK(zero_lower(n, dR, n, c.stream));
+    rc = read_status();
+  }
+  cudaStreamSynchronize(c.s_h2d);
+  cudaStreamSynchronize(c.s_d2h);
+  for (size_t j = 0; j < nc; ++j) {
+    cudaEventDestroy(sp.ev_in[j]);
+    cudaEventDestroy(sp.ev_fin[j]);
+  }
+  return rc;
+}
+
 int tcqr_factor_host(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, float* R) {
   if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
   if (m < 1) return -1;
@@ -937,6 +1057,10 @@ int tcqr_factor_host(int64_t m, int64_t n, const float* A, int64_t lda, float* Q
   if (!stage) return TCQR_ERR_OOM;
   float* dQ = reinterpret_cast<float*>(stage);
   float* dR = reinterpret_cast<float*>(stage + qbytes);
+  if (!c.cfg.reorth && c.nranks == 1 && n > 2 * c.cfg.cutoff && !g_prof && m >= n) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return factor_host_streamed((int)m, (int)n, A, lda, Q, R, dQ, dR);
+  }
   CK(cudaMemcpy2DAsync(dQ, sizeof(float) * m, A, sizeof(float) * lda, sizeof(float) * m, n,
                        cudaMemcpyHostToDevice, c.stream));
   int rc = tcqr_factor(m, n, dQ, m, dQ, dR);

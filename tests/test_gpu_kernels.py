@@ -170,3 +170,18 @@ def test_reorth_product_is_r2_r1(tq):
     assert np.array_equal(r, np.triu(r))
     assert np.linalg.norm(a - q @ r) / np.linalg.norm(a) < 5e-3
     assert orthogonality_f(q) < 5e-4      # FP16-GEMM level: the second pass cannot go below it
+
+
+def test_panel_nonfinite_data_does_not_stall(tq):
+    # the pipelined panel hands values over through a sentinel bit pattern; a NaN/Inf in the data
+    # must flow through (and be reported by the status), never be taken for "not yet written"
+    X = W.gaussian_cuda(32768, 32, 61)
+    X[1234, 7] = float("nan")
+    X[99, 20] = float("inf")
+    with pytest.raises(tq.TcqrError):
+        tq.panel_qr(X, br=1024)
+    # the next panel on clean data still works (sentinels were reset)
+    X2 = W.gaussian_cuda(32768, 32, 62)
+    Xq, R = tq.panel_qr(X2.clone(), br=1024)
+    q = Xq.double().cpu().numpy()
+    assert np.linalg.norm(q.T @ q - np.eye(32)) < 1e-4

@@ -273,3 +273,25 @@ def test_lls_warm_start(tq, kind, cond):
     assert x_rel_error(x2.cpu().numpy(), x_o) <= 1e-10
     if cond == 1:
         assert i2["iterations"] <= i1["iterations"], (i1, i2)
+
+
+# ---- streamed host entry (H2D / compute / D2H overlapped by column chunks) ----------------------
+def test_factor_host_streamed_bitwise_equals_device(tq):
+    # n > 2 * cutoff: tcqr_factor_host ships column chunks in and finished chunks out while the
+    # recursion runs; the kernels and their order are the device path's, so the factors match
+    # the device entry point bitwise.
+    tq.set_config()
+    a = W.gaussian(4096, 1024, seed=51)
+    q_h, r_h = tq.factor_host(a)
+    Q, R = tq.factor(tq.to_device_colmajor(a))
+    assert np.array_equal(q_h, Q.cpu().numpy()) and np.array_equal(r_h, R.cpu().numpy())
+    assert np.array_equal(np.tril(r_h, -1), np.zeros_like(r_h))
+
+
+def test_factor_host_streamed_nonfinite_column(tq):
+    tq.set_config()
+    a = W.gaussian(2048, 1024, seed=52)
+    a[17, 901] = np.inf  # a column in a late chunk: the status names the global column
+    with pytest.raises(tq.TcqrError) as e:
+        tq.factor_host(a)
+    assert e.value.code == 902
