@@ -144,6 +144,27 @@ def run_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def _streamed_r_bytes(n, cutoff):
+    """Bytes of R the streamed tcqr_factor_host copies back: for each column chunk (the subtrees
+    of width <= max(n/8, 2*cutoff), tcqr.cu plan_chunks) the rows [0, chunk end); the zero rows
+    below are written on the host."""
+    target = max(n // 8, 1)
+    chunks = []
+
+    def plan(c0, w):
+        if w <= target or w <= 2 * cutoff:
+            chunks.append((c0, c0 + w))
+            return
+        h = 32 * ((w + 63) // 64)
+        plan(c0, h)
+        plan(c0 + h, w - h)
+
+    if n <= 2 * cutoff:
+        return 4 * n * n
+    plan(0, n)
+    return sum(4 * b * (b - a) for a, b in chunks)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -313,8 +334,9 @@ def main():
         ems = float(te.item())
         e2e = {"value": conv_flops(M, n) / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": ems, "h2d_bytes_per_step": 4 * m * n,
-               "d2h_bytes_per_step": 4 * m * n + 4 * n * n,
-               "api": "tcqr_factor_host (pinned host A, Q, R)"}
+               "d2h_bytes_per_step": 4 * m * n + _streamed_r_bytes(n, args.cutoff),
+               "api": "tcqr_factor_host (pinned host A, Q, R): column chunks streamed in, "
+                      "finished chunks' Q and R columns streamed out during the factorization"}
         del a_host
 
     # ---- LLS time-to-FP64 accuracy (configs[3]: 32768x8192 geometric kappa=1e4) ----

@@ -483,8 +483,11 @@ static int chunk_done(FactorJob& J, int c0, int w) {
       CK(cudaStreamWaitEvent(c.s_d2h, sp->ev_fin[j], 0));
       CK(cudaMemcpyAsync(sp->hQ + (long long)c0 * J.m, J.Q + (long long)c0 * J.ldq,
                          sizeof(float) * (size_t)J.m * w, cudaMemcpyDeviceToHost, c.s_d2h));
-      CK(cudaMemcpyAsync(sp->hR + (long long)c0 * J.n, J.R + (long long)c0 * J.ldr,
-                         sizeof(float) * (size_t)J.n * w, cudaMemcpyDeviceToHost, c.s_d2h));
+      // R columns [c0, c0+w): rows [0, c0+w) hold the factor; the zero rows below are written on
+      // the host (factor_host_streamed) instead of crossing PCIe
+      CK(cudaMemcpy2DAsync(sp->hR + (long long)c0 * J.n, sizeof(float) * J.n,
+                           J.R + (long long)c0 * J.ldr, sizeof(float) * J.ldr,
+                           sizeof(float) * (size_t)(c0 + w), w, cudaMemcpyDeviceToHost, c.s_d2h));
     }
   return 0;
 }
@@ -506,27 +509,44 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     CKR(rgs(J, c0, h, tc || need_h));  // Alg. 2 line 7
     float* A2 = J.Q + (long long)(c0 + h) * J.ldq;
     float* Rblk = J.R + c0 + (long long)(c0 + h) * J.ldr;
-    need_cols(J, c0 + h, c0 + w);
     if (tc) {
-      // Alg. 2 line 8 on tensor cores: K1 cast of A2, K3 split-K TN, [allreduce], finalize.
+      // Alg. 2 line 8 on tensor cores: K1 cast of A2, K3 split-K TN, [allreduce], finalize;
+      // line 9 argument: K4.  Every output column depends only on its own A2 column, so the
+      // streamed host path runs them per arriving column chunk (pieces), the device path in one.
       __half* A1h = ws.Qh + (long long)c0 * ws.ldh;
-      __half* A2h = ws.Qh + (long long)(c0 + h) * ws.ldh;
-      PROF(TCQR_K1_CAST, 0, 6.0 * m * w2,
-           CK(cast_scale(m, w2, A2, J.ldq, A2h, ws.ldh, ws.inv_s + c0 + h, c.cfg.col_scaling,
-                         c.d_status, c0 + h, ws.cmax, c.stream)));
-      PROF(TCQR_K3_TN, 2.0 * m * h * w2, 2.0 * m * (h + w2) + 4.0 * h * w2,
-           CK(tc_gemm_tn(m, h, w2, A1h, ws.ldh, A2h, ws.ldh, ws.T, h, ws.inv_s + c0 + h, ws.P,
-                         ws.p_cap, c.num_sms, c.stream)));
-      CKR(allreduce_f32(ws.T, (size_t)h * w2));
       const long long ldh2 = round_up(h, 8);
-      PROF(TCQR_K3_FINALIZE, 0, 10.0 * h * w2,
-           CK(r12_finalize(h, w2, ws.T, h, Rblk, J.ldr, ws.R12h, ldh2, ws.inv_s2 + c0 + h,
-                           c.cfg.col_scaling, c.stream)));
-      // Alg. 2 line 9 argument on tensor cores: K4.
-      PROF(TCQR_K4_NN, 2.0 * m * h * w2, 2.0 * m * h + 2.0 * h * w2 + 8.0 * m * w2,
-           CK(tc_gemm_nn_update(m, h, w2, A1h, ws.ldh, ws.R12h, ldh2, A2, J.ldq,
-                                ws.inv_s2 + c0 + h, c.num_sms, c.stream)));
+      std::vector<std::pair<int, int>> pieces;
+      if (J.sp) {
+        for (size_t j = 0; j < J.sp->a.size(); ++j) {
+          const int p0 = std::max(J.sp->a[j], c0 + h), p1 = std::min(J.sp->b[j], c0 + w);
+          if (p0 < p1) pieces.push_back({p0, p1});
+        }
+      } else {
+        pieces.push_back({c0 + h, c0 + w});
+      }
+      for (auto& pc : pieces) {
+        const int p0 = pc.first, wp = pc.second - pc.first, off = p0 - (c0 + h);
+        need_cols(J, p0, p0 + wp);
+        float* A2p = J.Q + (long long)p0 * J.ldq;
+        __half* A2h = ws.Qh + (long long)p0 * ws.ldh;
+        float* Tp = ws.T + (long long)off * h;
+        __half* R12hp = ws.R12h + (long long)off * ldh2;
+        PROF(TCQR_K1_CAST, 0, 6.0 * m * wp,
+             CK(cast_scale(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling,
+                           c.d_status, p0, ws.cmax, c.stream)));
+        PROF(TCQR_K3_TN, 2.0 * m * h * wp, 2.0 * m * (h + wp) + 4.0 * h * wp,
+             CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, Tp, h, ws.inv_s + p0, ws.P,
+                           ws.p_cap, c.num_sms, c.stream)));
+        CKR(allreduce_f32(Tp, (size_t)h * wp));
+        PROF(TCQR_K3_FINALIZE, 0, 10.0 * h * wp,
+             CK(r12_finalize(h, wp, Tp, h, Rblk + (long long)off * J.ldr, J.ldr, R12hp, ldh2,
+                             ws.inv_s2 + p0, c.cfg.col_scaling, c.stream)));
+        PROF(TCQR_K4_NN, 2.0 * m * h * wp, 2.0 * m * h + 2.0 * h * wp + 8.0 * m * wp,
+             CK(tc_gemm_nn_update(m, h, wp, A1h, ws.ldh, R12hp, ldh2, A2p, J.ldq, ws.inv_s2 + p0,
+                                  c.num_sms, c.stream)));
+      }
     } else if (c.nranks == 1) {
+      need_cols(J, c0 + h, c0 + w);
       // one cooperative launch: R12 = Q1' A2 (deterministic), R block, A2 -= Q1 R12
       cudaError_t e = cudaErrorNotSupported;
       PROF(TCQR_K2B_TN, 4.0 * m * h * w2, 8.0 * m * h + 12.0 * m * w2,
@@ -544,6 +564,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
              CK(f32_nn_update(m, h, w2, Qc, J.ldq, ws.T, A2, J.ldq, c.stream)));
       }
     } else {
+      need_cols(J, c0 + h, c0 + w);
       PROF(TCQR_K2B_TN, 2.0 * m * h * w2, 4.0 * m * (h + w2),
            CK(f32_tn(m, h, w2, Qc, J.ldq, A2, J.ldq, ws.T, ws.P, ws.p_cap, c.num_sms,
                      c.stream)));
@@ -1027,6 +1048,10 @@ static int factor_host_streamed(int m, int n, const float* A, long long lda, flo
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   FactorJob J{m, n, dQ, (long long)m, dR, (long long)n, &ws, &sp};
   rc = rgs(J, 0, n, n > c.cfg.cutoff);
+  // while the device works: the strictly-lower zero rows of each chunk's R columns, on the host
+  for (size_t j = 0; j < nc; ++j)
+    for (int col = sp.a[j]; col < sp.b[j]; ++col)
+      memset(R + (long long)col * n + sp.b[j], 0, sizeof(float) * (size_t)(n - sp.b[j]));
   if (rc == 0) {
     need_cols(J, 0, n);  // every validation has finished before the status is read
     CK(zero_lower(n, dR, n, c.stream));
