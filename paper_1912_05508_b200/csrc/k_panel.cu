@@ -750,6 +750,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
     // (coalesced, one 128-byte row per load instruction, polled until no NaN is left) into
     // shared memory [block][129] (row r at r*32 + column).
     float* st0 = fsm;
+    float* Rsm = fsm + 32 * 129;  // the panel's R, column-major 32 x 32 (R(k,j) at k + 32 j)
     {
       float v[16];
 #pragma unroll
@@ -863,12 +864,18 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
           }
         }
         const int cnt = 32 * min(nwa, (k + 1) / 4 + 1);  // warps joined at step k
-        mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, 32 * w, a.Rout, 1, a.ldr,
+        mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, 32 * w, Rsm, 1, 32,
                               a.root_is_global != 0, a.status, a.col0, red, buf, k < i0, cnt);
         if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(&s_step) = k;  // barrier k passed
       }
     }
     __syncthreads();
+    // the panel's R (built in shared memory: the per-step row stores would be 32 scattered
+    // global stores each) -> Rout, column by column
+    for (int e = threadIdx.x; e < w * w; e += NT) {
+      const int i = e % w, j = e / w;
+      a.Rout[i + (long long)j * a.ldr] = Rsm[i + 32 * j];
+    }
     // every stack row has been consumed: reset the slots to NaN for the next panel in bulk (off
     // the per-step critical path; the children are still applying the last columns)
     const long long tot = (long long)srows * w;
