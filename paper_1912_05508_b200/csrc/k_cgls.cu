@@ -237,6 +237,118 @@ __global__ void __launch_bounds__(256, 1) trinv_pair_gemm_big(int n, int b,
     }
 }
 
+// FP64 tensor-core pair GEMM (b >= 128): the same 128 x 128 tiles, K-ranges and loaders as
+// trinv_pair_gemm_big, with the products on DMMA (mma.sync m8n8k4 f64): 8 warps as 4 (M) x 2
+// (N), warp tile 32 x 64 = 4 x 8 m8n8 tiles.  Shared rows padded to 136 doubles, so a fragment
+// load (4 k-rows x 8 consecutive m) takes the two wavefronts its 256 bytes need.
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) trinv_pair_dmma(int n, int b, const float* __restrict__ R,
+                                                          long long ldr, double* __restrict__ M,
+                                                          long long ldm, double* __restrict__ W) {
+  constexpr int TB = 128, KB = 8, NLD = KB * TB / 256, SP = 136;
+  __shared__ __align__(16) double As[2][KB][SP];
+  __shared__ __align__(16) double Bs[2][KB][SP];
+  const int p = blockIdx.z;
+  const int i0 = p * 2 * b;
+  const int b1 = b;
+  const int b2 = min(b, n - (i0 + b));
+  if (b2 <= 0) return;
+  const int tm = blockIdx.x * TB, tn = blockIdx.y * TB;
+  if (tm >= b1 || tn >= b2) return;
+  double* Wp = W + (long long)p * b * b;  // ld = b
+  const int K = (MODE == 0) ? b2 : b1;
+  const int kbeg = (MODE == 0) ? 0 : tm;
+  const int kend = (MODE == 0) ? min(K, tn + TB) : K;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 64;
+  auto loadA = [&](int k0, double (&ra)[NLD]) {
+#pragma unroll
+    for (int u = 0; u < NLD; ++u) {
+      const int e = tid + u * 256, kk = e >> 7, mm = e & 127;
+      const int r = tm + mm, k = k0 + kk;
+      double v = 0.0;
+      if (r < b1 && k < kend) {
+        if (MODE == 0)
+          v = (double)__ldg(R + (i0 + r) + (long long)(i0 + b1 + k) * ldr);
+        else
+          v = M[(i0 + r) + (long long)(i0 + k) * ldm];
+      }
+      ra[u] = v;
+    }
+  };
+  auto loadB = [&](int k0, double (&rb)[NLD]) {
+#pragma unroll
+    for (int u = 0; u < NLD; ++u) {
+      const int e = tid + u * 256, kk = e >> 7, mm = e & 127;
+      const int c = tn + mm, k = k0 + kk;
+      double v = 0.0;
+      if (c < b2 && k < kend) {
+        if (MODE == 0)
+          v = M[(i0 + b1 + k) + (long long)(i0 + b1 + c) * ldm];
+        else
+          v = Wp[k + (long long)c * b];
+      }
+      rb[u] = v;
+    }
+  };
+  double acc[4][8][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double ra[NLD], rb[NLD];
+  int buf = 0;
+  loadA(kbeg, ra);
+  loadB(kbeg, rb);
+  const int fk = lane & 3, fr = lane >> 2;  // fragment k index, row/col within an 8-block
+  for (int k0 = kbeg; k0 < kend; k0 += KB) {
+#pragma unroll
+    for (int u = 0; u < NLD; ++u) {
+      const int e = tid + u * 256, kk = e >> 7, mm = e & 127;
+      As[buf][kk][mm] = ra[u];
+      Bs[buf][kk][mm] = rb[u];
+    }
+    __syncthreads();
+    if (k0 + KB < kend) {
+      loadA(k0 + KB, ra);
+      loadB(k0 + KB, rb);
+    }
+#pragma unroll
+    for (int k4 = 0; k4 < KB; k4 += 4) {
+      double af[4], bf[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][k4 + fk][wm + 8 * i + fr];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bf[j] = Bs[buf][k4 + fk][wn + 8 * j + fr];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma_m8n8k4(acc[i][j], af[i], bf[j]);
+    }
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = tm + wm + 8 * i + fr, c = tn + wn + 8 * j + 2 * fk + h;
+        if (r < b1 && c < b2) {
+          if (MODE == 0)
+            Wp[r + (long long)c * b] = acc[i][j][h];
+          else
+            M[(i0 + r) + (long long)(i0 + b1 + c) * ldm] = -acc[i][j][h];
+        }
+      }
+}
+
 cudaError_t trinv_f64(int n, const float* R, long long ldr, double* M, long long ldm, double* W,
                       int num_sms, cudaStream_t st) {
   (void)num_sms;
@@ -249,8 +361,8 @@ cudaError_t trinv_f64(int n, const float* R, long long ldr, double* M, long long
     const int pairs = (n + 2 * b - 1) / (2 * b);
     if (b >= 128) {
       dim3 grid((b + 127) / 128, (b + 127) / 128, pairs);
-      trinv_pair_gemm_big<0><<<grid, 256, 0, st>>>(n, b, R, ldr, M, ldm, W);
-      trinv_pair_gemm_big<1><<<grid, 256, 0, st>>>(n, b, R, ldr, M, ldm, W);
+      trinv_pair_dmma<0><<<grid, 256, 0, st>>>(n, b, R, ldr, M, ldm, W);
+      trinv_pair_dmma<1><<<grid, 256, 0, st>>>(n, b, R, ldr, M, ldm, W);
     } else {
       dim3 grid((b + 63) / 64, (b + 63) / 64, pairs);
       trinv_pair_gemm_kernel<<<grid, 256, 0, st>>>(n, b, 0, R, ldr, M, ldm, W);
