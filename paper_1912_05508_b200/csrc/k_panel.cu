@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) panel_apply_kernel(int rows, int w, float
                                                           long long ldx, int br, int nb,
                                                           const float* __restrict__ S,
                                                           long long lds) {
-  __shared__ float T[32][33];
+  __shared__ __align__(16) float T[32][36];  // 16-byte rows: one LDS.128 per four FMAs
   const int i = blockIdx.x * 256 + threadIdx.x;
   // block index of the first row of this CTA (CTAs never straddle: chunks are 256 rows and br is
   // a multiple of 32 but not necessarily of 256 -> compute per row below, T loaded per block).
@@ -55,9 +55,9 @@ __global__ void __launch_bounds__(256) panel_apply_kernel(int rows, int w, float
   for (int j = 0; j < 32; ++j) y[j] = 0.f;
   for (int b = b_first; b <= b_last; ++b) {
     __syncthreads();
-    for (int e = threadIdx.x; e < w * w; e += 256) {
-      const int l = e % w, j = e / w;
-      T[l][j] = S[(long long)(b * w + l) + (long long)j * lds];
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      const int l = e & 31, j = e >> 5;
+      T[l][j] = (l < w && j < w) ? S[(long long)(b * w + l) + (long long)j * lds] : 0.f;
     }
     __syncthreads();
     if (ok && bi == b) {
@@ -65,9 +65,15 @@ __global__ void __launch_bounds__(256) panel_apply_kernel(int rows, int w, float
       for (int l = 0; l < 32; ++l) {
         if (l < w) {
           const float xl = x[l];
+          const float4* t4 = reinterpret_cast<const float4*>(&T[l][0]);
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < w) y[j] = fmaf(xl, T[l][j], y[j]);
+          for (int q = 0; q < 8; ++q) {
+            const float4 t = t4[q];
+            y[4 * q] = fmaf(xl, t.x, y[4 * q]);
+            y[4 * q + 1] = fmaf(xl, t.y, y[4 * q + 1]);
+            y[4 * q + 2] = fmaf(xl, t.z, y[4 * q + 2]);
+            y[4 * q + 3] = fmaf(xl, t.w, y[4 * q + 3]);
+          }
         }
       }
     }

@@ -383,7 +383,17 @@ static int caqr_rec(FactorWs& ws, long long& stack_off, int rows, int w, float* 
   PROF(TCQR_K2_MGS, 2.0 * rows * w * w, 8.0 * rows * w,
        CK(panel_mgs_level(rows, w, X, ldx, br, nb, S, lds, nullptr, 0, 0, c.d_status, col0,
                           c.stream)));
-  CKR(caqr_rec(ws, stack_off, nb * w, w, S, lds, Rout, ldr, top, col0));
+  // the stacked R's (nb*w rows) are factored by the pipelined panel when they fit it (Eq. (6)
+  // holds for any blocking of the stack), else by the next level of this recursion
+  cudaError_t e = cudaErrorNotSupported;
+  PROF(TCQR_K2_MGS, 4.0 * nb * w * w * w, 10.0 * nb * w * w,
+       e = panel_pipe(nb * w, w, S, lds, nullptr, 0, 1024, Rout, ldr, top ? 1 : 0, c.d_status,
+                      col0, ws.pipeR, ws.pipeS, c.num_sms, c.stream));
+  if (e != cudaSuccess) {
+    if (e != cudaErrorNotSupported) CK(e);
+    cudaGetLastError();
+    CKR(caqr_rec(ws, stack_off, nb * w, w, S, lds, Rout, ldr, top, col0));
+  }
   PROF(TCQR_K2_APPLY, 2.0 * rows * w * w, 8.0 * rows * w,
        CK(panel_apply(rows, w, X, ldx, br, nb, S, lds, c.stream)));
   return 0;
