@@ -34,6 +34,8 @@ WORKLOADS = {
                  name="QR of 262144x2048 Gaussian (BASELINE configs[4])"),
     "cfg1": dict(m=1024, n=128, kind="gaussian", seed=1,
                  name="QR of 1024x128 Gaussian (BASELINE configs[0])"),
+    "next3": dict(m=4194304, n=128, kind="gaussian", seed=9,
+                  name="orthogonalization of 4194304x128 Gaussian (NEXT-3, PAPER.md:598)"),
 }
 
 
@@ -243,14 +245,19 @@ def main():
     if rank == 0 and world == 1:
         from oracle.qr import rgs
         from oracle.metrics import r_rel_error
-        k = 256
-        a_lead = A[:, :k].cpu().numpy().astype(np.float64)
-        _, r_o = rgs(a_lead)
-        r_lead = R[:k, :k].cpu().numpy().astype(np.float64)
-        q_lead = Q[:, :k].cpu().numpy().astype(np.float64)
-        parity = {"R_lead256_rel_err_vs_oracle": r_rel_error(r_lead, r_o),
-                  "Q_lead256_orthogonality_f": float(np.linalg.norm(q_lead.T @ q_lead - np.eye(k))
-                                                     / np.sqrt(k))}
+        k = min(256, n)
+        if M <= 262144:
+            a_lead = A[:, :k].cpu().numpy().astype(np.float64)
+            _, r_o = rgs(a_lead)
+            r_lead = R[:k, :k].cpu().numpy().astype(np.float64)
+            q_lead = Q[:, :k].cpu().numpy().astype(np.float64)
+            parity = {f"R_lead{k}_rel_err_vs_oracle": r_rel_error(r_lead, r_o),
+                      f"Q_lead{k}_orthogonality_f": float(
+                          np.linalg.norm(q_lead.T @ q_lead - np.eye(k)) / np.sqrt(k))}
+        else:
+            # the FP64 CPU oracle on all rows of a 4M-row block takes minutes: device invariants
+            # only (tests/test_gpu_fullsize.py pins the oracle comparison at smaller row counts)
+            parity = {"oracle": "skipped at this row count; device FP64 invariants below"}
         # full-size invariants on the device in FP64 (harness arithmetic, not the method)
         Rd = R.to(torch.float64)
         res = 0.0

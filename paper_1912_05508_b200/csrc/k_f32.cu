@@ -287,9 +287,10 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
 #pragma unroll
       for (int c = 0; c < MT; ++c) acc[a][c] = 0.f;
     constexpr int NL = kTnRows * TD / 256;  // loads per thread per matrix per chunk
-    for (long long c0 = r0; c0 < r1; c0 += kTnRows) {
-      __syncthreads();
-      float qv_[NL], av_[NL];
+    // the next chunk's loads are issued before the current chunk's products (register double
+    // buffering): one HBM round trip per chunk overlaps the compute instead of following it
+    float qv_[NL], av_[NL];
+    auto load_chunk = [&](long long c0) {
 #pragma unroll
       for (int u = 0; u < NL; ++u) {
         const int e = tid + u * 256;
@@ -299,6 +300,10 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
         qv_[u] = (rok && cc < h) ? __ldg(Q1 + row + cc * ldq) : 0.f;
         av_[u] = (rok && cc < w2) ? A2[row + cc * lda] : 0.f;
       }
+    };
+    if (r0 < r1) load_chunk(r0);
+    for (long long c0 = r0; c0 < r1; c0 += kTnRows) {
+      __syncthreads();
 #pragma unroll
       for (int u = 0; u < NL; ++u) {
         const int e = tid + u * 256;
@@ -307,6 +312,7 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
         As[rr][cc] = av_[u];
       }
       __syncthreads();
+      if (c0 + kTnRows < r1) load_chunk(c0 + kTnRows);
 #pragma unroll 4
       for (int rr = grp; rr < kTnRows; rr += 4) {
         float qv[MT], av[MT];
@@ -373,6 +379,10 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
     }
     __syncthreads();
     for (long long row = r0 + tid; row < r1; row += 256) {
+      // the whole Q1 row first (h <= TD loads in flight), then each 32-column half of A2
+      float qrow[TD];
+#pragma unroll
+      for (int i = 0; i < TD; ++i) qrow[i] = (i < h) ? __ldg(Q1 + row + (long long)i * ldq) : 0.f;
 #pragma unroll 1
       for (int jh = 0; jh < TD; jh += 32) {  // 32-column halves keep registers bounded
         float cold[32];
@@ -381,19 +391,16 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
         float acc[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-        for (int i0 = 0; i0 < h; i0 += 8) {
-          float qb[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) qb[u] = (i0 + u < h) ? __ldg(Q1 + row + (long long)(i0 + u) * ldq) : 0.f;
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
+        for (int i = 0; i < TD; ++i) {
+          if (i < h) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
-              const float4 tv = *reinterpret_cast<const float4*>(&Ts[(i0 + u) * TD + jh + j]);
-              acc[j] = fmaf(qb[u], tv.x, acc[j]);
-              acc[j + 1] = fmaf(qb[u], tv.y, acc[j + 1]);
-              acc[j + 2] = fmaf(qb[u], tv.z, acc[j + 2]);
-              acc[j + 3] = fmaf(qb[u], tv.w, acc[j + 3]);
+              const float4 tv = *reinterpret_cast<const float4*>(&Ts[i * TD + jh + j]);
+              acc[j] = fmaf(qrow[i], tv.x, acc[j]);
+              acc[j + 1] = fmaf(qrow[i], tv.y, acc[j + 1]);
+              acc[j + 2] = fmaf(qrow[i], tv.z, acc[j + 2]);
+              acc[j + 3] = fmaf(qrow[i], tv.w, acc[j + 3]);
             }
           }
         }

@@ -127,3 +127,15 @@ def test_config4_kappa1e6_reports_honestly(tq):
     assert bool(torch.all(torch.isfinite(x)))
     if info["converged"] == 1:
         assert err <= 1e-6, (err, info)
+
+
+def test_next3_extreme_tall_skinny(tq):
+    # NEXT-3: 4194304 x 128 orthogonalization.  n equals the cutoff, so the whole
+    # factorization is the FP32 leaf (panels + FP32 projections, multi-level CAQR whose stack is
+    # factored by the pipelined panel): FP32-level backward error and orthogonality.
+    A = W.gaussian_cuda(4194304, 128, 9)
+    Q, R = tq.factor(A)
+    torch.cuda.synchronize()
+    be, orth = _device_metrics(A, Q, R)
+    assert be <= 1e-5 and orth <= 1e-5, (be, orth)
+    assert bool(torch.all(torch.diagonal(R) > 0))
