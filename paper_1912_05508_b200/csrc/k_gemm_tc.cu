@@ -18,7 +18,7 @@
 
 namespace tcqr {
 
-template <int BN, int MODE, bool TMAC = false>
+template <int BN, int MODE, int NBUF = 0>
 struct TcCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
@@ -26,19 +26,23 @@ struct TcCfg {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // NN keeps four 128 x 32 FP32 C chunks (16 KB each) for the TMA epilogue; its K = h is short,
   // so fewer mainloop stages suffice
-  static constexpr int CBUF = TMAC ? 4 * 16384 : 0;
-  static constexpr int ST = TMAC ? ((BN == 128) ? 4 : 3) : ((BN == 128) ? 6 : 4);
+  // NBUF = 0: direct-load epilogue; 2 / 4: TMA epilogue with that many 16 KB C-chunk buffers (4
+  // buffers prefetch three chunks ahead for short-K updates at the cost of one mainloop stage; 2
+  // keep the full mainloop depth for long K, where the epilogue hides behind the next tile)
+  static constexpr int CBUF = NBUF * 16384;
+  static constexpr int ST = (NBUF == 4) ? ((BN == 128) ? 4 : 3) : ((BN == 128) ? 6 : 4);
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static constexpr int SMEM = ST * STAGE + CBUF + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int BN, int MODE, bool TMAC>
+template <int BN, int MODE, int NBUF>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int splits,
                    float* __restrict__ C, long long ldc, long long split_stride,
                    const float* __restrict__ col_mult) {
-  using Cfg = TcCfg<BN, MODE, TMAC>;
+  using Cfg = TcCfg<BN, MODE, NBUF>;
+  constexpr bool TMAC = NBUF > 0;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, ST = Cfg::ST, STAGE = Cfg::STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(192, 1)
       const int ncol = min(BN, N - nb * BN), nch = (ncol + 31) / 32;
       if (issuer) {
         bulk_wait_read<0>();  // the previous tile's stores have read their buffers
-        for (int c = 0; c < 3 && c < nch; ++c) {
+        for (int c = 0; c < NBUF - 1 && c < nch; ++c) {
           mbar_arrive_expect_tx(&cfull[c], 16384);
           tma_load_2d(cbuf + c * 4096, &tmC, &cfull[c], mb * BM, nb * BN + 32 * c);
         }
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c = 0; c < nch; ++c) {
-        const int buf = c & 3;
+        const int buf = c % (NBUF > 0 ? NBUF : 1);
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + 32 * c, r);
         mbar_wait(&cfull[buf], (cph >> buf) & 1);
@@ -187,11 +191,13 @@ __global__ void __launch_bounds__(192, 1)
         if (issuer) {
           tma_store_2d(&tmC, cb, mb * BM, col0);
           bulk_commit();
-          if (c + 3 < nch) {
-            const int nbuf = (c + 3) & 3;  // last used by chunk c-1, whose store must have read it
+          if (c + NBUF - 1 < nch) {
+            // buffer of chunk c+NBUF-1 was last used by chunk c-1, whose store must have read it
+            const int nbuf = (c + NBUF - 1) % NBUF;
             bulk_wait_read<1>();
             mbar_arrive_expect_tx(&cfull[nbuf], 16384);
-            tma_load_2d(cbuf + nbuf * 4096, &tmC, &cfull[nbuf], mb * BM, nb * BN + 32 * (c + 3));
+            tma_load_2d(cbuf + nbuf * 4096, &tmC, &cfull[nbuf], mb * BM,
+                        nb * BN + 32 * (c + NBUF - 1));
           }
         }
       }
@@ -369,21 +375,21 @@ static bool make_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uin
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int MODE, bool TMAC = false>
+template <int BN, int MODE, int NBUF = 0>
 static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
                              int M, int N, int K, int splits, float* C, long long ldc,
                              long long sstride, const float* mult, int num_sms, cudaStream_t st) {
-  using Cfg = TcCfg<BN, MODE, TMAC>;
+  using Cfg = TcCfg<BN, MODE, NBUF>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE, TMAC>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE, NBUF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int tiles = ((M + 127) / 128) * ((N + BN - 1) / BN) * splits;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  tc_gemm_kernel<BN, MODE, TMAC><<<grid, 192, Cfg::SMEM, st>>>(a, b, cm, M, N, K, splits, C, ldc,
+  tc_gemm_kernel<BN, MODE, NBUF><<<grid, 192, Cfg::SMEM, st>>>(a, b, cm, M, N, K, splits, C, ldc,
                                                                sstride, mult);
   return cudaGetLastError();
 }
@@ -440,17 +446,17 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
   const int BN = (w2 > 128) ? 256 : 128;
   if (!make_map_f16(&ma, Qh, m, h, ldq, 64, 64)) return cudaErrorInvalidValue;
   if (!make_map_f16(&mb, Bh, h, w2, ldb, 64, BN)) return cudaErrorInvalidValue;
-  // TMA epilogue (C chunks through shared memory) when the update is epilogue-bound (short K = h)
-  // and C's columns are 16-byte aligned; the direct-load epilogue with deeper mainloop pipelining
-  // otherwise
+  // TMA epilogue (C chunks through shared memory, four buffers) for short K = h, where the
+  // update is epilogue-bound, when C's columns are 16-byte aligned; the direct-load epilogue with
+  // the deeper mainloop for long K (measured: the 2-buffer TMA variant is 6% slower at h = 8192)
   CUtensorMap mc;
-  const bool tmac = h <= 2048 && (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0) &&
+  const bool tmac = (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0) &&
                     make_map_f32(&mc, C, m, w2, ldc, 128, 32);
-  if (tmac)
-    return (BN == 256) ? launch_tc<256, kModeNN, true>(ma, mb, mc, m, w2, h, 1, C, ldc, 0, col_mult,
-                                                       num_sms, st)
-                       : launch_tc<128, kModeNN, true>(ma, mb, mc, m, w2, h, 1, C, ldc, 0, col_mult,
-                                                       num_sms, st);
+  if (tmac && h <= 2048)
+    return (BN == 256) ? launch_tc<256, kModeNN, 4>(ma, mb, mc, m, w2, h, 1, C, ldc, 0, col_mult,
+                                                    num_sms, st)
+                       : launch_tc<128, kModeNN, 4>(ma, mb, mc, m, w2, h, 1, C, ldc, 0, col_mult,
+                                                    num_sms, st);
   return (BN == 256) ? launch_tc<256, kModeNN>(ma, mb, ma, m, w2, h, 1, C, ldc, 0, col_mult, num_sms,
                                                st)
                      : launch_tc<128, kModeNN>(ma, mb, ma, m, w2, h, 1, C, ldc, 0, col_mult, num_sms,
