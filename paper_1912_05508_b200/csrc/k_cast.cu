@@ -181,6 +181,56 @@ __global__ void __launch_bounds__(kCastThreads) r12_finalize_kernel(
   }
 }
 
+// Split-K reduction fused with the finalize: column j of R12 = (sum_s P[s](:, j)) * col_mult[j]
+// (partials summed in the fixed order s = 0..splits-1), written to the R block, then the column
+// scale s' and the scaled FP16 copy as in r12_finalize_kernel.
+__global__ void __launch_bounds__(kCastThreads) r12_splitk_finalize_kernel(
+    int h, const float* __restrict__ P, int splits, long long pstride, long long ldp,
+    const float* __restrict__ col_mult, float* __restrict__ Rblk, long long ldr,
+    __half* __restrict__ R12h, long long ldh2, float* __restrict__ inv_s2, int scaling) {
+  __shared__ float red[32];
+  const int j = blockIdx.x;
+  const float cm = col_mult ? col_mult[j] : 1.f;
+  float* r = Rblk + (long long)j * ldr;
+  float mx = 0.f;
+  for (int i = threadIdx.x; i < h; i += kCastThreads) {
+    const float* p = P + i + (long long)j * ldp;
+    float acc = 0.f;
+    int s0 = 0;
+    for (; s0 + 8 <= splits; s0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (long long)(s0 + u) * pstride);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; s0 < splits; ++s0) acc += __ldcg(p + (long long)s0 * pstride);
+    const float v = acc * cm;
+    r[i] = v;
+    mx = fmaxf(mx, fabsf(v));
+  }
+  float sc = 1.f;
+  if (scaling) {
+    mx = block_max(mx, red);
+    sc = pow2_scale_for(mx);
+  }
+  if (threadIdx.x == 0) inv_s2[j] = 1.f / sc;
+  if (R12h) {
+    __half* o = R12h + (long long)j * ldh2;
+    for (int i = threadIdx.x; i < h; i += kCastThreads) o[i] = __float2half_rn(r[i] * sc);
+  }
+}
+
+cudaError_t r12_splitk_finalize(int h, int w2, const float* P, int splits, long long pstride,
+                                long long ldp, const float* col_mult, float* Rblk, long long ldr,
+                                __half* R12h, long long ldh2, float* inv_s2, int scaling,
+                                cudaStream_t st) {
+  if (h <= 0 || w2 <= 0) return cudaSuccess;
+  r12_splitk_finalize_kernel<<<w2, kCastThreads, 0, st>>>(h, P, splits, pstride, ldp, col_mult,
+                                                          Rblk, ldr, R12h, ldh2, inv_s2, scaling);
+  return cudaGetLastError();
+}
+
 cudaError_t r12_finalize(int h, int w2, const float* T, long long ldt, float* Rblk, long long ldr,
                          __half* R12h, long long ldh2, float* inv_s2, int scaling,
                          cudaStream_t st) {

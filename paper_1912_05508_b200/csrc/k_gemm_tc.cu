@@ -398,7 +398,7 @@ static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const C
 // partials P (splits > 1; P has room for splits * ldp * w2 floats) followed by the reduction.
 cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, const __half* A2h,
                        long long lda2, float* C, long long ldc, const float* col_mult, float* P,
-                       long long p_cap, int num_sms, cudaStream_t st) {
+                       long long p_cap, int num_sms, cudaStream_t st, const R12Finalize* fin) {
   if (m <= 0 || h <= 0 || w2 <= 0) return cudaSuccess;
   CUtensorMap ma, mb;
   const int BN = (w2 > 128) ? 256 : 128;
@@ -422,7 +422,9 @@ cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, 
     e = (BN == 256)
             ? launch_tc<256, kModeTN>(ma, mb, ma, h, w2, m, 1, C, ldc, 0, col_mult, num_sms, st)
             : launch_tc<128, kModeTN>(ma, mb, ma, h, w2, m, 1, C, ldc, 0, col_mult, num_sms, st);
-    return e;
+    if (e != cudaSuccess || !fin) return e;
+    return r12_finalize(h, w2, C, ldc, fin->Rblk, fin->ldr, fin->R12h, fin->ldh2, fin->inv_s2,
+                        fin->scaling, st);
   }
   const long long sstride = (long long)h * w2;
   e = (BN == 256) ? launch_tc<256, kModeTN>(ma, mb, ma, h, w2, m, splits, P, h, sstride,
@@ -430,6 +432,9 @@ cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, 
                   : launch_tc<128, kModeTN>(ma, mb, ma, h, w2, m, splits, P, h, sstride,
                                             nullptr, num_sms, st);
   if (e != cudaSuccess) return e;
+  if (fin)
+    return r12_splitk_finalize(h, w2, P, splits, sstride, h, col_mult, fin->Rblk, fin->ldr,
+                               fin->R12h, fin->ldh2, fin->inv_s2, fin->scaling, st);
   const long long total = (long long)h * w2;
   int grid = (int)((total + 31) / 32);
   if (grid > 8 * num_sms) grid = 8 * num_sms;

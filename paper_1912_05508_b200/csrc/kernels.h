@@ -10,9 +10,24 @@ constexpr int kModeTN = 0;
 constexpr int kModeNN = 1;
 
 // ---- K3 / K4 (k_gemm_tc.cu) ----
+// Alg. 2 line 8 finalize targets (R block, scaled FP16 copy, column scales): when given to
+// tc_gemm_tn, the split-K reduction is fused with the finalize (no separate C pass).
+struct R12Finalize {
+  float* Rblk;
+  long long ldr;
+  __half* R12h;
+  long long ldh2;
+  float* inv_s2;
+  int scaling;
+};
 cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, const __half* A2h,
                        long long lda2, float* C, long long ldc, const float* col_mult, float* P,
-                       long long p_cap, int num_sms, cudaStream_t st);
+                       long long p_cap, int num_sms, cudaStream_t st,
+                       const R12Finalize* fin = nullptr);
+cudaError_t r12_splitk_finalize(int h, int w2, const float* P, int splits, long long pstride,
+                                long long ldp, const float* col_mult, float* Rblk, long long ldr,
+                                __half* R12h, long long ldh2, float* inv_s2, int scaling,
+                                cudaStream_t st);
 cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long ldq,
                               const __half* Bh, long long ldb, float* C, long long ldc,
                               const float* col_mult, int num_sms, cudaStream_t st);

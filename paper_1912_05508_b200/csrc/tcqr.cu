@@ -544,13 +544,22 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
         PROF(TCQR_K1_CAST, 0, 6.0 * m * wp,
              CK(cast_scale(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling,
                            c.d_status, p0, ws.cmax, c.stream)));
-        PROF(TCQR_K3_TN, 2.0 * m * h * wp, 2.0 * m * (h + wp) + 4.0 * h * wp,
-             CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, Tp, h, ws.inv_s + p0, ws.P,
-                           ws.p_cap, c.num_sms, c.stream)));
-        CKR(allreduce_f32(Tp, (size_t)h * wp));
-        PROF(TCQR_K3_FINALIZE, 0, 10.0 * h * wp,
-             CK(r12_finalize(h, wp, Tp, h, Rblk + (long long)off * J.ldr, J.ldr, R12hp, ldh2,
-                             ws.inv_s2 + p0, c.cfg.col_scaling, c.stream)));
+        if (c.nranks == 1) {
+          // one rank: the split-K reduction runs fused with the finalize
+          const R12Finalize fin{Rblk + (long long)off * J.ldr, J.ldr, R12hp, ldh2, ws.inv_s2 + p0,
+                                c.cfg.col_scaling};
+          PROF(TCQR_K3_TN, 2.0 * m * h * wp, 2.0 * m * (h + wp) + 14.0 * h * wp,
+               CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, Tp, h, ws.inv_s + p0, ws.P,
+                             ws.p_cap, c.num_sms, c.stream, &fin)));
+        } else {
+          PROF(TCQR_K3_TN, 2.0 * m * h * wp, 2.0 * m * (h + wp) + 4.0 * h * wp,
+               CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, Tp, h, ws.inv_s + p0, ws.P,
+                             ws.p_cap, c.num_sms, c.stream)));
+          CKR(allreduce_f32(Tp, (size_t)h * wp));
+          PROF(TCQR_K3_FINALIZE, 0, 10.0 * h * wp,
+               CK(r12_finalize(h, wp, Tp, h, Rblk + (long long)off * J.ldr, J.ldr, R12hp, ldh2,
+                               ws.inv_s2 + p0, c.cfg.col_scaling, c.stream)));
+        }
         PROF(TCQR_K4_NN, 2.0 * m * h * wp, 2.0 * m * h + 2.0 * h * wp + 8.0 * m * wp,
              CK(tc_gemm_nn_update(m, h, wp, A1h, ws.ldh, R12hp, ldh2, A2p, J.ldq, ws.inv_s2 + p0,
                                   c.num_sms, c.stream)));
