@@ -13,6 +13,9 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (128 x BN x 16 per instruction)
 //   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> coalesced column-major stores
 // Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap the MMAs of tile i+1.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -282,6 +285,218 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// K3 on CTA pairs (cta_group::2): a cluster of two CTAs on one TPC computes a 256 x 256 tile of
+// R12 = A' B.  Each CTA stages its own 128 rows of A (M = h) and its own 128 columns of B
+// (N = w2) per K-block, both CTAs' TMA loads complete on the leader's full barrier, and the
+// leader issues one 256 x 256 x 16 tcgen05.mma per K step that reads both CTAs' shared
+// operands (halving the shared-memory operand traffic per SM of the 1-CTA 128 x 256 tile).  Each
+// CTA's TMEM holds its 128 accumulator rows; the commits multicast to both CTAs' barriers.
+// Deterministic split-K exactly as the 1-CTA kernel (own partial per split, fixed-order sum).
+// ------------------------------------------------------------------------------------------
+struct Tc2Cfg {
+  static constexpr int BM = 128, BN = 256, BK = 64;  // per CTA: 128 A rows, 128 B columns
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;    // 32 KB
+  static constexpr int ST = 6;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;      // two 256-column accumulators
+  static constexpr int SMEM = ST * STAGE + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the leader CTA's copy of a shared-memory object (shared::cluster address, rank bit cleared)
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  return smem_u32(p) & 0xFEFFFFFFu;
+}
+
+__global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
+    tc_gemm2_tn_kernel(const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmB, int M, int N, int K, int splits,
+                       float* __restrict__ C, long long ldc, long long split_stride,
+                       const float* __restrict__ col_mult) {
+  using Cfg = Tc2Cfg;
+  constexpr int BK = Cfg::BK, ST = Cfg::ST, STAGE = Cfg::STAGE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * STAGE);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int tiles_m = (M + 255) / 256, tiles_n = (N + 255) / 256;
+  const int nkb = (K + BK - 1) / BK;
+  const int total = tiles_m * tiles_n * splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);  // four epilogue warps in each CTA of the pair
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(Cfg::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers of both CTAs initialized, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = pair; w < total; w += npairs) {
+        const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n, s = w / (tiles_m * tiles_n);
+        const int kb0 = (int)((long long)s * nkb / splits), kb1 = (int)((long long)(s + 1) * nkb / splits);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);  // both CTAs' bytes
+          uint8_t* sa = smem + stage * STAGE;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          const uint32_t bar = leader_addr(&full[stage]);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sa)),
+              "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(bar), "r"(kb * BK),
+              "r"(mb * 256 + (int)rank * 128)
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sb)),
+              "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(bar), "r"(kb * BK),
+              "r"(nb * 256 + (int)rank * 128)
+              : "memory");
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only) ----------------
+      constexpr uint32_t idesc = make_idesc_f16(256, 256, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int w = pair; w < total; w += npairs, ++it) {
+        const int s = w / (tiles_m * tiles_n);
+        const int kb0 = (int)((long long)s * nkb / splits), kb1 = (int)((long long)(s + 1) * nkb / splits);
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tacc = tmem_base + acc * Cfg::BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t base_a = smem_u32(smem + stage * STAGE);
+          const uint32_t base_b = base_a + Cfg::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t da = make_sw128_desc(base_a + kk * 32, 16, 1024);
+            const uint64_t db = make_sw128_desc(base_b + kk * 32, 16, 1024);
+            const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n"
+                ".reg .pred p;\n"
+                "setp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+                "}\n" ::"r"(tacc),
+                "l"(da), "l"(db), "r"(idesc), "r"(accum)
+                : "memory");
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+              " [%0], %1;" ::"r"(smem_u32(&empty[stage])),
+              "h"((unsigned short)3)
+              : "memory");
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+            " [%0], %1;" ::"r"(smem_u32(&tfull[acc])),
+            "h"((unsigned short)3)
+            : "memory");
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5 (both CTAs): own 128 rows ----------------
+    const int q = warp & 3;
+    int it = 0;
+    for (int w = pair; w < total; w += npairs, ++it) {
+      const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n, s = w / (tiles_m * tiles_n);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int row = mb * 256 + (int)rank * 128 + q * 32 + lane;
+      const bool rok = row < M;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * Cfg::BN;
+#pragma unroll 1
+      for (int c = 0; c < Cfg::BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c, r);
+        const int col0 = nb * Cfg::BN + c;
+        tmem_ld_wait();
+        if (rok) {
+          float* out = C + (splits > 1 ? (long long)s * split_stride : 0LL) + row;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = col0 + j;
+            if (col < N) {
+              float v = __uint_as_float(r[j]);
+              if (splits == 1 && col_mult) v *= __ldg(col_mult + col);
+              out[(long long)col * ldc] = v;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(leader_addr(&tempty[acc]))
+                     : "memory");
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(Cfg::TMEM_COLS)
+                 : "memory");
+  }
+}
+
 // Deterministic split-K reduction: C[i + j*ldc] = (sum_s P[s][i + j*ldp]) * col_mult[j].
 // 8 threads per output element (each sums a contiguous range of splits with all loads in
 // flight), combined in a fixed order through shared memory.
@@ -394,18 +609,82 @@ static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const C
   return cudaGetLastError();
 }
 
+// 2-CTA TN launch (h, w2 >= 256): one cluster pair per 256 x 256 tile and split.
+static cudaError_t launch_tc2_tn(const __half* A1h, long long lda1, const __half* A2h,
+                                 long long lda2, int m, int h, int w2, int splits, float* C,
+                                 long long ldc, long long sstride, const float* mult, int num_sms,
+                                 cudaStream_t st) {
+  using Cfg = Tc2Cfg;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm2_tn_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap ma, mb;
+  if (!make_map_f16(&ma, A1h, m, h, lda1, 64, 128)) return cudaErrorInvalidValue;
+  if (!make_map_f16(&mb, A2h, m, w2, lda2, 64, 128)) return cudaErrorInvalidValue;
+  const int units = ((h + 255) / 256) * ((w2 + 255) / 256) * splits;
+  const int npairs = std::min(units, num_sms / 2);
+  tc_gemm2_tn_kernel<<<2 * npairs, 192, Cfg::SMEM, st>>>(ma, mb, h, w2, m, splits, C, ldc, sstride,
+                                                         mult);
+  return cudaGetLastError();
+}
+
+static bool use_tc2() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("TCQR_TC2");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // D (h x w2) = A1h' A2h ; writes C (ldc) directly (splits == 1, scaled by col_mult) or the
 // partials P (splits > 1; P has room for splits * ldp * w2 floats) followed by the reduction.
 cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, const __half* A2h,
                        long long lda2, float* C, long long ldc, const float* col_mult, float* P,
                        long long p_cap, int num_sms, cudaStream_t st, const R12Finalize* fin) {
   if (m <= 0 || h <= 0 || w2 <= 0) return cudaSuccess;
+  const int nkb = (m + 63) / 64;
+  if (use_tc2() && h >= 256 && w2 >= 256) {
+    // CTA pairs: 256 x 256 tiles, split-K over the pairs
+    const int tiles2 = ((h + 255) / 256) * ((w2 + 255) / 256);
+    int splits = 1;
+    const int np = num_sms / 2;
+    if (tiles2 < np) {
+      splits = np / tiles2;
+      if (splits > nkb / 8) splits = nkb / 8;
+      if (splits < 1) splits = 1;
+      const long long per = (long long)h * w2;
+      if (P == nullptr || per * splits > p_cap) splits = P ? (int)(p_cap / per) : 1;
+      if (splits < 1) splits = 1;
+    }
+    cudaError_t e;
+    if (splits == 1) {
+      e = launch_tc2_tn(A1h, lda1, A2h, lda2, m, h, w2, 1, C, ldc, 0, col_mult, num_sms, st);
+      if (e != cudaSuccess || !fin) return e;
+      return r12_finalize(h, w2, C, ldc, fin->Rblk, fin->ldr, fin->R12h, fin->ldh2, fin->inv_s2,
+                          fin->scaling, st);
+    }
+    const long long sstride = (long long)h * w2;
+    e = launch_tc2_tn(A1h, lda1, A2h, lda2, m, h, w2, splits, P, h, sstride, nullptr, num_sms, st);
+    if (e != cudaSuccess) return e;
+    if (fin)
+      return r12_splitk_finalize(h, w2, P, splits, sstride, h, col_mult, fin->Rblk, fin->ldr,
+                                 fin->R12h, fin->ldh2, fin->inv_s2, fin->scaling, st);
+    const long long total = (long long)h * w2;
+    int grid = (int)((total + 31) / 32);
+    if (grid > 8 * num_sms) grid = 8 * num_sms;
+    splitk_reduce_kernel<<<grid, 256, 0, st>>>(P, splits, sstride, h, h, w2, C, ldc, col_mult);
+    return cudaGetLastError();
+  }
   CUtensorMap ma, mb;
   const int BN = (w2 > 128) ? 256 : 128;
   if (!make_map_f16(&ma, A1h, m, h, lda1, 64, 128)) return cudaErrorInvalidValue;
   if (!make_map_f16(&mb, A2h, m, w2, lda2, 64, BN)) return cudaErrorInvalidValue;
   const int tiles = ((h + 127) / 128) * ((w2 + BN - 1) / BN);
-  const int nkb = (m + 63) / 64;
   int splits = 1;
   if (tiles < num_sms) {
     splits = num_sms / tiles;

@@ -59,7 +59,11 @@ def _fp16_operand(rng, m, k, scale=1.0):
 
 
 @pytest.mark.parametrize("m,h,w2", [(64, 128, 128), (1000, 96, 200), (4160, 128, 384),
-                                    (8192, 300, 130), (262144, 128, 128)])
+                                    (8192, 300, 130), (262144, 128, 128),
+                                    # h, w2 >= 256: the CTA-pair (cta_group::2) kernel, with
+                                    # ragged 256-tiles and split-K / no split
+                                    (8192, 512, 384), (4104, 300, 640), (16384, 2048, 1024),
+                                    (96, 256, 256)])
 def test_gemm_tn_envelope(tq, m, h, w2):
     rng = np.random.default_rng(h + w2)
     a1 = _fp16_operand(rng, m, h)
