@@ -38,6 +38,23 @@ struct TcCfg {
   static constexpr int SMEM = ST * STAGE + CBUF + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// Work unit w -> (tile row mb, tile column nb, split s).  Tile rows are taken in groups of 16:
+// inside a group the row index runs fastest and the column index next, so the tiles in flight at
+// once share 16 row blocks of A and a few column blocks of B through L2 (the plain row-fastest
+// order streams a different A row block per CTA for every column block: 4x the HBM traffic of
+// the top-level update).
+__device__ __forceinline__ void tile_of(int w, int tiles_m, int tiles_n, int& mb, int& nb, int& s) {
+  constexpr int GM = 16;
+  const int per = tiles_m * tiles_n;
+  s = w / per;
+  const int t = w - s * per;
+  const int g = t / (GM * tiles_n);
+  const int gm = min(GM, tiles_m - g * GM);
+  const int l = t - g * GM * tiles_n;
+  mb = g * GM + l % gm;
+  nb = l / gm;
+}
+
 template <int BN, int MODE, int NBUF>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -89,7 +106,8 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n, s = w / (tiles_m * tiles_n);
+        int mb, nb, s;
+        tile_of(w, tiles_m, tiles_n, mb, nb, s);
         const int kb0 = (int)((long long)s * nkb / splits), kb1 = (int)((long long)(s + 1) * nkb / splits);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -159,7 +177,8 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t cph = 0;
     int it = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
-      const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n;
+      int mb, nb, s_unused;
+      tile_of(w, tiles_m, tiles_n, mb, nb, s_unused);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int ncol = min(BN, N - nb * BN), nch = (ncol + 31) / 32;
@@ -213,7 +232,8 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int it = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
-      const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n, s = w / (tiles_m * tiles_n);
+      int mb, nb, s;
+      tile_of(w, tiles_m, tiles_n, mb, nb, s);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int row = mb * BM + q * 32 + lane;
@@ -318,8 +338,9 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {
   return smem_u32(p) & 0xFEFFFFFFu;
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
-    tc_gemm2_tn_kernel(const __grid_constant__ CUtensorMap tmA,
+    tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K, int splits,
                        float* __restrict__ C, long long ldc, long long split_stride,
                        const float* __restrict__ col_mult) {
@@ -372,7 +393,8 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int w = pair; w < total; w += npairs) {
-        const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n, s = w / (tiles_m * tiles_n);
+        int mb, nb, s;
+        tile_of(w, tiles_m, tiles_n, mb, nb, s);
         const int kb0 = (int)((long long)s * nkb / splits), kb1 = (int)((long long)(s + 1) * nkb / splits);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -380,12 +402,23 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
           uint8_t* sa = smem + stage * STAGE;
           uint8_t* sb = sa + Cfg::A_BYTES;
           const uint32_t bar = leader_addr(&full[stage]);
-          asm volatile(
-              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-              " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sa)),
-              "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(bar), "r"(kb * BK),
-              "r"(mb * 256 + (int)rank * 128)
-              : "memory");
+          if (MODE == kModeTN) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sa)),
+                "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(bar), "r"(kb * BK),
+                "r"(mb * 256 + (int)rank * 128)
+                : "memory");
+          } else {  // A = Q1 MN-major: two 64 (M) x 64 (K) boxes of this CTA's 128 rows
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sa + hh * 8192)),
+                  "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(bar),
+                  "r"(mb * 256 + (int)rank * 128 + hh * 64), "r"(kb * BK)
+                  : "memory");
+          }
           asm volatile(
               "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
               " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sb)),
@@ -401,7 +434,7 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only) ----------------
-      constexpr uint32_t idesc = make_idesc_f16(256, 256, 0, 0);
+      constexpr uint32_t idesc = make_idesc_f16(256, 256, MODE == kModeNN ? 1 : 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -420,7 +453,8 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
           const uint32_t base_b = base_a + Cfg::A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t da = make_sw128_desc(base_a + kk * 32, 16, 1024);
+            const uint64_t da = (MODE == kModeTN) ? make_sw128_desc(base_a + kk * 32, 16, 1024)
+                                                  : make_sw128_desc(base_a + kk * 2048, 8192, 1024);
             const uint64_t db = make_sw128_desc(base_b + kk * 32, 16, 1024);
             const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
             asm volatile(
@@ -453,11 +487,22 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
     const int q = warp & 3;
     int it = 0;
     for (int w = pair; w < total; w += npairs, ++it) {
-      const int mb = w % tiles_m, nb = (w / tiles_m) % tiles_n, s = w / (tiles_m * tiles_n);
+      int mb, nb, s;
+      tile_of(w, tiles_m, tiles_n, mb, nb, s);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int row = mb * 256 + (int)rank * 128 + q * 32 + lane;
       const bool rok = row < M;
+      // NN: the first FP32 C chunk is loaded before waiting for the accumulator, later chunks
+      // one ahead (as the 1-CTA kernel)
+      float cv[32];
+      if (MODE == kModeNN) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = nb * Cfg::BN + j;
+          cv[j] = (rok && col < N) ? C[row + (long long)col * ldc] : 0.f;
+        }
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * Cfg::BN;
@@ -466,18 +511,41 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c, r);
         const int col0 = nb * Cfg::BN + c;
-        tmem_ld_wait();
-        if (rok) {
-          float* out = C + (splits > 1 ? (long long)s * split_stride : 0LL) + row;
+        if (MODE == kModeTN) {
+          tmem_ld_wait();
+          if (rok) {
+            float* out = C + (splits > 1 ? (long long)s * split_stride : 0LL) + row;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = col0 + j;
-            if (col < N) {
-              float v = __uint_as_float(r[j]);
-              if (splits == 1 && col_mult) v *= __ldg(col_mult + col);
-              out[(long long)col * ldc] = v;
+            for (int j = 0; j < 32; ++j) {
+              const int col = col0 + j;
+              if (col < N) {
+                float v = __uint_as_float(r[j]);
+                if (splits == 1 && col_mult) v *= __ldg(col_mult + col);
+                out[(long long)col * ldc] = v;
+              }
             }
           }
+        } else {
+          float cn[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = col0 + 32 + j;
+            cn[j] = (rok && c + 32 < Cfg::BN && col < N) ? C[row + (long long)col * ldc] : 0.f;
+          }
+          tmem_ld_wait();
+          if (rok) {
+            float* out = C + row;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = col0 + j;
+              if (col < N) {
+                const float mlt = col_mult ? __ldg(col_mult + col) : 1.f;
+                out[(long long)col * ldc] = cv[j] - __uint_as_float(r[j]) * mlt;
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) cv[j] = cn[j];
         }
       }
       tc_fence_before();
@@ -609,27 +677,34 @@ static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const C
   return cudaGetLastError();
 }
 
-// 2-CTA TN launch (h, w2 >= 256): one cluster pair per 256 x 256 tile and split.
-static cudaError_t launch_tc2_tn(const __half* A1h, long long lda1, const __half* A2h,
-                                 long long lda2, int m, int h, int w2, int splits, float* C,
-                                 long long ldc, long long sstride, const float* mult, int num_sms,
-                                 cudaStream_t st) {
+// CTA-pair launches: one cluster pair per 256 x 256 tile (and split for TN).
+template <int MODE>
+static cudaError_t launch_tc2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
+                              int splits, float* C, long long ldc, long long sstride,
+                              const float* mult, int num_sms, cudaStream_t st) {
   using Cfg = Tc2Cfg;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm2_tn_kernel,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm2_kernel<MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  const int units = ((M + 255) / 256) * ((N + 255) / 256) * splits;
+  const int npairs = std::min(units, num_sms / 2);
+  tc_gemm2_kernel<MODE><<<2 * npairs, 192, Cfg::SMEM, st>>>(ma, mb, M, N, K, splits, C, ldc,
+                                                             sstride, mult);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_tc2_tn(const __half* A1h, long long lda1, const __half* A2h,
+                                 long long lda2, int m, int h, int w2, int splits, float* C,
+                                 long long ldc, long long sstride, const float* mult, int num_sms,
+                                 cudaStream_t st) {
   CUtensorMap ma, mb;
   if (!make_map_f16(&ma, A1h, m, h, lda1, 64, 128)) return cudaErrorInvalidValue;
   if (!make_map_f16(&mb, A2h, m, w2, lda2, 64, 128)) return cudaErrorInvalidValue;
-  const int units = ((h + 255) / 256) * ((w2 + 255) / 256) * splits;
-  const int npairs = std::min(units, num_sms / 2);
-  tc_gemm2_tn_kernel<<<2 * npairs, 192, Cfg::SMEM, st>>>(ma, mb, h, w2, m, splits, C, ldc, sstride,
-                                                         mult);
-  return cudaGetLastError();
+  return launch_tc2<kModeTN>(ma, mb, h, w2, m, splits, C, ldc, sstride, mult, num_sms, st);
 }
 
 static bool use_tc2() {
@@ -727,8 +802,13 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
                               const float* col_mult, int num_sms, cudaStream_t st) {
   if (m <= 0 || h <= 0 || w2 <= 0) return cudaSuccess;
   CUtensorMap ma, mb;
-  const int BN = (w2 > 128) ? 256 : 128;
   if (!make_map_f16(&ma, Qh, m, h, ldq, 64, 64)) return cudaErrorInvalidValue;
+  if (use_tc2() && h > 2048 && w2 >= 256) {
+    // long K: CTA pairs with 256 x 256 tiles (each CTA stages 128 columns of B)
+    if (!make_map_f16(&mb, Bh, h, w2, ldb, 64, 128)) return cudaErrorInvalidValue;
+    return launch_tc2<kModeNN>(ma, mb, m, w2, h, 1, C, ldc, 0, col_mult, num_sms, st);
+  }
+  const int BN = (w2 > 128) ? 256 : 128;
   if (!make_map_f16(&mb, Bh, h, w2, ldb, 64, BN)) return cudaErrorInvalidValue;
   // TMA epilogue (C chunks through shared memory, four buffers) for short K = h, where the
   // update is epilogue-bound, when C's columns are 16-byte aligned; the direct-load epilogue with

@@ -79,7 +79,9 @@ def test_gemm_tn_envelope(tq, m, h, w2):
 
 
 @pytest.mark.parametrize("m,h,w2", [(128, 64, 128), (1000, 96, 200), (4160, 256, 384),
-                                    (3000, 512, 64)])
+                                    (3000, 512, 64),
+                                    # h > 2048, w2 >= 256: the CTA-pair kernel (ragged tiles)
+                                    (4104, 2304, 320), (704, 4096, 256)])
 def test_gemm_nn_update_envelope(tq, m, h, w2):
     rng = np.random.default_rng(m + h)
     qh = _fp16_operand(rng, m, h, 0.05)
