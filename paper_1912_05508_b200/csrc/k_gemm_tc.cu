@@ -707,11 +707,15 @@ static cudaError_t launch_tc2_tn(const __half* A1h, long long lda1, const __half
   return launch_tc2<kModeTN>(ma, mb, h, w2, m, splits, C, ldc, sstride, mult, num_sms, st);
 }
 
+static int kTc2NnMinK = 2049;  // NN on CTA pairs from this K = h on (env TCQR_TC2_NN_MINK)
+
 static bool use_tc2() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("TCQR_TC2");
     on = (e && e[0] == '0') ? 0 : 1;
+    const char* k = getenv("TCQR_TC2_NN_MINK");
+    if (k) kTc2NnMinK = atoi(k);
   }
   return on == 1;
 }
@@ -803,7 +807,7 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
   if (m <= 0 || h <= 0 || w2 <= 0) return cudaSuccess;
   CUtensorMap ma, mb;
   if (!make_map_f16(&ma, Qh, m, h, ldq, 64, 64)) return cudaErrorInvalidValue;
-  if (use_tc2() && h > 2048 && w2 >= 256) {
+  if (use_tc2() && h >= kTc2NnMinK && w2 >= 256) {
     // long K: CTA pairs with 256 x 256 tiles (each CTA stages 128 columns of B)
     if (!make_map_f16(&mb, Bh, h, w2, ldb, 64, 128)) return cudaErrorInvalidValue;
     return launch_tc2<kModeNN>(ma, mb, m, w2, h, 1, C, ldc, 0, col_mult, num_sms, st);
