@@ -4,6 +4,8 @@
 // The paper is silent on FP16 range (PAPER.md:127-141 only notes FP16's "significantly
 // constrained range"); reading R-A4 guards it with a per-column power-of-two scale
 // s_j = 2^-floor(log2 max_i |X_ij|), exact to apply and undo.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -35,7 +37,8 @@ __global__ void __launch_bounds__(kCastThreads) cast_scale_kernel(
   const int m4 = vec ? (m & ~3) : 0;
   float mx = 0.f;
   bool bad = false;
-  for (int i = threadIdx.x * 4; i < m4; i += kCastThreads * 4) {
+#pragma unroll 8
+  for (int i = threadIdx.x * 4; i < m4; i += kCastThreads * 4) {  // 8 loads in flight
     const float4 v = *reinterpret_cast<const float4*>(x + i);
     mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
     bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
@@ -52,6 +55,7 @@ __global__ void __launch_bounds__(kCastThreads) cast_scale_kernel(
     s = pow2_scale_for(mx);
   }
   if (threadIdx.x == 0 && inv_s) inv_s[j] = 1.f / s;
+#pragma unroll 8
   for (int i = threadIdx.x * 4; i < m4; i += kCastThreads * 4) {
     const float4 v = *reinterpret_cast<const float4*>(x + i);
     __half2 lo = __floats2half2_rn(v.x * s, v.y * s);
@@ -135,7 +139,12 @@ cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, 
   if (m <= 0 || w <= 0) return cudaSuccess;
   // Few columns x many rows: split rows (2-D grid, pass 1 = column max via atomicMax).
   // Many columns: one CTA per column already fills the GPU.
-  if (w >= 1024 || (!scaling && !status) || !cmax) {
+  static int col_min = -1;  // per-column kernel from this width on (env TCQR_CAST_COL_MIN)
+  if (col_min < 0) {
+    const char* e = getenv("TCQR_CAST_COL_MIN");
+    col_min = e ? atoi(e) : 1024;
+  }
+  if (w >= col_min || (!scaling && !status) || !cmax) {
     if (!scaling && !status) {
       const int rows_per = 8192;
       dim3 g((m + rows_per - 1) / rows_per, w);
