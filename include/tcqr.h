@@ -69,6 +69,11 @@ typedef struct tcqr_config {
   int warm_start;    /* 1: tcqr_lls_solve starts CGLS from the direct QR solution
                         x0 = R^-1 Q' b (Alg. 1; NEXT-2) instead of x0 = 0
                         (Alg. 5 line 4); pass 1 then iterates on r0 = b - A x0 (default 0)      */
+  int leaf_kernel;   /* 1: every leaf (w <= min(cutoff, 128), one GPU, m <= 148 * 256) runs as ONE
+                        cooperative launch with 256-row blocks resident in shared memory and the
+                        Eq. (6) stack factored through its FP64 Gram matrix (reading R-A28);
+                        0: one pipelined MGS-root panel launch per 32 columns plus FP32
+                        projection launches (default 1)                                         */
 } tcqr_config_t;
 
 /* Per-solve report (SPEC.md:296-299 CglsReport). */
@@ -204,7 +209,8 @@ enum {
   TCQR_K6_TRI = 10,     /* CGLS inv(R) p and inv(R') v                             */
   TCQR_K7_SCALAR = 11,  /* CGLS scalar / vector recurrences                        */
   TCQR_TRINV = 12,      /* one-time explicit inverse of R                          */
-  TCQR_NUM_CLASSES = 13
+  TCQR_K2_LEAF = 13,    /* K2L whole-leaf kernel: panels + FP32 projections (k_leaf.cu) */
+  TCQR_NUM_CLASSES = 14
 };
 int tcqr_profile_enable(int on);
 int tcqr_profile_read(int cls, double* ms, double* flops, double* bytes, int* launches);

@@ -33,7 +33,8 @@ class TcqrConfig(ctypes.Structure):
                 ("col_scaling", ctypes.c_int), ("restart", ctypes.c_int),
                 ("tol2", ctypes.c_double), ("stag_window", ctypes.c_int),
                 ("stag_floor", ctypes.c_double), ("use_graphs", ctypes.c_int),
-                ("reorth", ctypes.c_int), ("warm_start", ctypes.c_int)]
+                ("reorth", ctypes.c_int), ("warm_start", ctypes.c_int),
+                ("leaf_kernel", ctypes.c_int)]
 
 
 class TcqrLlsInfo(ctypes.Structure):
@@ -79,7 +80,7 @@ _SIGS = {
     "tcqr_last_launch_count": (ctypes.c_int, []),
 }
 PROFILE_CLASSES = ["copy", "k1_cast", "k3_tn", "k3_finalize", "k4_nn", "k2_mgs", "k2_apply",
-                   "k2b_tn", "k2b_nn", "k5_gemv", "k6_tri", "k7_scalar", "trinv"]
+                   "k2b_tn", "k2b_nn", "k5_gemv", "k6_tri", "k7_scalar", "trinv", "k2_leaf"]
 EXPORTS = tuple(_SIGS)
 
 

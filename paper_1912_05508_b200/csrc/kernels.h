@@ -79,6 +79,18 @@ int fused_panel_max_rows();
 extern unsigned long long* g_panel_dbg;
 extern unsigned long long* g_proj_dbg;  // debug: phase timestamps of the FP32 projection  // debug: phase timestamps of the fused panel
 
+// ---- K2L whole-leaf kernel (k_leaf.cu) ----
+// The leaf columns [0, wl) of X (m rows, ldx; wl <= 128) factored in one cooperative launch:
+// Q in place (and its FP16 shadow into Xh when non-null), R(i, j) of the leaf at R[i + j ldr].
+// scratch: leaf_scratch_bytes() of device memory; bar: an arrival counter zeroed together with
+// *bar_seq = 0 (the host's count of completed grid barriers, advanced by each launch).
+// cudaErrorNotSupported when the blocks do not fit the co-resident grid.
+size_t leaf_scratch_bytes();
+extern unsigned long long* g_leaf_dbg;  // debug: CTA-0 phase timestamps of the leaf kernel
+cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long long ldh, float* R,
+                       long long ldr, int col0, int* status, void* scratch, size_t scratch_bytes,
+                       unsigned* bar, unsigned* bar_seq, int num_sms, cudaStream_t st);
+
 // ---- K2b FP32 intra-leaf products (k_f32.cu) ----
 // T (h x w2, ld h) = Q1' A2 over m rows (deterministic split-K with partials in P).
 cudaError_t f32_tn(int m, int h, int w2, const float* Q1, long long ldq, const float* A2,

@@ -130,6 +130,7 @@ struct FactorWs {
   float* pipeS = nullptr;        // pipelined panel: root Q slices (NaN between uses)
   float* R2 = nullptr;           // re-orthogonalization: R of the second pass (n x n)
   float* Rt = nullptr;           // re-orthogonalization: R2 * R1 staging (n x n)
+  unsigned leaf_bars = 0;        // grid barriers the leaf kernels completed since iws was zeroed
 };
 
 static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, FactorWs& w,
@@ -507,6 +508,19 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   FactorWs& ws = *J.ws;
   const int m = J.m;
   float* Qc = J.Q + (long long)c0 * J.ldq;
+  if (c.cfg.leaf_kernel && c.nranks == 1 && w <= 128 && w <= c.cfg.cutoff) {
+    // the whole leaf (every node below the cutoff) in one cooperative launch (k_leaf.cu)
+    need_cols(J, c0, c0 + w);
+    cudaError_t e = cudaErrorNotSupported;
+    PROF(TCQR_K2_LEAF, 2.0 * m * w * w, 8.0 * m * w + (need_h ? 2.0 * m * w : 0.0),
+         e = leaf_fused(m, w, Qc, J.ldq, need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, ws.ldh,
+                        J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0, c.d_status, ws.P,
+                        sizeof(float) * (size_t)ws.p_cap, reinterpret_cast<unsigned*>(ws.iws + ws.iws_cap - 16),
+                        &ws.leaf_bars, c.num_sms, c.stream));
+    if (e == cudaSuccess) return chunk_done(J, c0, w);
+    if (e != cudaErrorNotSupported) CK(e);
+    cudaGetLastError();
+  }
   if (w <= 32) {
     bool wrote_h = false;
     need_cols(J, c0, c0 + w);
@@ -611,6 +625,7 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));  // INT_MAX-ish = OK
   CK(cudaMemsetAsync(R, 0, sizeof(float) * (size_t)n * n, c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
+  ws.leaf_bars = 0;
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   PROF(TCQR_COPY, 0, 8.0 * m * n, CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream)));
   FactorJob J{m, n, Q, (long long)m, R, (long long)n, &ws};
@@ -649,7 +664,8 @@ static std::string graph_key(const char* tag, std::initializer_list<long long> v
     k += buf;
   }
   const tcqr_config_t& f = g_ctx.cfg;
-  snprintf(buf, sizeof buf, "|%d,%d,%d,%d", f.cutoff, f.panel_rows, f.col_scaling, f.reorth);
+  snprintf(buf, sizeof buf, "|%d,%d,%d,%d,%d", f.cutoff, f.panel_rows, f.col_scaling, f.reorth,
+           f.leaf_kernel);
   k += buf;
   return k;
 }
@@ -727,6 +743,7 @@ void tcqr_default_config(tcqr_config_t* c) {
   c->use_graphs = 1;
   c->reorth = 0;
   c->warm_start = 0;
+  c->leaf_kernel = 1;
 }
 
 int tcqr_set_config(const tcqr_config_t* cfg) {
@@ -737,6 +754,7 @@ int tcqr_set_config(const tcqr_config_t* cfg) {
   if (cfg->tol2 <= 0 || cfg->stag_window < 1 || cfg->stag_floor < 0) return -1;
   if (cfg->reorth != 0 && cfg->reorth != 1) return -1;
   if (cfg->warm_start != 0 && cfg->warm_start != 1) return -1;
+  if (cfg->leaf_kernel != 0 && cfg->leaf_kernel != 1) return -1;
   g_ctx.cfg = *cfg;
   return 0;
 }
@@ -1064,6 +1082,7 @@ static int factor_host_streamed(int m, int n, const float* A, long long lda, flo
   // compute stream
   CK(cudaMemsetAsync(dR, 0, sizeof(float) * (size_t)n * n, c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
+  ws.leaf_bars = 0;
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   FactorJob J{m, n, dQ, (long long)m, dR, (long long)n, &ws, &sp};
   rc = rgs(J, 0, n, n > c.cfg.cutoff);
@@ -1235,6 +1254,7 @@ int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t
   plan_factor_ws(a, m, 32, 1, ws);
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
+  ws.leaf_bars = 0;
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   bool wrote_h = false;
   int rc = panel(ws, (int)m, (int)w, X, ldx, R, ldr, 0, nullptr, &wrote_h);
@@ -1327,6 +1347,10 @@ int tcqr_last_launch_count(void) { return g_last_launches; }
 // Debug: pointer to 64 device uint64 slots receiving fused-panel phase timestamps (or NULL).
 int tcqr_debug_panel_timestamps(void* dptr) {
   g_panel_dbg = static_cast<unsigned long long*>(dptr);
+  return 0;
+}
+int tcqr_debug_leaf_timestamps(void* dptr) {
+  g_leaf_dbg = static_cast<unsigned long long*>(dptr);
   return 0;
 }
 int tcqr_debug_proj_timestamps(void* dptr) {

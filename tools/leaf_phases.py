@@ -1,0 +1,41 @@
+"""Phase timestamps (us, CTA 0) of the whole-leaf kernel on an m x 128 leaf (debug hook
+tcqr_debug_leaf_timestamps); phases: load, then per op (panel: mgs, gram+barrier, sum, barrier,
+chol+S, apply; proj: partial, barrier, sum, barrier, update), then the final write."""
+import ctypes, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np, torch
+import paper_1912_05508_b200 as tq
+import workloads as W
+tq.init(0)
+L = tq.lib()
+L.tcqr_debug_leaf_timestamps.argtypes = [ctypes.c_void_p]
+names = ["load"]
+for op in ["P0", "J01", "P1", "J0123", "P2", "J23", "P3"]:
+    if op[0] == "P":
+        names += [op + s for s in (":mgs", ":gram+bar", ":sum", ":bar", ":chol+S", ":apply")]
+    else:
+        names += [op + s for s in (":partial", ":bar", ":sum", ":bar", ":update")]
+names += ["write"]
+for m in [int(v) for v in (sys.argv[1:] or ["32768"])]:
+    dbg = torch.zeros(128, dtype=torch.int64, device="cuda")
+    A = W.gaussian_cuda(m, 128, 3)
+    Q = torch.empty_like(A)
+    R = torch.empty(128, 128, device="cuda").t()
+    tq.set_config(use_graphs=0)
+    for _ in range(3):
+        tq.factor(A, Q, R)
+    L.tcqr_debug_leaf_timestamps(ctypes.c_void_p(dbg.data_ptr()))
+    runs, extra = [], []
+    for _ in range(5):
+        dbg.zero_()
+        tq.factor(A, Q, R)
+        torch.cuda.synchronize()
+        d = dbg.cpu().numpy().astype(np.int64)
+        runs.append(np.diff(d[:len(names) + 1]) / 1000.0)
+        extra.append(((d[102] - d[100]) / 1000.0, (d[103] - d[101]) / 1000.0))
+    L.tcqr_debug_leaf_timestamps(None)
+    med = np.median(np.array(runs), axis=0)
+    print(f"m={m}: total {med.sum():.1f} us; last panel: chol warp {np.median([e[0] for e in extra]):.2f} us, S warp {np.median([e[1] for e in extra]):.2f} us")
+    for nm, v in zip(names, med):
+        print(f"  {nm:16s} {v:7.2f}")
