@@ -72,12 +72,11 @@ struct Smem {
   float L[kRows * kLd];  // the block's rows of the leaf, row-major
   float Rb[32 * 32];     // R_b of the current panel, row-major
   float Sf[32 * 32];     // S_b (FP32), row-major [l][j]
-  double Rd[32 * 34];    // the panel's R in FP64, row-major (ld 34)
-  double Ri[32];         // 1 / R(k, k)
+  double Rd[32 * 34 + 34];  // the panel's R in FP64, row-major (ld 34; one row of slack)
+  double Rbd[32 * 32];   // R_b widened to FP64, row-major
   float T[4096];         // R12 (row-major [i][w2p]) / projection group partials
   float red[2 * kNW * 32];
   float wsum[kNW * 32];  // per-warp partial sums of the cross-CTA reductions
-  int flag;              // Cholesky rows published to the S_b warp
   unsigned barseq;       // grid barriers passed by this CTA in this launch (thread 0)
 };
 
@@ -195,13 +194,16 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
   }
   __syncthreads();
   leaf_ts(a, slot);
-  // (2) this block's Gram G_b = R_b' R_b (upper triangle), FP64
+  // (2) this block's Gram G_b = R_b' R_b (upper triangle), FP64.  R_b is widened to FP64 once
+  // (the FP32 -> FP64 conversions run at 1/8 of the FMA rate: widening inside the product loop
+  // cost ~1 us per panel)
+  for (int e = t; e < 1024; e += kNT) s.Rbd[e] = (double)s.Rb[e];
+  __syncthreads();
   for (int e = t; e < 1024; e += kNT) {
     const int i = e >> 5, j = e & 31;
     double g = 0.0;
     if (i <= j && j < pw) {
-      for (int l = 0; l <= i; ++l)
-        g = fma((double)s.Rb[l * 32 + i], (double)s.Rb[l * 32 + j], g);
+      for (int l = 0; l <= i; ++l) g = fma(s.Rbd[l * 32 + i], s.Rbd[l * 32 + j], g);
     }
     a.gpart[(long long)blockIdx.x * 1024 + e] = g;
   }
@@ -212,67 +214,73 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
   leaf_ts(a, slot);
   leaf_barrier(a, s);
   leaf_ts(a, slot);
-  // (3) R = chol(G) (warp 0, lane j = column j) and S_b = R_b R^-1 (warp 1, lane i = row i),
-  // warp 1 one row of R behind warp 0.  One FP64 reciprocal square root per step (1/R(k,k),
-  // <= 1 ulp): R(k, j) = W(k, j) / R(k, k) and the S_b quotients become products.  FP64 values
-  // within an ulp round to the same FP32 R and Q outputs (exact inputs stay exact: the planted pin).
-  if (t == 0) s.flag = 0;
-  __syncthreads();
-  if (a.dbg && blockIdx.x == 0 && (t == 0 || t == 32)) {  // debug: chol / S warp start
+  if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: Cholesky start
     unsigned long long v;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
-    a.dbg[100 + (t >> 5)] = v;
+    a.dbg[100] = v;
   }
+  // (3) R = chol(G) and S_b = R_b R^-1 in warp 0, one ROLLED pass over k (the fully unrolled
+  // 32-step chain was ~100 KB of straight-line code run once per panel: instruction-fetch bound).
+  // Lane j holds column j of the trailing Gram, c[i] = W(k+i, j) (shifted down one slot per step,
+  // so the pivot is always c[0]), and row j of S_b under forward substitution, r[i] = the running
+  // value of column k+i.  Step k: the pivot G(k,k) from lane k by shuffle, one FP64 reciprocal
+  // square root (1/R(k,k), <= 1 ulp: R(k,j) = W(k,j) / R(k,k) and the S_b quotients become
+  // products; FP64 values within an ulp round to the same FP32 R and Q, exact inputs stay exact
+  // -- the planted pin), row k of R broadcast through shared memory.
   if (warp == 0) {
-    double c[32];  // lane j: c[i] = W(i, j), the trailing Gram's column j (i <= j used)
+    double c[32], r[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) c[i] = (i <= lane && lane < pw) ? __ldcg(a.gsum + i * 32 + lane) : 0.0;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      if (k < pw) {
-        const double d = __shfl_sync(0xffffffffu, c[k], k);
-        const bool ok = d > 0.0 && d <= 1.7976931348623157e308;
-        const double ri = ok ? rsqrt(d) : 0.0;
-        const double rkj = lane == k ? d * ri : (lane > k ? c[k] * ri : 0.0);
-        s.Rd[k * 34 + lane] = rkj;
-        if (lane == 0) s.Ri[k] = ri;
-        if (!ok && lane == 0 && blockIdx.x == 0 && a.status) atomicMin(a.status, a.col0 + c0 + k + 1);
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence_block();  // row k of R (all lanes, ordered by the warp barrier) first
-          *reinterpret_cast<volatile int*>(&s.flag) = k + 1;
-        }
-        // trailing update with row k broadcast from shared memory
-        const double* rk = s.Rd + k * 34;
-#pragma unroll
-        for (int i = k + 1; i < 32; ++i) c[i] = fma(-rk[i], rkj, c[i]);
-      }
+    for (int j = 0; j < 32; ++j) r[j] = (lane < pw && j < pw) ? s.Rbd[lane * 32 + j] : 0.0;
+    if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: Cholesky inputs loaded
+      unsigned long long v;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v) : "d"(c[31]), "d"(r[31]));
+      a.dbg[101] = v;
     }
-  } else if (warp == 1) {
-    // row i of S_b: s R = R_b(i, :), s_t = (R_b(i, t) - sum_{l<t} s_l R(l, t)) / R(t, t)
-    double r[32];
+    // software-pipelined: the pivot of step k+1 (lane k+1's first update -> shuffle -> rsqrt) is
+    // issued at the top of step k's trailing updates; branch-free so it all schedules together
+    double d = __shfl_sync(0xffffffffu, c[0], 0);
+    bool ok = d > 0.0 && d <= 1.7976931348623157e308;
+    double ri = rsqrt_nr(ok ? d : 1.0);
+#pragma unroll 1
+    for (int k = 0; k < pw; ++k) {
+      ri = ok ? ri : 0.0;
+      const double rkj = lane == k ? d * ri : (lane > k ? c[0] * ri : 0.0);
+      s.Rd[k * 34 + lane] = rkj;
+      if (!ok && lane == 0 && blockIdx.x == 0 && a.status) atomicMin(a.status, a.col0 + c0 + k + 1);
+      const double sk = r[0] * ri;
+      s.Sf[lane * 32 + k] = (float)sk;
+      __syncwarp();
+      const double* rk = s.Rd + k * 34 + k + 1;  // R(k, k+1+i); entries past column 31 are unused
+      const double v0 = rk[0];
+      c[0] = fma(-v0, rkj, c[1]);
+      r[0] = fma(-sk, v0, r[1]);
+      d = __shfl_sync(0xffffffffu, c[0], (k + 1) & 31);  // next pivot (unused after the last step)
+      ok = d > 0.0 && d <= 1.7976931348623157e308;
+      ri = rsqrt_nr(ok ? d : 1.0);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) r[j] = (lane < pw && j < pw) ? (double)s.Rb[lane * 32 + j] : 0.0;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      if (k < pw) {
-        while (*reinterpret_cast<volatile int*>(&s.flag) <= k) {
-        }
-        __threadfence_block();
-        const volatile double* rk = s.Rd + k * 34;
-        const double sk = r[k] * *reinterpret_cast<volatile double*>(&s.Ri[k]);
-        r[k] = sk;
-#pragma unroll
-        for (int j = k + 1; j < 32; ++j) r[j] = fma(-sk, rk[j], r[j]);
+      for (int i = 1; i < 31; ++i) {
+        const double v = rk[i];
+        c[i] = fma(-v, rkj, c[i + 1]);
+        r[i] = fma(-sk, v, r[i + 1]);
       }
+      c[31] = 0.0;
+      r[31] = 0.0;
     }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) s.Sf[lane * 32 + j] = (float)r[j];
+#pragma unroll 1
+    for (int j = pw; j < 32; ++j) s.Sf[lane * 32 + j] = 0.f;
   }
-  if (a.dbg && blockIdx.x == 0 && (t == 0 || t == 32)) {  // debug: chol / S warp end
+  __syncthreads();
+  if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: Cholesky end
     unsigned long long v;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
-    a.dbg[102 + (t >> 5)] = v;
+    a.dbg[102] = v;
+  }
+  if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: S end
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    a.dbg[103] = v;
   }
   __syncthreads();
   leaf_ts(a, slot);
@@ -282,33 +290,24 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
       if (i <= j) a.R[(c0 + i) + (long long)(c0 + j) * a.ldr] = (float)s.Rd[i * 34 + j];
     }
   }
-  // (4) Q_b <- Q_b S_b (S_b upper triangular: the zero terms add exactly nothing)
+  // (4) Q_b <- Q_b S_b (S_b upper triangular: the zero terms add exactly nothing); rolled over l
+  // (Q_b(t, l) read from shared memory per step) to keep the code small
   if (t < nrows) {
     float* row = s.L + t * kLd + c0;
-    float q[32];
-#pragma unroll
-    for (int l4 = 0; l4 < 8; ++l4) {
-      const float4 v = *reinterpret_cast<const float4*>(row + 4 * l4);
-      q[4 * l4] = v.x;
-      q[4 * l4 + 1] = v.y;
-      q[4 * l4 + 2] = v.z;
-      q[4 * l4 + 3] = v.w;
-    }
     float y[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) y[j] = 0.f;
+#pragma unroll 1
+    for (int l = 0; l < pw; ++l) {
+      const float ql = row[l];
+      const float4* sr = reinterpret_cast<const float4*>(s.Sf + l * 32);
 #pragma unroll
-    for (int l = 0; l < 32; ++l) {
-      if (l < pw) {
-        const float4* sr = reinterpret_cast<const float4*>(s.Sf + l * 32);
-#pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 v = sr[j4];
-          y[4 * j4] = fmaf(q[l], v.x, y[4 * j4]);
-          y[4 * j4 + 1] = fmaf(q[l], v.y, y[4 * j4 + 1]);
-          y[4 * j4 + 2] = fmaf(q[l], v.z, y[4 * j4 + 2]);
-          y[4 * j4 + 3] = fmaf(q[l], v.w, y[4 * j4 + 3]);
-        }
+      for (int j4 = 0; j4 < 8; ++j4) {
+        const float4 v = sr[j4];
+        y[4 * j4] = fmaf(ql, v.x, y[4 * j4]);
+        y[4 * j4 + 1] = fmaf(ql, v.y, y[4 * j4 + 1]);
+        y[4 * j4 + 2] = fmaf(ql, v.z, y[4 * j4 + 2]);
+        y[4 * j4 + 3] = fmaf(ql, v.w, y[4 * j4 + 3]);
       }
     }
 #pragma unroll
@@ -316,6 +315,11 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
       if (j < pw) row[j] = y[j];
   }
   __syncthreads();
+  if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: apply end (before the Q stores)
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    a.dbg[104] = v;
+  }
   // these pw columns of Q are final (later ops only read them): stream them out now (FP32 and
   // the FP16 shadow), coalesced down each column, overlapping the rest of the leaf
   if (t < nrows) {

@@ -17,7 +17,7 @@ for op in ["P0", "J01", "P1", "J0123", "P2", "J23", "P3"]:
     else:
         names += [op + s for s in (":partial", ":bar", ":sum", ":bar", ":update")]
 names += ["write"]
-for m in [int(v) for v in (sys.argv[1:] or ["32768"])]:
+for m in [int(v) for v in (sys.argv[1:] or ["32768"])]:  # m <= 148 * 256 (leaf kernel)
     dbg = torch.zeros(128, dtype=torch.int64, device="cuda")
     A = W.gaussian_cuda(m, 128, 3)
     Q = torch.empty_like(A)
@@ -33,9 +33,10 @@ for m in [int(v) for v in (sys.argv[1:] or ["32768"])]:
         torch.cuda.synchronize()
         d = dbg.cpu().numpy().astype(np.int64)
         runs.append(np.diff(d[:len(names) + 1]) / 1000.0)
-        extra.append(((d[102] - d[100]) / 1000.0, (d[103] - d[101]) / 1000.0))
+        extra.append(((d[102] - d[100]) / 1000.0, (d[104] - d[102]) / 1000.0, (d[101] - d[100]) / 1000.0))
     L.tcqr_debug_leaf_timestamps(None)
     med = np.median(np.array(runs), axis=0)
-    print(f"m={m}: total {med.sum():.1f} us; last panel: chol warp {np.median([e[0] for e in extra]):.2f} us, S warp {np.median([e[1] for e in extra]):.2f} us")
+    print(f"m={m}: total {med.sum():.1f} us; last panel: chol+S {np.median([e[0] for e in extra]):.2f} us, "
+          f"apply before stores {np.median([e[1] for e in extra]):.2f} us, chol input loads {np.median([e[2] for e in extra]):.2f} us")
     for nm, v in zip(names, med):
         print(f"  {nm:16s} {v:7.2f}")
