@@ -43,6 +43,12 @@ def conv_flops(m, n):
     return 2.0 * m * n * n - 2.0 / 3.0 * n ** 3
 
 
+def fp32_peak_tflops(sm_mhz=1965.0):
+    """FP32 SIMT peak of one B200: 148 SMs x 128 FP32 lanes x 2 flop (FMA) x the max SM clock
+    (1965 MHz, the clock nvidia-smi reports under load on this pool)."""
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -296,13 +302,26 @@ def main():
             roofline = {"bound": "tensor", "achieved": ach, "peak": peaks["tc_sustained"],
                         "unit": "TFLOP/s", "frac": ach / peaks["tc_sustained"], "traffic": traffic}
         else:
-            ach = c["bytes"] / (c["ms"] * 1e-3) / 1e9
-            roofline = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s",
-                        "frac": ach / peaks["hbm"], "traffic": traffic}
+            # SIMT classes: the bound is whichever ideal time is longer, HBM bytes at the measured
+            # copy bandwidth or FP32 flops at the FP32 SIMT peak (148 SMs x 128 FP32 lanes x 2 flop
+            # x the max SM clock -- DESIGN.md section 6); the whole-leaf kernel is FP32-bound
+            t_hbm = c["bytes"] / (peaks["hbm"] * 1e9)
+            t_alu = c["flops"] / (fp32_peak_tflops() * 1e12)
+            if t_alu > t_hbm:
+                ach = c["flops"] / (c["ms"] * 1e-3) / 1e12
+                roofline = {"bound": "alu", "achieved": ach, "peak": fp32_peak_tflops(),
+                            "unit": "TFLOP/s", "frac": ach / fp32_peak_tflops(), "traffic": traffic,
+                            "hbm_achieved_gbs": c["bytes"] / (c["ms"] * 1e-3) / 1e9}
+            else:
+                ach = c["bytes"] / (c["ms"] * 1e-3) / 1e9
+                roofline = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s",
+                            "frac": ach / peaks["hbm"], "traffic": traffic}
         roofline.update({"kernel": dom, "share_of_step": c["ms"] / tot,
                          "launches_per_step": c["launches"], "ms_per_launch": per_launch_ms,
-                         "peak_source": peaks["src"] + (" bf16 sustained (fp16 dense = bf16 rate)"
-                                                        if dom in ("k3_tn", "k4_nn") else " hbm_gbs")})
+                         "peak_source": (peaks["src"] + " bf16 sustained (fp16 dense = bf16 rate)"
+                                         if dom in ("k3_tn", "k4_nn") else
+                                         "derived FP32 SIMT peak: 148 SMs x 128 lanes x 2 x 1965 MHz"
+                                         if roofline["bound"] == "alu" else peaks["src"] + " hbm_gbs")})
         classes = {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
                        "share": round(v["ms"] / tot, 4),
                        "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 2),
