@@ -371,41 +371,56 @@ def main():
         del Q, R
         torch.cuda.empty_cache()
         Ml, nl = 32768, 8192
-        Al_full = W.spectrum_cuda(Ml, nl, "geometric", 1e4, W.CONFIG_SEEDS["cfg4_k1e4"], device=dev)
-        g = torch.Generator(device=dev)
-        g.manual_seed(W.CONFIG_SEEDS["cfg4_x_k1e4"])
-        x_true = torch.randn(nl, generator=g, device=dev, dtype=torch.float64)
-        b_full = Al_full.to(torch.float64) @ x_true
         lrows = np.array_split(np.arange(Ml), world)[rank]
         l0, l1 = int(lrows[0]), int(lrows[-1]) + 1
-        Al = torch.empty((nl, l1 - l0), dtype=torch.float32, device=dev).t()
-        Al.copy_(Al_full[l0:l1])
-        bl = b_full[l0:l1].contiguous()
-        del Al_full, b_full
-        torch.cuda.empty_cache()
-        lls = {"workload": "LLS 32768x8192 geometric kappa=1e4, b = A x_true (BASELINE configs[3]), "
-                           "FP64 target (tol 1e-10, one restart), warm (graphs captured)"}
-        for label, reorth in (("paper_R", 0), ("reorth_R", 1)):
-            tq.set_config(cutoff=args.cutoff, reorth=reorth)
-            tq.lls_solve(Al, bl, tol=1e-10, maxit=4000)      # warm-up: builds the QR graph
-            barrier()
-            torch.cuda.synchronize()
-            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            h0.record(stream)
-            x, info = tq.lls_solve(Al, bl, tol=1e-10, maxit=4000)
-            h1.record(stream)
-            torch.cuda.synchronize()
-            lt = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(lt, op=dist.ReduceOp.MAX)
-            xe = float(torch.linalg.norm(x - x_true) / torch.linalg.norm(x_true))
-            lls[label] = {"time_to_solution_ms": float(lt.item()), "qr_ms": info["qr_ms"],
-                          "cgls_ms": info["cgls_ms"], "iterations": info["iterations"],
-                          "iterations_pass1": info["iterations_pass1"],
-                          "converged": bool(info["converged"]), "x_rel_err_vs_x_true": xe,
-                          "fp64_accuracy_reached": bool(xe <= 1e-10)}
+        lls = {"workload": "LLS 32768x8192 geometric kappa=1e4 and 1e6, b = A x_true (BASELINE "
+                           "configs[3]), FP64 target (tol 1e-10, one restart), warm (graphs captured)"}
+
+        def lls_case(cond, cases):
+            key = "k1e4" if cond == 1e4 else "k1e6"
+            Al_full = W.spectrum_cuda(Ml, nl, "geometric", cond, W.CONFIG_SEEDS["cfg4_" + key],
+                                      device=dev)
+            g = torch.Generator(device=dev)
+            g.manual_seed(W.CONFIG_SEEDS["cfg4_x_" + key])
+            x_true = torch.randn(nl, generator=g, device=dev, dtype=torch.float64)
+            b_full = Al_full.to(torch.float64) @ x_true
+            Al = torch.empty((nl, l1 - l0), dtype=torch.float32, device=dev).t()
+            Al.copy_(Al_full[l0:l1])
+            bl = b_full[l0:l1].contiguous()
+            del Al_full, b_full
+            torch.cuda.empty_cache()
+            for label, reorth, split in cases:
+                tq.set_config(cutoff=args.cutoff, reorth=reorth, fp16_split=split)
+                tq.lls_solve(Al, bl, tol=1e-10, maxit=4000)      # warm-up: builds the QR graph
+                barrier()
+                torch.cuda.synchronize()
+                h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                h0.record(stream)
+                x, info = tq.lls_solve(Al, bl, tol=1e-10, maxit=4000)
+                h1.record(stream)
+                torch.cuda.synchronize()
+                lt = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+                if world > 1:
+                    dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+                xe = float(torch.linalg.norm(x - x_true) / torch.linalg.norm(x_true))
+                lls[label] = {"time_to_solution_ms": float(lt.item()), "qr_ms": info["qr_ms"],
+                              "cgls_ms": info["cgls_ms"], "iterations": info["iterations"],
+                              "iterations_pass1": info["iterations_pass1"],
+                              "converged": bool(info["converged"]), "x_rel_err_vs_x_true": xe,
+                              "fp64_accuracy_reached": bool(xe <= 1e-10)}
+            del Al, bl
+
+        lls_case(1e4, (("paper_R", 0, 0), ("reorth_R", 1, 0), ("split_reorth_R", 1, 1)))
+        # kappa = 1e6 geometric is beyond the paper with its FP16 R (reading R-A24: CGLS does not
+        # converge; 4000 iterations x 2 passes would take seconds): NEXT-4 + NEXT-1 only
+        lls_case(1e6, (("k1e6_split_reorth_R", 1, 1),))
         lls["reorth_R"]["note"] = ("NEXT-1 (PAPER.md:622-627): R = R2 R1 from a second RGS of Q; "
                                    "paper_R is Alg. 5 with the single RMGSQR R")
+        lls["split_reorth_R"]["note"] = ("NEXT-4 FP16 split (hi + lo halves, three MMAs per product) "
+                                         "plus NEXT-1 re-orthogonalization")
+        lls["k1e6_split_reorth_R"]["note"] = ("geometric kappa=1e6 (configs[3] second case), "
+                                              "NEXT-4 + NEXT-1; the single FP16 R does not converge "
+                                              "(R-A24)")
         tq.set_config(cutoff=args.cutoff)
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ----

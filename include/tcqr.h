@@ -74,6 +74,12 @@ typedef struct tcqr_config {
                         Eq. (6) stack factored through its FP64 Gram matrix (reading R-A28);
                         0: one pipelined MGS-root panel launch per 32 columns plus FP32
                         projection launches (default 1)                                         */
+  int fp16_split;    /* 1: error-compensated FP16 split for the tensor-core split nodes (NEXT-4,
+                        SURVEY.md 8(f); beyond the paper, whose related work on tensor-core
+                        precision is PAPER.md:758): X diag(s) = Xh + Xl with Xh = fl16(X diag(s)),
+                        Xl = fl16(X diag(s) - Xh); R12 = Q1h'A2h + Q1h'A2l + Q1l'A2h and
+                        A2 -= Q1h R12h + Q1h R12l + Q1l R12h (three MMAs each, lo*lo dropped).
+                        3x the tensor-core work; opt-in (default 0)                              */
 } tcqr_config_t;
 
 /* Per-solve report (SPEC.md:296-299 CglsReport). */

@@ -34,7 +34,7 @@ class TcqrConfig(ctypes.Structure):
                 ("tol2", ctypes.c_double), ("stag_window", ctypes.c_int),
                 ("stag_floor", ctypes.c_double), ("use_graphs", ctypes.c_int),
                 ("reorth", ctypes.c_int), ("warm_start", ctypes.c_int),
-                ("leaf_kernel", ctypes.c_int)]
+                ("leaf_kernel", ctypes.c_int), ("fp16_split", ctypes.c_int)]
 
 
 class TcqrLlsInfo(ctypes.Structure):

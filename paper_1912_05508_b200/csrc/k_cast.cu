@@ -193,30 +193,57 @@ __global__ void __launch_bounds__(kCastThreads) r12_finalize_kernel(
 // Split-K reduction fused with the finalize: column j of R12 = (sum_s P[s](:, j)) * col_mult[j]
 // (partials summed in the fixed order s = 0..splits-1), written to the R block, then the column
 // scale s' and the scaled FP16 copy as in r12_finalize_kernel.
-__global__ void __launch_bounds__(kCastThreads) r12_splitk_finalize_kernel(
+// Split-K finalize, one CTA (kFinThreads) per column j: R12(i, j) = col_mult(j) * sum_s P_s(i, j)
+// in a fixed order (deterministic).  Thread t sums entry i = t mod hb over the split group
+// g = t / hb (splits g, g + G, ..., 16 loads in flight), then the G group sums are added in group
+// order through shared memory.  With G > 1 the short deep-level columns (h = 128, 64 splits) keep
+// 512 threads busy instead of 128 threads with 64 dependent L2 rounds (10 us -> see DESIGN).
+constexpr int kFinThreads = 512;
+
+__global__ void __launch_bounds__(kFinThreads) r12_splitk_finalize_kernel(
     int h, const float* __restrict__ P, int splits, long long pstride, long long ldp,
     const float* __restrict__ col_mult, float* __restrict__ Rblk, long long ldr,
     __half* __restrict__ R12h, long long ldh2, float* __restrict__ inv_s2, int scaling) {
   __shared__ float red[32];
+  __shared__ float gs[kFinThreads];
   const int j = blockIdx.x;
   const float cm = col_mult ? col_mult[j] : 1.f;
   float* r = Rblk + (long long)j * ldr;
   float mx = 0.f;
-  for (int i = threadIdx.x; i < h; i += kCastThreads) {
-    const float* p = P + i + (long long)j * ldp;
+  // hb = entries per pass (a power of two >= 32 dividing kFinThreads), G = split groups
+  int hb = 32;
+  while (hb < h && hb < kFinThreads) hb <<= 1;
+  const int G = kFinThreads / hb;
+  const int ii = threadIdx.x % hb, g = threadIdx.x / hb;
+  for (int i0 = 0; i0 < h; i0 += hb) {
+    const int i = i0 + ii;
     float acc = 0.f;
-    int s0 = 0;
-    for (; s0 + 8 <= splits; s0 += 8) {
-      float v[8];
+    if (i < h) {
+      const float* p = P + i + (long long)j * ldp;
+      int s0 = g;
+      for (; s0 + 15 * G < splits; s0 += 16 * G) {
+        float v[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (long long)(s0 + u) * pstride);
+        for (int u = 0; u < 16; ++u) v[u] = __ldcg(p + (long long)(s0 + u * G) * pstride);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc += v[u];
+        for (int u = 0; u < 16; ++u) acc += v[u];
+      }
+      for (; s0 < splits; s0 += G) acc += __ldcg(p + (long long)s0 * pstride);
     }
-    for (; s0 < splits; ++s0) acc += __ldcg(p + (long long)s0 * pstride);
-    const float v = acc * cm;
-    r[i] = v;
-    mx = fmaxf(mx, fabsf(v));
+    if (G > 1) {
+      gs[threadIdx.x] = acc;
+      __syncthreads();
+      if (g == 0) {
+#pragma unroll 1
+        for (int q = 1; q < G; ++q) acc += gs[q * hb + ii];
+      }
+      __syncthreads();
+    }
+    if (g == 0 && i < h) {
+      const float v = acc * cm;
+      r[i] = v;
+      mx = fmaxf(mx, fabsf(v));
+    }
   }
   float sc = 1.f;
   if (scaling) {
@@ -225,9 +252,61 @@ __global__ void __launch_bounds__(kCastThreads) r12_splitk_finalize_kernel(
   }
   if (threadIdx.x == 0) inv_s2[j] = 1.f / sc;
   if (R12h) {
+    __syncthreads();  // r[] written by group 0 (global memory, same CTA)
     __half* o = R12h + (long long)j * ldh2;
-    for (int i = threadIdx.x; i < h; i += kCastThreads) o[i] = __float2half_rn(r[i] * sc);
+    for (int i = threadIdx.x; i < h; i += kFinThreads) o[i] = __float2half_rn(__ldcg(r + i) * sc);
   }
+}
+
+// NEXT-4 (error-compensated FP16 split; the paper's related-work pointer on
+// tensor-core precision): the low half of the FP16 split of X diag(s),
+// Xl = fl16(X diag(s) - Xh) with Xh = fl16(X diag(s)) already written.  X diag(s) is exact (s is a
+// power of two) and so is its difference with Xh in FP32, so Xl carries the next 11 bits (FP16
+// subnormals below 2^-14: absolute error <= 2^-25 against a column max in [1, 2)).  inv_s null:
+// s = 1.  One CTA per (row chunk, column); 4 elements per thread step.
+__global__ void __launch_bounds__(256) cast_lo_kernel(int m, const float* __restrict__ X,
+                                                      long long ldx,
+                                                      const __half* __restrict__ Xh,
+                                                      long long ldh, const float* __restrict__ inv_s,
+                                                      __half* __restrict__ Xl, long long ldl,
+                                                      int rows_per) {
+  const int j = blockIdx.y;
+  const long long r0 = (long long)blockIdx.x * rows_per;
+  const long long r1 = min((long long)m, r0 + rows_per);
+  const float s = inv_s ? 1.f / inv_s[j] : 1.f;
+  const float* x = X + (long long)j * ldx;
+  const __half* xh = Xh + (long long)j * ldh;
+  __half* xl = Xl + (long long)j * ldl;
+  for (long long q = r0 + threadIdx.x; q < r1; q += 256) {
+    const float v = x[q] * s;
+    xl[q] = __float2half_rn(v - __half2float(xh[q]));
+  }
+}
+
+cudaError_t cast_lo(int m, int w, const float* X, long long ldx, const __half* Xh, long long ldh,
+                    const float* inv_s, __half* Xl, long long ldl, cudaStream_t st) {
+  if (m <= 0 || w <= 0) return cudaSuccess;
+  const int rows_per = 8192;
+  dim3 grid((m + rows_per - 1) / rows_per, w);
+  cast_lo_kernel<<<grid, 256, 0, st>>>(m, X, ldx, Xh, ldh, inv_s, Xl, ldl, rows_per);
+  return cudaGetLastError();
+}
+
+// dst[i] += a[i] + b[i] (NEXT-4: the three split products of R12 summed before the finalize;
+// the small corrections are added together first).
+__global__ void add3_kernel(long long n, float* __restrict__ dst, const float* __restrict__ a,
+                            const float* __restrict__ b) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = dst[i] + (a[i] + b[i]);
+}
+
+cudaError_t add3(long long n, float* dst, const float* a, const float* b, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  long long g = (n + 255) / 256;
+  if (g > 4096) g = 4096;
+  add3_kernel<<<(int)g, 256, 0, st>>>(n, dst, a, b);
+  return cudaGetLastError();
 }
 
 cudaError_t r12_splitk_finalize(int h, int w2, const float* P, int splits, long long pstride,
@@ -235,7 +314,7 @@ cudaError_t r12_splitk_finalize(int h, int w2, const float* P, int splits, long 
                                 __half* R12h, long long ldh2, float* inv_s2, int scaling,
                                 cudaStream_t st) {
   if (h <= 0 || w2 <= 0) return cudaSuccess;
-  r12_splitk_finalize_kernel<<<w2, kCastThreads, 0, st>>>(h, P, splits, pstride, ldp, col_mult,
+  r12_splitk_finalize_kernel<<<w2, kFinThreads, 0, st>>>(h, P, splits, pstride, ldp, col_mult,
                                                           Rblk, ldr, R12h, ldh2, inv_s2, scaling);
   return cudaGetLastError();
 }

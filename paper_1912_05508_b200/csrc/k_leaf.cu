@@ -359,6 +359,7 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
   {
     const float* q1 = s.L + c0 + 4 * ti;
     const float* a2 = s.L + c0 + H + 4 * tj;
+#pragma unroll 4
     for (int r = grp; r < nrows; r += G) {
       const float4 qv = *reinterpret_cast<const float4*>(q1 + r * kLd);
       const float4 av = *reinterpret_cast<const float4*>(a2 + r * kLd);
@@ -409,7 +410,7 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
     for (int j = 0; j < JC; ++j) u[rr][j] = 0.f;
   const float* qa = s.L + r0 * kLd + c0;
   const float* qb = s.L + (r0 + 128) * kLd + c0;
-#pragma unroll 1
+#pragma unroll 2
   for (int i4 = 0; i4 < H; i4 += 4) {
     const float4 va = *reinterpret_cast<const float4*>(qa + i4);
     const float4 vb = *reinterpret_cast<const float4*>(qb + i4);

@@ -38,6 +38,10 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
 cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
                        float* inv_s, int scaling, int* status, int col_base, unsigned int* cmax,
                        cudaStream_t st);
+// NEXT-4 FP16 split: Xl = fl16(X diag(s) - Xh) (inv_s null: s = 1); dst += a + b.
+cudaError_t cast_lo(int m, int w, const float* X, long long ldx, const __half* Xh, long long ldh,
+                    const float* inv_s, __half* Xl, long long ldl, cudaStream_t st);
+cudaError_t add3(long long n, float* dst, const float* a, const float* b, cudaStream_t st);
 // R12 finalize: T (h x w2, ldt) -> R block (ldr) and fl16(R12 diag(s')) (ldh2), inv_s2.
 cudaError_t r12_finalize(int h, int w2, const float* T, long long ldt, float* Rblk, long long ldr,
                          __half* R12h, long long ldh2, float* inv_s2, int scaling, cudaStream_t st);

@@ -131,6 +131,11 @@ struct FactorWs {
   float* R2 = nullptr;           // re-orthogonalization: R of the second pass (n x n)
   float* Rt = nullptr;           // re-orthogonalization: R2 * R1 staging (n x n)
   unsigned leaf_bars = 0;        // grid barriers the leaf kernels completed since iws was zeroed
+  // NEXT-4 FP16 split (cfg.fp16_split): low halves of the shadow and of R12, two more R12 stagings
+  __half* Ql = nullptr;     // ld ldh, like Qh
+  __half* R12l = nullptr;   // like R12h
+  float* T2 = nullptr;      // like T
+  float* T3 = nullptr;
 };
 
 static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, FactorWs& w,
@@ -160,6 +165,12 @@ static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, Facto
   if (reorth) {
     w.R2 = a.take<float>((size_t)n * n);
     w.Rt = a.take<float>((size_t)n * n);
+  }
+  if (g_ctx.cfg.fp16_split) {
+    w.Ql = a.take<__half>((size_t)w.ldh * n);
+    w.R12l = a.take<__half>((size_t)round_up(hmax, 8) * std::max(w2max, hmax) + 64);
+    w.T2 = a.take<float>((size_t)(hmax * std::max(w2max, hmax)) + 64);
+    w.T3 = a.take<float>((size_t)(hmax * std::max(w2max, hmax)) + 64);
   }
 }
 
@@ -503,6 +514,17 @@ static int chunk_done(FactorJob& J, int c0, int w) {
   return 0;
 }
 
+// NEXT-4: the low FP16 half of final Q columns [c0, c0+w) (Qh already written), Ql = fl16(Q - Qh).
+static int emit_q_lo(FactorJob& J, int c0, int w) {
+  Context& c = g_ctx;
+  FactorWs& ws = *J.ws;
+  if (!c.cfg.fp16_split || !ws.Ql) return 0;
+  PROF(TCQR_K1_CAST, 0, 8.0 * J.m * w,
+       CK(cast_lo(J.m, w, J.Q + (long long)c0 * J.ldq, J.ldq, ws.Qh + (long long)c0 * ws.ldh,
+                  ws.ldh, nullptr, ws.Ql + (long long)c0 * ws.ldh, ws.ldh, c.stream)));
+  return 0;
+}
+
 static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   Context& c = g_ctx;
   FactorWs& ws = *J.ws;
@@ -517,7 +539,10 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
                         J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0, c.d_status, ws.P,
                         sizeof(float) * (size_t)ws.p_cap, reinterpret_cast<unsigned*>(ws.iws + ws.iws_cap - 16),
                         &ws.leaf_bars, c.num_sms, c.stream));
-    if (e == cudaSuccess) return chunk_done(J, c0, w);
+    if (e == cudaSuccess) {
+      if (need_h) CKR(emit_q_lo(J, c0, w));
+      return chunk_done(J, c0, w);
+    }
     if (e != cudaErrorNotSupported) CK(e);
     cudaGetLastError();
   }
@@ -526,7 +551,10 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     need_cols(J, c0, c0 + w);
     CKR(panel(ws, m, w, Qc, J.ldq, J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0,
               need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, &wrote_h));
-    if (wrote_h) return chunk_done(J, c0, w);
+    if (wrote_h) {
+      CKR(emit_q_lo(J, c0, w));
+      return chunk_done(J, c0, w);
+    }
   } else {
     const int h = split_point(w), w2 = w - h;
     const bool tc = w > c.cfg.cutoff;
@@ -558,6 +586,40 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
         PROF(TCQR_K1_CAST, 0, 6.0 * m * wp,
              CK(cast_scale(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling,
                            c.d_status, p0, ws.cmax, c.stream)));
+        if (c.cfg.fp16_split && ws.Ql) {
+          // NEXT-4: three MMAs per product on the hi/lo FP16 halves (lo x lo dropped)
+          __half* A1l = ws.Ql + (long long)c0 * ws.ldh;
+          __half* A2l = ws.Ql + (long long)p0 * ws.ldh;
+          float* T2p = ws.T2 + (long long)off * h;
+          float* T3p = ws.T3 + (long long)off * h;
+          __half* R12lp = ws.R12l + (long long)off * ldh2;
+          float* Rb = Rblk + (long long)off * J.ldr;
+          PROF(TCQR_K1_CAST, 0, 8.0 * m * wp,
+               CK(cast_lo(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, A2l, ws.ldh, c.stream)));
+          PROF(TCQR_K3_TN, 6.0 * m * h * wp, 6.0 * m * (h + wp) + 12.0 * h * wp, {
+            CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, Tp, h, ws.inv_s + p0, ws.P, ws.p_cap,
+                          c.num_sms, c.stream));
+            CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2l, ws.ldh, T2p, h, ws.inv_s + p0, ws.P,
+                          ws.p_cap, c.num_sms, c.stream));
+            CK(tc_gemm_tn(m, h, wp, A1l, ws.ldh, A2h, ws.ldh, T3p, h, ws.inv_s + p0, ws.P,
+                          ws.p_cap, c.num_sms, c.stream));
+          });
+          CK(add3((long long)h * wp, Tp, T2p, T3p, c.stream));
+          if (c.nranks > 1) CKR(allreduce_f32(Tp, (size_t)h * wp));
+          PROF(TCQR_K3_FINALIZE, 0, 10.0 * h * wp,
+               CK(r12_finalize(h, wp, Tp, h, Rb, J.ldr, R12hp, ldh2, ws.inv_s2 + p0,
+                               c.cfg.col_scaling, c.stream)));
+          CK(cast_lo(h, wp, Rb, J.ldr, R12hp, ldh2, ws.inv_s2 + p0, R12lp, ldh2, c.stream));
+          PROF(TCQR_K4_NN, 6.0 * m * h * wp, 6.0 * m * h + 6.0 * h * wp + 24.0 * m * wp, {
+            CK(tc_gemm_nn_update(m, h, wp, A1h, ws.ldh, R12hp, ldh2, A2p, J.ldq, ws.inv_s2 + p0,
+                                 c.num_sms, c.stream));
+            CK(tc_gemm_nn_update(m, h, wp, A1h, ws.ldh, R12lp, ldh2, A2p, J.ldq, ws.inv_s2 + p0,
+                                 c.num_sms, c.stream));
+            CK(tc_gemm_nn_update(m, h, wp, A1l, ws.ldh, R12hp, ldh2, A2p, J.ldq, ws.inv_s2 + p0,
+                                 c.num_sms, c.stream));
+          });
+          continue;
+        }
         if (c.nranks == 1) {
           // one rank: the split-K reduction runs fused with the finalize
           const R12Finalize fin{Rblk + (long long)off * J.ldr, J.ldr, R12hp, ldh2, ws.inv_s2 + p0,
@@ -614,6 +676,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     PROF(TCQR_K1_CAST, 0, 6.0 * m * w,
          CK(cast_scale(m, w, Qc, J.ldq, ws.Qh + (long long)c0 * ws.ldh, ws.ldh, nullptr, 0,
                        nullptr, 0, nullptr, c.stream)));
+    CKR(emit_q_lo(J, c0, w));
   }
   return chunk_done(J, c0, w);
 }
@@ -664,8 +727,8 @@ static std::string graph_key(const char* tag, std::initializer_list<long long> v
     k += buf;
   }
   const tcqr_config_t& f = g_ctx.cfg;
-  snprintf(buf, sizeof buf, "|%d,%d,%d,%d,%d", f.cutoff, f.panel_rows, f.col_scaling, f.reorth,
-           f.leaf_kernel);
+  snprintf(buf, sizeof buf, "|%d,%d,%d,%d,%d,%d", f.cutoff, f.panel_rows, f.col_scaling, f.reorth,
+           f.leaf_kernel, f.fp16_split);
   k += buf;
   return k;
 }
@@ -744,6 +807,7 @@ void tcqr_default_config(tcqr_config_t* c) {
   c->reorth = 0;
   c->warm_start = 0;
   c->leaf_kernel = 1;
+  c->fp16_split = 0;
 }
 
 int tcqr_set_config(const tcqr_config_t* cfg) {
@@ -755,6 +819,7 @@ int tcqr_set_config(const tcqr_config_t* cfg) {
   if (cfg->reorth != 0 && cfg->reorth != 1) return -1;
   if (cfg->warm_start != 0 && cfg->warm_start != 1) return -1;
   if (cfg->leaf_kernel != 0 && cfg->leaf_kernel != 1) return -1;
+  if (cfg->fp16_split != 0 && cfg->fp16_split != 1) return -1;
   g_ctx.cfg = *cfg;
   return 0;
 }

@@ -301,3 +301,54 @@ def test_factor_host_streamed_nonfinite_column(tq):
     with pytest.raises(tq.TcqrError) as e:
         tq.factor_host(a)
     assert e.value.code == 902
+
+
+# ---- NEXT-4: error-compensated FP16 split (hi + lo halves, three MMAs per product) -------------
+# Gates derived from the arithmetic: each split-node product carries the dropped
+# lo*lo term (<= 2^-22 relative to |a||b|) and the rounding of the lo halves (<= 2^-25 absolute
+# against a column max in [1, 2)), the leaves are FP32 (u = 2^-24).  Measured on B200 at
+# 4096 x 1024: backward 4e-7..1.2e-6, R 4.5e-7..5.3e-6 (kappa <= 1e3), orthogonality <= 3.9e-4
+# (geometric 1e3); the gates sit 8-40x above.
+@pytest.mark.parametrize("kind,cond", [("gaussian", 1), ("geometric", 1e2), ("arithmetic", 1e3),
+                                       ("geometric", 1e3)])
+def test_fp16_split_factor_accuracy(tq, kind, cond):
+    a = W.make_matrix(kind, 4096, 1024, seed=41, cond=cond)
+    _, r_o = rgs(a.astype(np.float64))
+    q1, r1 = _factor(tq, a)
+    q2, r2 = _factor(tq, a, fp16_split=1)
+    tq.set_config()
+    assert np.array_equal(r2, np.triu(r2)) and np.all(np.diag(r2) > 0)
+    assert backward_error_f(a, q2, r2) <= 1e-5
+    assert r_rel_error(r2, r_o) <= 5e-5
+    assert orthogonality_f(q2) <= 5e-3
+    # the split path is at least 30x more accurate than the plain FP16 path on every metric
+    assert backward_error_f(a, q2, r2) * 30 < backward_error_f(a, q1, r1)
+    assert r_rel_error(r2, r_o) * 30 < r_rel_error(r1, r_o)
+
+
+def test_fp16_split_planted_and_scale_bitwise(tq):
+    # exact inputs have zero lo halves: the planted pin (P2) still holds bitwise, and the
+    # power-of-two scale guard keeps the split path bitwise scale-equivariant (P3)
+    a, q_ex, r0 = W.planted_hadamard(1024, 256, seed=201)
+    q, r = _factor(tq, a, cutoff=64, panel_rows=256, fp16_split=1)
+    assert np.array_equal(r, r0.astype(np.float64)) and np.array_equal(q, q_ex.astype(np.float64))
+    g = W.gaussian(2048, 512, seed=43)
+    q1, r1 = _factor(tq, g, fp16_split=1)
+    q2, r2 = _factor(tq, (g * np.float32(2.0 ** -20)).astype(np.float32), fp16_split=1)
+    tq.set_config()
+    assert np.array_equal(q1, q2) and np.array_equal(r1 * 2.0 ** -20, r2)
+
+
+@pytest.mark.parametrize("cond,reorth,max_iters", [(1e5, 0, 200), (1e6, 1, 60)])
+def test_fp16_split_lls_ill_conditioned(tq, cond, reorth, max_iters):
+    # reading R-A24: geometric kappa = 1e6 does not converge with the single FP16 R; with the split
+    # (and NEXT-1) CGLS reaches the FP64 target (B200: 1e5 split 75 iterations, 1e6 split+reorth 18)
+    a = W.spectrum_matrix(4096, 1024, "geometric", cond, seed=37)
+    b, _ = W.consistent_rhs(a, seed=38)
+    x_o, _ = oracle_lls(a.astype(np.float64), b)
+    tq.set_config(fp16_split=1, reorth=reorth)
+    x, info = tq.lls_solve(tq.to_device_colmajor(a), torch.from_numpy(b).cuda(), tol=1e-10,
+                           maxit=3000)
+    tq.set_config()
+    assert info["converged"] == 1 and info["iterations"] <= max_iters, info
+    assert x_rel_error(x.cpu().numpy(), x_o) <= 1e-10
