@@ -154,9 +154,10 @@ def run_reference(args, wl):
 
 def _streamed_r_bytes(n, cutoff):
     """Bytes of R the streamed tcqr_factor_host copies back: for each column chunk (the subtrees
-    of width <= max(n/8, 2*cutoff), tcqr.cu plan_chunks) the rows [0, chunk end); the zero rows
-    below are written on the host."""
-    target = max(n // 8, 1)
+    of width <= max(n/div, 2*cutoff), div = TCQR_STREAM_DIV or 16, tcqr.cu plan_chunks) the rows
+    [0, chunk end); the zero rows below are written on the host."""
+    div = int(os.environ.get("TCQR_STREAM_DIV", "16") or 16)
+    target = max(n // max(div, 1), 1)
     chunks = []
 
     def plan(c0, w):

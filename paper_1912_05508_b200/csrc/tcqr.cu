@@ -1119,7 +1119,14 @@ static int factor_host_streamed(int m, int n, const float* A, long long lda, flo
   FactorWs ws;
   plan_factor_ws(ar, m, n, c.nranks, ws, false);
   StreamPlan sp;
-  plan_chunks(0, n, std::max(n / 8, 1), c.cfg.cutoff, sp);
+  // chunk width: finer chunks shorten the pipeline head (first H2D) and tail (last D2H) and send
+  // less of R's zero lower part; TCQR_STREAM_DIV overrides the divisor (default 16; 8..64 measured within 2%: the e2e is PCIe-bound, tools/e2e_chunks.py)
+  static int div = -1;
+  if (div < 0) {
+    const char* e = getenv("TCQR_STREAM_DIV");
+    div = (e && atoi(e) > 0) ? atoi(e) : 16;
+  }
+  plan_chunks(0, n, std::max(n / div, 1), c.cfg.cutoff, sp);
   const size_t nc = sp.a.size();
   sp.ev_in.resize(nc);
   sp.ev_fin.resize(nc);
