@@ -352,3 +352,29 @@ def test_fp16_split_lls_ill_conditioned(tq, cond, reorth, max_iters):
     tq.set_config()
     assert info["converged"] == 1 and info["iterations"] <= max_iters, info
     assert x_rel_error(x.cpu().numpy(), x_o) <= 1e-10
+
+
+# ---- K2S: streamed panel for m > 32768 rows (one warp per 64-row block, Gram-factored stack) ----
+@pytest.mark.parametrize("m,n,cutoff", [(70001, 128, 128), (65600, 96, 32)])
+def test_streamed_panel_gates(tq, m, n, cutoff):
+    a = W.gaussian(m, n, seed=m % 1000 + n)
+    q, r = _factor(tq, a, cutoff=cutoff)
+    tq.set_config()
+    _, r_o = rgs(a.astype(np.float64))
+    be, orth, re = _gates(a, q, r, r_o)
+    if n <= cutoff:   # leaves only: FP32 accuracy
+        assert be < 1e-5 and re < 1e-4 and orth < 1e-5
+
+
+def test_streamed_panel_planted_bitwise_and_breakdown(tq):
+    # 65536 = 4^8 rows, 64 = 4^3 rows per block, 1024 = 4^5 blocks: every norm exact (P2)
+    a, qt, r0 = W.planted_hadamard(65536, 128, seed=202)
+    q, r = _factor(tq, a, cutoff=64)
+    assert np.array_equal(r, r0)
+    assert np.array_equal(q, qt)
+    b = W.gaussian(40000, 64, seed=5)
+    b[:, 37] = 0.0
+    tq.set_config()
+    with pytest.raises(tq.TcqrError) as e:
+        tq.factor(tq.to_device_colmajor(b))
+    assert e.value.code == 38
