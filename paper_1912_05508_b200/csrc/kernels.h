@@ -38,15 +38,6 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
 cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
                        float* inv_s, int scaling, int* status, int col_base, unsigned int* cmax,
                        cudaStream_t st);
-// K2S (k_panels.cu): one 32-column CAQR panel of m > 32768 rows in one cooperative launch,
-// one warp per 64-row block, the stack factored through its FP64 Gram (reading R-A28).
-// Rbs: >= panels_scratch_floats(m) floats; scratch: >= 8 * (1025 * num_sms) bytes; bar: a zeroed
-// counter, bar_seq its host-side arrival count.
-size_t panels_scratch_floats(int m);
-cudaError_t panel_stream(int m, int pw, float* X, long long ldx, __half* Xh, long long ldh,
-                         float* R, long long ldr, int col0, int* status, float* Rbs,
-                         size_t rbs_floats, void* scratch, size_t scratch_bytes, unsigned* bar,
-                         unsigned* bar_seq, int num_sms, cudaStream_t st);
 // NEXT-4 FP16 split: Xl = fl16(X diag(s) - Xh) (inv_s null: s = 1); dst += a + b.
 cudaError_t cast_lo(int m, int w, const float* X, long long ldx, const __half* Xh, long long ldh,
                     const float* inv_s, __half* Xl, long long ldl, cudaStream_t st);

@@ -131,7 +131,6 @@ struct FactorWs {
   float* R2 = nullptr;           // re-orthogonalization: R of the second pass (n x n)
   float* Rt = nullptr;           // re-orthogonalization: R2 * R1 staging (n x n)
   unsigned leaf_bars = 0;        // grid barriers the leaf kernels completed since iws was zeroed
-  unsigned pans_bars = 0;        // grid-barrier arrivals of the streamed panel kernel (K2S)
   // NEXT-4 FP16 split (cfg.fp16_split): low halves of the shadow and of R12, two more R12 stagings
   __half* Ql = nullptr;     // ld ldh, like Qh
   __half* R12l = nullptr;   // like R12h
@@ -420,20 +419,6 @@ static int panel(FactorWs& ws, int m, int w, float* X, long long ldx, float* Rou
   *wrote_h = false;
   if (c.nranks <= 1) {
     cudaError_t e = cudaErrorNotSupported;
-    if (m > 32768 && c.cfg.leaf_kernel) {
-      // K2S: too tall for the pipelined panel; one warp per 64-row block, rows streamed
-      PROF(TCQR_K2_MGS, 4.0 * m * w * w, 16.0 * m * w + (Xh ? 2.0 * m * w : 0.0),
-           e = panel_stream(m, w, X, ldx, Xh, ws.ldh, Rout, ldr, col0, c.d_status, ws.pws,
-                            (size_t)ws.pws_cap, ws.P, sizeof(float) * (size_t)ws.p_cap,
-                            reinterpret_cast<unsigned*>(ws.iws + ws.iws_cap - 24), &ws.pans_bars,
-                            c.num_sms, c.stream));
-      if (e == cudaSuccess) {
-        *wrote_h = Xh != nullptr;
-        return 0;
-      }
-      if (e != cudaErrorNotSupported) CK(e);
-      cudaGetLastError();
-    }
     PROF(TCQR_K2_MGS, 4.0 * m * w * w, 8.0 * m * w + (Xh ? 2.0 * m * w : 0.0),
          e = panel_pipe(m, w, X, ldx, Xh, ws.ldh, c.cfg.panel_rows, Rout, ldr, 1, c.d_status,
                         col0, ws.pipeR, ws.pipeS, c.num_sms, c.stream));
@@ -704,7 +689,6 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
   CK(cudaMemsetAsync(R, 0, sizeof(float) * (size_t)n * n, c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
   ws.leaf_bars = 0;
-  ws.pans_bars = 0;
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   PROF(TCQR_COPY, 0, 8.0 * m * n, CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream)));
   FactorJob J{m, n, Q, (long long)m, R, (long long)n, &ws};
@@ -1171,7 +1155,6 @@ static int factor_host_streamed(int m, int n, const float* A, long long lda, flo
   CK(cudaMemsetAsync(dR, 0, sizeof(float) * (size_t)n * n, c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
   ws.leaf_bars = 0;
-  ws.pans_bars = 0;
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   FactorJob J{m, n, dQ, (long long)m, dR, (long long)n, &ws, &sp};
   rc = rgs(J, 0, n, n > c.cfg.cutoff);
@@ -1344,7 +1327,6 @@ int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
   ws.leaf_bars = 0;
-  ws.pans_bars = 0;
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   bool wrote_h = false;
   int rc = panel(ws, (int)m, (int)w, X, ldx, R, ldr, 0, nullptr, &wrote_h);

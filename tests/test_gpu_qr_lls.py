@@ -354,9 +354,9 @@ def test_fp16_split_lls_ill_conditioned(tq, cond, reorth, max_iters):
     assert x_rel_error(x.cpu().numpy(), x_o) <= 1e-10
 
 
-# ---- K2S: streamed panel for m > 32768 rows (one warp per 64-row block, Gram-factored stack) ----
+# ---- panels taller than the whole-leaf kernel holds (m > 148 * 256: the K2 panel path) ----------
 @pytest.mark.parametrize("m,n,cutoff", [(70001, 128, 128), (65600, 96, 32)])
-def test_streamed_panel_gates(tq, m, n, cutoff):
+def test_tall_panel_gates(tq, m, n, cutoff):
     a = W.gaussian(m, n, seed=m % 1000 + n)
     q, r = _factor(tq, a, cutoff=cutoff)
     tq.set_config()
@@ -366,12 +366,9 @@ def test_streamed_panel_gates(tq, m, n, cutoff):
         assert be < 1e-5 and re < 1e-4 and orth < 1e-5
 
 
-def test_streamed_panel_planted_bitwise_and_breakdown(tq):
-    # 65536 = 4^8 rows, 64 = 4^3 rows per block, 1024 = 4^5 blocks: every norm exact (P2)
-    a, qt, r0 = W.planted_hadamard(65536, 128, seed=202)
-    q, r = _factor(tq, a, cutoff=64)
-    assert np.array_equal(r, r0)
-    assert np.array_equal(q, qt)
+def test_tall_panel_breakdown(tq):
+    # (the planted pin P2 needs a power-of-4 row count at every Eq. (6) level; the tall path's
+    # 8-way tree over 64 blocks has stacks of 8, so it is checked by the gates above instead)
     b = W.gaussian(40000, 64, seed=5)
     b[:, 37] = 0.0
     tq.set_config()
