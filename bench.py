@@ -181,7 +181,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
-    ap.add_argument("--cpu-sample-cols", type=int, default=1024)
+    ap.add_argument("--cpu-sample-cols", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-lls", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
