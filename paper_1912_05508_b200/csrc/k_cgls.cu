@@ -506,14 +506,18 @@ __global__ void __launch_bounds__(kTriBlk) tri_n_part_kernel(int n, const double
   const int i = rb * kTriBlk + threadIdx.x;
   if (i >= n) return;
   const double* mm = M + i + (long long)j0 * ldm;
-  double a0 = 0.0, a1 = 0.0;
+  // 8 loads in flight per thread (with 2 the kernel ran at 3.5 TB/s)
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   int j = 0;
-  for (; j + 2 <= nc; j += 2) {
-    a0 = fma(mm[(long long)j * ldm], ps[j], a0);
-    a1 = fma(mm[(long long)(j + 1) * ldm], ps[j + 1], a1);
+  for (; j + 8 <= nc; j += 8) {
+    double mv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) mv[u] = __ldg(mm + (long long)(j + u) * ldm);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u & 3] = fma(mv[u], ps[j + u], acc[u & 3]);
   }
-  if (j < nc) a0 = fma(mm[(long long)j * ldm], ps[j], a0);
-  part[(long long)cb * n + i] = a0 + a1;
+  for (; j < nc; ++j) acc[0] = fma(mm[(long long)j * ldm], ps[j], acc[0]);
+  part[(long long)cb * n + i] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 __global__ void tri_n_reduce_kernel(int n, int nch, const double* __restrict__ part,
@@ -537,12 +541,27 @@ __global__ void __launch_bounds__(256) tri_t_kernel(int n, const double* __restr
   if (j >= n) return;
   const double* mm = M + (long long)j * ldm;
   double a0 = 0.0, a1 = 0.0;
-  int i = lane;
-  for (; i + 32 <= j; i += 64) {
-    a0 = fma(mm[i], v[i], a0);
-    a1 = fma(mm[i + 32], v[i + 32], a1);
+  int i = 0;
+  // rows [0, j]: 16-byte loads, four in flight per lane (256 rows per warp step) when M's
+  // columns are 16-byte aligned
+  if ((ldm & 1) == 0 && (reinterpret_cast<uintptr_t>(M) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+    const int j256 = ((j + 1) / 256) * 256;
+    for (; i < j256; i += 256) {
+      double2 mv[4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        mv[u] = __ldg(reinterpret_cast<const double2*>(mm + i + 64 * u + 2 * lane));
+        vv[u] = *reinterpret_cast<const double2*>(v + i + 64 * u + 2 * lane);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0 = fma(mv[u].x, vv[u].x, a0);
+        a1 = fma(mv[u].y, vv[u].y, a1);
+      }
+    }
   }
-  for (; i <= j; i += 32) a0 = fma(mm[i], v[i], a0);
+  for (i += lane; i <= j; i += 32) a0 = fma(mm[i], v[i], a0);
   const double r = warp_sum_d(a0 + a1);
   if (lane == 0) s[j] = r;
 }
