@@ -334,10 +334,36 @@ __global__ void copy_validate_kernel(int m, const float* __restrict__ A, long lo
   const float* a = A + (long long)j * lda;
   float* q = Q + (long long)j * ldq;
   bool bad = false;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+  const bool inplace = q == a;
+  int i0 = 0;
+  if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(q)) & 15) == 0) {
+    // 16-byte path: four independent float4 loads in flight per thread (the scalar loop ran at
+    // ~3.1 TB/s of the 6.5 measured copy bandwidth at config 3)
+    const int m4 = m >> 2, stride = gridDim.x * blockDim.x;
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    float4* q4 = reinterpret_cast<float4*>(q);
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < m4; i += 4 * stride) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(a4 + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        bad |= !isfinite(v[u].x) || !isfinite(v[u].y) || !isfinite(v[u].z) || !isfinite(v[u].w);
+        if (!inplace) q4[i + u * stride] = v[u];
+      }
+    }
+    for (; i < m4; i += stride) {
+      const float4 v = __ldcs(a4 + i);
+      bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+      if (!inplace) q4[i] = v;
+    }
+    i0 = m4 << 2;
+  }
+  for (int i = i0 + blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     const float v = a[i];
     bad |= !isfinite(v);
-    if (q != a) q[i] = v;
+    if (!inplace) q[i] = v;
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMin(status, col0 + j + 1);
 }
@@ -345,7 +371,7 @@ __global__ void copy_validate_kernel(int m, const float* __restrict__ A, long lo
 cudaError_t copy_validate(int m, int n, const float* A, long long lda, float* Q, long long ldq,
                           int* status, cudaStream_t st, int col0) {
   if (m <= 0 || n <= 0) return cudaSuccess;
-  int gx = (m + 1023) / 1024;
+  int gx = (m + 4095) / 4096;  // ~4 float4 per thread
   if (gx > 64) gx = 64;
   dim3 grid(gx, n);
   copy_validate_kernel<<<grid, 256, 0, st>>>(m, A, lda, Q, ldq, status, col0);

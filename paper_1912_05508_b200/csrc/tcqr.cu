@@ -62,6 +62,11 @@ struct Context {
   cudaStream_t user_stream = nullptr;  // the caller's stream (may be the legacy NULL stream)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // copy streams of the streamed host factor
+  // K1 cast of a split node's A2 runs on s_side beside the node's left recursion (it reads only
+  // A2, which the left subtree never touches); fork / join events per recursion depth
+  cudaStream_t s_side = nullptr;
+  cudaEvent_t ev_fork[64] = {}, ev_join[64] = {};
+  int cast_overlap = 1;  // env TCQR_CAST_OVERLAP=0 turns it off
   int num_sms = 148;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
@@ -480,6 +485,7 @@ struct FactorJob {
   long long ldr;
   FactorWs* ws;
   StreamPlan* sp = nullptr;
+  int depth = 0;  // recursion depth of the current rgs call (fork / join event slot)
 };
 
 // The compute stream waits for every chunk overlapping columns [c0, c1).
@@ -558,7 +564,27 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   } else {
     const int h = split_point(w), w2 = w - h;
     const bool tc = w > c.cfg.cutoff;
-    CKR(rgs(J, c0, h, tc || need_h));  // Alg. 2 line 7
+    // K1 of this node's A2 does not depend on the left recursion (Alg. 2 line 7 writes only
+    // columns [c0, c0+h)): fork it onto the side stream, join before the TN product
+    const bool side = tc && !J.sp && c.cast_overlap && !g_prof && J.depth < 64;
+    if (side) {
+      const int p0 = c0 + h;
+      float* A2p = J.Q + (long long)p0 * J.ldq;
+      __half* A2h = ws.Qh + (long long)p0 * ws.ldh;
+      CK(cudaEventRecord(c.ev_fork[J.depth], c.stream));
+      CK(cudaStreamWaitEvent(c.s_side, c.ev_fork[J.depth], 0));
+      CK(cast_scale(m, w2, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling, c.d_status,
+                    p0, ws.cmax + p0, c.s_side));
+      if (c.cfg.fp16_split && ws.Ql)
+        CK(cast_lo(m, w2, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, ws.Ql + (long long)p0 * ws.ldh,
+                   ws.ldh, c.s_side));
+      CK(cudaEventRecord(c.ev_join[J.depth], c.s_side));
+    }
+    ++J.depth;
+    const int lrc = rgs(J, c0, h, tc || need_h);  // Alg. 2 line 7
+    --J.depth;
+    if (side) CK(cudaStreamWaitEvent(c.stream, c.ev_join[J.depth], 0));
+    CKR(lrc);
     float* A2 = J.Q + (long long)(c0 + h) * J.ldq;
     float* Rblk = J.R + c0 + (long long)(c0 + h) * J.ldr;
     if (tc) {
@@ -583,9 +609,10 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
         __half* A2h = ws.Qh + (long long)p0 * ws.ldh;
         float* Tp = ws.T + (long long)off * h;
         __half* R12hp = ws.R12h + (long long)off * ldh2;
-        PROF(TCQR_K1_CAST, 0, 6.0 * m * wp,
-             CK(cast_scale(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling,
-                           c.d_status, p0, ws.cmax, c.stream)));
+        if (!side)
+          PROF(TCQR_K1_CAST, 0, 6.0 * m * wp,
+               CK(cast_scale(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling,
+                             c.d_status, p0, ws.cmax + p0, c.stream)));
         if (c.cfg.fp16_split && ws.Ql) {
           // NEXT-4: three MMAs per product on the hi/lo FP16 halves (lo x lo dropped)
           __half* A1l = ws.Ql + (long long)c0 * ws.ldh;
@@ -594,8 +621,9 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
           float* T3p = ws.T3 + (long long)off * h;
           __half* R12lp = ws.R12l + (long long)off * ldh2;
           float* Rb = Rblk + (long long)off * J.ldr;
-          PROF(TCQR_K1_CAST, 0, 8.0 * m * wp,
-               CK(cast_lo(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, A2l, ws.ldh, c.stream)));
+          if (!side)
+            PROF(TCQR_K1_CAST, 0, 8.0 * m * wp,
+                 CK(cast_lo(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, A2l, ws.ldh, c.stream)));
           PROF(TCQR_K3_TN, 6.0 * m * h * wp, 6.0 * m * (h + wp) + 12.0 * h * wp, {
             CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, Tp, h, ws.inv_s + p0, ws.P, ws.p_cap,
                           c.num_sms, c.stream));
@@ -668,7 +696,10 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
       PROF(TCQR_K2B_NN, 2.0 * m * h * w2, 4.0 * m * h + 8.0 * m * w2,
            CK(f32_nn_update(m, h, w2, Qc, J.ldq, ws.T, A2, J.ldq, c.stream)));
     }
-    CKR(rgs(J, c0 + h, w2, need_h));  // Alg. 2 line 9
+    ++J.depth;
+    const int rrc = rgs(J, c0 + h, w2, need_h);  // Alg. 2 line 9
+    --J.depth;
+    CKR(rrc);
     return chunk_done(J, c0, w);
   }
   if (need_h) {
@@ -857,6 +888,13 @@ int tcqr_finalize(void) {
   if (c.ev_in) cudaEventDestroy(c.ev_in);
   if (c.ev_out) cudaEventDestroy(c.ev_out);
   if (c.stream) cudaStreamDestroy(c.stream);
+  if (c.s_side) cudaStreamDestroy(c.s_side);
+  c.s_side = nullptr;
+  for (int i = 0; i < 64; ++i) {
+    if (c.ev_fork[i]) cudaEventDestroy(c.ev_fork[i]);
+    if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
+    c.ev_fork[i] = c.ev_join[i] = nullptr;
+  }
   if (c.s_h2d) cudaStreamDestroy(c.s_h2d);
   if (c.s_d2h) cudaStreamDestroy(c.s_d2h);
   c.s_h2d = c.s_d2h = nullptr;
@@ -889,8 +927,17 @@ int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int ran
   cudaEventCreateWithFlags(&c.ev_in, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c.ev_out, cudaEventDisableTiming);
   if (cudaStreamCreateWithFlags(&c.s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c.s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+      cudaStreamCreateWithFlags(&c.s_d2h, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c.s_side, cudaStreamNonBlocking) != cudaSuccess)
     return TCQR_ERR_CUDA;
+  for (int i = 0; i < 64; ++i)
+    if (cudaEventCreateWithFlags(&c.ev_fork[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming) != cudaSuccess)
+      return TCQR_ERR_CUDA;
+  {
+    const char* e = getenv("TCQR_CAST_OVERLAP");
+    c.cast_overlap = (e && atoi(e) == 0) ? 0 : 1;
+  }
   c.num_sms = prop.multiProcessorCount;
   c.rank = rank;
   c.nranks = nranks;
