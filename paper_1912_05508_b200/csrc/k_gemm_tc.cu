@@ -32,8 +32,12 @@ struct TcCfg {
   // NBUF = 0: direct-load epilogue; 2 / 4: TMA epilogue with that many 16 KB C-chunk buffers (4
   // buffers prefetch three chunks ahead for short-K updates at the cost of one mainloop stage; 2
   // keep the full mainloop depth for long K, where the epilogue hides behind the next tile)
+  // NBUF = 2 is the short-K update (K = h <= 512, BN = 128): two mainloop stages, 97 KB of
+  // shared memory and 256 TMEM columns, so TWO CTAs share an SM and one CTA's C loads overlap the
+  // other's epilogue (the deep levels are HBM-bound on the C read-modify-write)
   static constexpr int CBUF = NBUF * 16384;
-  static constexpr int ST = (NBUF == 4) ? ((BN == 128) ? 4 : 3) : ((BN == 128) ? 6 : 4);
+  static constexpr int ST = (NBUF == 2) ? 2 : (NBUF == 4) ? ((BN == 128) ? 4 : 3) : ((BN == 128) ? 6 : 4);
+  static constexpr int OCC = (NBUF == 2 && BN == 128) ? 2 : 1;  // CTAs per SM
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static constexpr int SMEM = ST * STAGE + CBUF + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -671,7 +675,8 @@ static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const C
     attr = true;
   }
   const int tiles = ((M + 127) / 128) * ((N + BN - 1) / BN) * splits;
-  const int grid = tiles < num_sms ? tiles : num_sms;
+  const int slots = Cfg::OCC * num_sms;
+  const int grid = tiles < slots ? tiles : slots;
   tc_gemm_kernel<BN, MODE, NBUF><<<grid, 192, Cfg::SMEM, st>>>(a, b, cm, M, N, K, splits, C, ldc,
                                                                sstride, mult);
   return cudaGetLastError();
@@ -720,6 +725,17 @@ static bool use_tc2() {
   return on == 1;
 }
 
+// fewest K-blocks (of 64 rows) per split-K slice of the TN product (env TCQR_TN_MINKB)
+static int tn_min_kb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TCQR_TN_MINKB");
+    v = e ? atoi(e) : 8;
+    if (v < 1) v = 1;
+  }
+  return v;
+}
+
 // D (h x w2) = A1h' A2h ; writes C (ldc) directly (splits == 1, scaled by col_mult) or the
 // partials P (splits > 1; P has room for splits * ldp * w2 floats) followed by the reduction.
 cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, const __half* A2h,
@@ -734,7 +750,7 @@ cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, 
     const int np = num_sms / 2;
     if (tiles2 < np) {
       splits = np / tiles2;
-      if (splits > nkb / 8) splits = nkb / 8;
+      if (splits > nkb / tn_min_kb()) splits = nkb / tn_min_kb();
       if (splits < 1) splits = 1;
       const long long per = (long long)h * w2;
       if (P == nullptr || per * splits > p_cap) splits = P ? (int)(p_cap / per) : 1;
@@ -769,7 +785,7 @@ cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, 
     splits = num_sms / tiles;
     // keep >= 8 K-blocks per split: the partials (and their reduction) cost HBM traffic and a
     // split that only fills the pipeline is latency, not throughput
-    if (splits > nkb / 8) splits = nkb / 8;
+    if (splits > nkb / tn_min_kb()) splits = nkb / tn_min_kb();
     if (splits < 1) splits = 1;
     const long long per = (long long)h * w2;
     if (P == nullptr || per * splits > p_cap) splits = P ? (int)(p_cap / per) : 1;
@@ -800,6 +816,16 @@ cudaError_t tc_gemm_tn(int m, int h, int w2, const __half* A1h, long long lda1, 
   return cudaGetLastError();
 }
 
+// K = h up to which the update runs as the two-CTAs-per-SM short-K variant (env TCQR_NN_SHORTK)
+static int nn_short_k() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TCQR_NN_SHORTK");
+    v = e ? atoi(e) : 512;
+  }
+  return v;
+}
+
 // C (m x w2) -= (Qh Bh) diag(col_mult);  Qh m x h (ldq), Bh h x w2 (ldb).
 cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long ldq,
                               const __half* Bh, long long ldb, float* C, long long ldc,
@@ -820,6 +846,11 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
   CUtensorMap mc;
   const bool tmac = (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0) &&
                     make_map_f32(&mc, C, m, w2, ldc, 128, 32);
+  if (tmac && h <= nn_short_k()) {
+    CUtensorMap mb1;
+    if (!make_map_f16(&mb1, Bh, h, w2, ldb, 64, 128)) return cudaErrorInvalidValue;
+    return launch_tc<128, kModeNN, 2>(ma, mb1, mc, m, w2, h, 1, C, ldc, 0, col_mult, num_sms, st);
+  }
   if (tmac && h <= 2048)
     return (BN == 256) ? launch_tc<256, kModeNN, 4>(ma, mb, mc, m, w2, h, 1, C, ldc, 0, col_mult,
                                                     num_sms, st)

@@ -67,6 +67,14 @@ struct Context {
   cudaStream_t s_side = nullptr;
   cudaEvent_t ev_fork[64] = {}, ev_join[64] = {};
   int cast_overlap = 1;  // env TCQR_CAST_OVERLAP=0 turns it off
+  // Look-ahead (one rank, device path): a split node of width w <= la_max_w updates only the
+  // columns of its right subtree's first leaf on the critical stream; the rest of the K4 update
+  // runs on s_la, low priority, on a budget of la_sms SMs, beside that leaf (which uses the
+  // other SMs).  The critical stream waits for it right after the leaf.
+  cudaStream_t s_la = nullptr;
+  cudaEvent_t ev_la[64] = {}, ev_la_fork[64] = {};
+  int la_max_w = 512;  // env TCQR_LOOKAHEAD_W (0: off); measured: 1024 and up lose (the tail outlasts the leaf)
+  int la_sms = 10;      // env TCQR_LA_SMS (the short-K update runs two CTAs per SM)
   int num_sms = 148;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
@@ -486,6 +494,7 @@ struct FactorJob {
   FactorWs* ws;
   StreamPlan* sp = nullptr;
   int depth = 0;  // recursion depth of the current rgs call (fork / join event slot)
+  cudaEvent_t la_pending = nullptr;  // look-ahead update to wait for after the next leaf
 };
 
 // The compute stream waits for every chunk overlapping columns [c0, c1).
@@ -535,6 +544,15 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   Context& c = g_ctx;
   FactorWs& ws = *J.ws;
   const int m = J.m;
+  if (J.la_pending && w <= c.cfg.cutoff) {
+    // the first leaf after a look-ahead split touches only the columns updated on the critical
+    // stream; everything after it waits for the rest of that update
+    cudaEvent_t e = J.la_pending;
+    J.la_pending = nullptr;
+    const int rc = rgs(J, c0, w, need_h);
+    CK(cudaStreamWaitEvent(c.stream, e, 0));
+    return rc;
+  }
   float* Qc = J.Q + (long long)c0 * J.ldq;
   if (c.cfg.leaf_kernel && c.nranks == 1 && w <= 128 && w <= c.cfg.cutoff) {
     // the whole leaf (every node below the cutoff) in one cooperative launch (k_leaf.cu)
@@ -664,9 +682,27 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
                CK(r12_finalize(h, wp, Tp, h, Rblk + (long long)off * J.ldr, J.ldr, R12hp, ldh2,
                                ws.inv_s2 + p0, c.cfg.col_scaling, c.stream)));
         }
-        PROF(TCQR_K4_NN, 2.0 * m * h * wp, 2.0 * m * h + 2.0 * h * wp + 8.0 * m * wp,
-             CK(tc_gemm_nn_update(m, h, wp, A1h, ws.ldh, R12hp, ldh2, A2p, J.ldq, ws.inv_s2 + p0,
-                                  c.num_sms, c.stream)));
+        // look-ahead: L = width of the right subtree's first leaf-level subtree
+        int L = w2;
+        while (L > c.cfg.cutoff) L = split_point(L);
+        if (side && c.nranks == 1 && w <= c.la_max_w && L < wp && J.depth < 64) {
+          const int d = J.depth;
+          CK(cudaEventRecord(c.ev_la_fork[d], c.stream));
+          CK(cudaStreamWaitEvent(c.s_la, c.ev_la_fork[d], 0));
+          CK(tc_gemm_nn_update(m, h, wp - L, A1h, ws.ldh, R12hp + (long long)L * ldh2, ldh2,
+                               A2p + (long long)L * J.ldq, J.ldq, ws.inv_s2 + p0 + L, c.la_sms,
+                               c.s_la));
+          CK(cudaEventRecord(c.ev_la[d], c.s_la));
+          // the casts the right subtree forks read those columns
+          CK(cudaStreamWaitEvent(c.s_side, c.ev_la[d], 0));
+          CK(tc_gemm_nn_update(m, h, L, A1h, ws.ldh, R12hp, ldh2, A2p, J.ldq, ws.inv_s2 + p0,
+                               c.num_sms, c.stream));
+          J.la_pending = c.ev_la[d];
+        } else {
+          PROF(TCQR_K4_NN, 2.0 * m * h * wp, 2.0 * m * h + 2.0 * h * wp + 8.0 * m * wp,
+               CK(tc_gemm_nn_update(m, h, wp, A1h, ws.ldh, R12hp, ldh2, A2p, J.ldq,
+                                    ws.inv_s2 + p0, c.num_sms, c.stream)));
+        }
       }
     } else if (c.nranks == 1) {
       need_cols(J, c0 + h, c0 + w);
@@ -890,10 +926,14 @@ int tcqr_finalize(void) {
   if (c.stream) cudaStreamDestroy(c.stream);
   if (c.s_side) cudaStreamDestroy(c.s_side);
   c.s_side = nullptr;
+  if (c.s_la) cudaStreamDestroy(c.s_la);
+  c.s_la = nullptr;
   for (int i = 0; i < 64; ++i) {
     if (c.ev_fork[i]) cudaEventDestroy(c.ev_fork[i]);
     if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
-    c.ev_fork[i] = c.ev_join[i] = nullptr;
+    if (c.ev_la[i]) cudaEventDestroy(c.ev_la[i]);
+    if (c.ev_la_fork[i]) cudaEventDestroy(c.ev_la_fork[i]);
+    c.ev_fork[i] = c.ev_join[i] = c.ev_la[i] = c.ev_la_fork[i] = nullptr;
   }
   if (c.s_h2d) cudaStreamDestroy(c.s_h2d);
   if (c.s_d2h) cudaStreamDestroy(c.s_d2h);
@@ -922,21 +962,38 @@ int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int ran
   }
   c.device = device;
   c.user_stream = static_cast<cudaStream_t>(cuda_stream);
-  if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess)
-    return TCQR_ERR_CUDA;
+  {
+    // the critical stream is the most urgent (the look-ahead and cast streams fill in behind it)
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, hi) != cudaSuccess)
+      return TCQR_ERR_CUDA;
+  }
   cudaEventCreateWithFlags(&c.ev_in, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c.ev_out, cudaEventDisableTiming);
   if (cudaStreamCreateWithFlags(&c.s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c.s_d2h, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c.s_side, cudaStreamNonBlocking) != cudaSuccess)
     return TCQR_ERR_CUDA;
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo: the least urgent
+    if (cudaStreamCreateWithPriority(&c.s_la, cudaStreamNonBlocking, lo) != cudaSuccess)
+      return TCQR_ERR_CUDA;
+  }
   for (int i = 0; i < 64; ++i)
     if (cudaEventCreateWithFlags(&c.ev_fork[i], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.ev_la[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.ev_la_fork[i], cudaEventDisableTiming) != cudaSuccess)
       return TCQR_ERR_CUDA;
   {
     const char* e = getenv("TCQR_CAST_OVERLAP");
     c.cast_overlap = (e && atoi(e) == 0) ? 0 : 1;
+    const char* w = getenv("TCQR_LOOKAHEAD_W");
+    c.la_max_w = w ? atoi(w) : 512;
+    const char* n = getenv("TCQR_LA_SMS");
+    c.la_sms = n ? std::max(1, atoi(n)) : 10;
   }
   c.num_sms = prop.multiProcessorCount;
   c.rank = rank;

@@ -80,6 +80,9 @@ def test_gemm_tn_envelope(tq, m, h, w2):
 
 @pytest.mark.parametrize("m,h,w2", [(128, 64, 128), (1000, 96, 200), (4160, 256, 384),
                                     (3000, 512, 64),
+                                    # K = h <= 256: the two-CTAs-per-SM short-K variant, with more
+                                    # tiles than CTA slots (persistent loop) and ragged rows/columns
+                                    (40000, 128, 256), (33000, 200, 130), (70000, 256, 128),
                                     # h > 2048, w2 >= 256: the CTA-pair kernel (ragged tiles)
                                     (4104, 2304, 320), (704, 4096, 256)])
 def test_gemm_nn_update_envelope(tq, m, h, w2):
