@@ -290,24 +290,31 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
       if (i <= j) a.R[(c0 + i) + (long long)(c0 + j) * a.ldr] = (float)s.Rd[i * 34 + j];
     }
   }
-  // (4) Q_b <- Q_b S_b (S_b upper triangular: the zero terms add exactly nothing); rolled over l
-  // (Q_b(t, l) read from shared memory per step) to keep the code small
+  // (4) Q_b <- Q_b S_b (S_b upper triangular: the zero terms add exactly nothing).  Rolled over
+  // groups of four l: Q_b(t, l..l+3) is one conflict-free 16-byte shared load (the scalar load per
+  // l hit 8 banks per warp), then four unrolled rank-1 steps in the same l order as before.  Rows
+  // l >= pw of S_b are zero (lanes >= pw above), so the padded tail adds exact zeros.
   if (t < nrows) {
     float* row = s.L + t * kLd + c0;
     float y[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) y[j] = 0.f;
 #pragma unroll 1
-    for (int l = 0; l < pw; ++l) {
-      const float ql = row[l];
-      const float4* sr = reinterpret_cast<const float4*>(s.Sf + l * 32);
+    for (int l4 = 0; l4 < pw; l4 += 4) {
+      const float4 q4 = *reinterpret_cast<const float4*>(row + l4);
+      const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
-      for (int j4 = 0; j4 < 8; ++j4) {
-        const float4 v = sr[j4];
-        y[4 * j4] = fmaf(ql, v.x, y[4 * j4]);
-        y[4 * j4 + 1] = fmaf(ql, v.y, y[4 * j4 + 1]);
-        y[4 * j4 + 2] = fmaf(ql, v.z, y[4 * j4 + 2]);
-        y[4 * j4 + 3] = fmaf(ql, v.w, y[4 * j4 + 3]);
+      for (int u = 0; u < 4; ++u) {
+        const float ql = qv[u];
+        const float4* sr = reinterpret_cast<const float4*>(s.Sf + (l4 + u) * 32);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 v = sr[j4];
+          y[4 * j4] = fmaf(ql, v.x, y[4 * j4]);
+          y[4 * j4 + 1] = fmaf(ql, v.y, y[4 * j4 + 1]);
+          y[4 * j4 + 2] = fmaf(ql, v.z, y[4 * j4 + 2]);
+          y[4 * j4 + 3] = fmaf(ql, v.w, y[4 * j4 + 3]);
+        }
       }
     }
 #pragma unroll
