@@ -4,6 +4,7 @@
 // The paper is silent on FP16 range (PAPER.md:127-141 only notes FP16's "significantly
 // constrained range"); reading R-A4 guards it with a per-column power-of-two scale
 // s_j = 2^-floor(log2 max_i |X_ij|), exact to apply and undo.
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -133,6 +134,95 @@ __global__ void __launch_bounds__(256) cast_pass2_kernel(int m, const float* __r
   for (long long q = i + threadIdx.x; q < r1; q += 256) xh[q] = __float2half_rn(x[q] * s);
 }
 
+// Few columns x many rows, fused: one thread-block cluster per column, CTA r of the cluster owns
+// rows [r * RPC, (r + 1) * RPC) with its 4 * V rows per thread held in registers.  Pass 1 (max |x|
+// and non-finite detection) reads HBM once; the per-CTA maxima meet through distributed shared
+// memory (max is order-independent: the same s as the two-kernel path, bit for bit); pass 2 casts
+// from the registers.  One launch and one read of X instead of memset + colmax + cast_pass2.
+template <int V>
+__global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* __restrict__ X,
+                                                           long long ldx, __half* __restrict__ Xh,
+                                                           long long ldh, float* __restrict__ inv_s,
+                                                           int scaling, int* status, int col_base) {
+  namespace cg = cooperative_groups;
+  constexpr int RPC = 256 * 4 * V;  // rows per CTA
+  __shared__ float red[32];
+  __shared__ float cm;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int j = blockIdx.y;
+  const int rank = (int)cluster.block_rank();
+  const long long r0 = (long long)rank * RPC;
+  const float* x = X + (long long)j * ldx;
+  float4 v[V];
+  float mx = 0.f;
+  bool bad = false;
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const long long q = r0 + 4LL * (threadIdx.x + 256 * u);
+    if (q + 3 < m) {
+      v[u] = *reinterpret_cast<const float4*>(x + q);
+    } else {
+      v[u].x = q < m ? x[q] : 0.f;
+      v[u].y = q + 1 < m ? x[q + 1] : 0.f;
+      v[u].z = q + 2 < m ? x[q + 2] : 0.f;
+      v[u].w = q + 3 < m ? x[q + 3] : 0.f;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+    bad |= !(isfinite(v[u].x) && isfinite(v[u].y) && isfinite(v[u].z) && isfinite(v[u].w));
+  }
+  if (bad && status) atomicMin(status, col_base + j + 1);
+  float s = 1.f;
+  if (scaling) {
+    mx = block_max(mx, red);
+    if (threadIdx.x == 0) cm = mx;
+    cluster.sync();
+    float g = 0.f;
+    for (int r = 0; r < (int)cluster.num_blocks(); ++r) g = fmaxf(g, *cluster.map_shared_rank(&cm, r));
+    s = pow2_scale_for(g);
+    cluster.sync();  // the peers' cm stays live until every CTA has read it
+  }
+  if (rank == 0 && threadIdx.x == 0 && inv_s) inv_s[j] = 1.f / s;
+  __half* xh = Xh + (long long)j * ldh;
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const long long q = r0 + 4LL * (threadIdx.x + 256 * u);
+    if (q + 3 < m) {
+      __half2 lo = __floats2half2_rn(v[u].x * s, v[u].y * s);
+      __half2 hi = __floats2half2_rn(v[u].z * s, v[u].w * s);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(xh + q) = pk;
+    } else {
+      if (q < m) xh[q] = __float2half_rn(v[u].x * s);
+      if (q + 1 < m) xh[q + 1] = __float2half_rn(v[u].y * s);
+      if (q + 2 < m) xh[q + 2] = __float2half_rn(v[u].z * s);
+    }
+  }
+}
+
+template <int V>
+static cudaError_t launch_cast_cluster(int m, int w, const float* X, long long ldx, __half* Xh,
+                                       long long ldh, float* inv_s, int scaling, int* status,
+                                       int col_base, int nchunks, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nchunks, w);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = nchunks;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, cast_cluster_kernel<V>, m, X, ldx, Xh, ldh, inv_s, scaling, status,
+                            col_base);
+}
+
 cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
                        float* inv_s, int scaling, int* status, int col_base, unsigned int* cmax,
                        cudaStream_t st) {
@@ -154,6 +244,19 @@ cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, 
     cast_scale_kernel<<<w, kCastThreads, 0, st>>>(m, X, ldx, Xh, ldh, inv_s, scaling, status,
                                                    col_base);
     return cudaGetLastError();
+  }
+  static int use_cluster = -1;  // env TCQR_CAST_CLUSTER=0: the two-kernel path below
+  if (use_cluster < 0) {
+    const char* ev = getenv("TCQR_CAST_CLUSTER");
+    use_cluster = ev ? atoi(ev) : 1;
+  }
+  const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
+                   ((ldh & 3) == 0) && ((reinterpret_cast<uintptr_t>(Xh) & 7) == 0);
+  if (use_cluster && vec) {
+    if (m <= 8 * 4096) return launch_cast_cluster<4>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
+                                                     col_base, (m + 4095) / 4096, st);
+    if (m <= 8 * 8192) return launch_cast_cluster<8>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
+                                                     col_base, (m + 8191) / 8192, st);
   }
   cudaError_t e = cudaMemsetAsync(cmax, 0, sizeof(unsigned int) * w, st);
   if (e != cudaSuccess) return e;

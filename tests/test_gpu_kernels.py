@@ -29,7 +29,10 @@ def _h2np(xh):
     return xh.float().cpu().numpy().astype(np.float64)
 
 
-@pytest.mark.parametrize("m,w", [(1000, 7), (4096, 33), (37, 3)])
+# (20000, 3): five 4096-row CTAs per cluster with a ragged last one; (40000, 2): the 8192-row
+# cluster variant; (70000, 2): past the cluster path (memset + colmax + cast_pass2)
+@pytest.mark.parametrize("m,w", [(1000, 7), (4096, 33), (37, 3), (20000, 3), (32768, 4),
+                                 (40000, 2), (70000, 2)])
 def test_cast_scale_bitwise(tq, m, w):
     rng = np.random.default_rng(m)
     x = (rng.standard_normal((m, w)) * np.exp2(rng.integers(-30, 20, w))).astype(np.float32)
@@ -52,6 +55,16 @@ def test_cast_flags_nonfinite(tq):
     with pytest.raises(tq.TcqrError) as e:
         tq.cast_scale(X)
     assert e.value.code == 4
+
+
+def test_cast_flags_nonfinite_late_chunk(tq):
+    """Non-finite entry in the last row chunk of a multi-CTA column (cluster cast path)."""
+    x = np.ones((32768, 3), np.float32)
+    x[30001, 2] = np.inf
+    X = tq.to_device_colmajor(x)
+    with pytest.raises(tq.TcqrError) as e:
+        tq.cast_scale(X)
+    assert e.value.code == 3
 
 
 def _fp16_operand(rng, m, k, scale=1.0):
