@@ -227,8 +227,24 @@ cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, 
                        float* inv_s, int scaling, int* status, int col_base, unsigned int* cmax,
                        cudaStream_t st) {
   if (m <= 0 || w <= 0) return cudaSuccess;
-  // Few columns x many rows: split rows (2-D grid, pass 1 = column max via atomicMax).
-  // Many columns: one CTA per column already fills the GPU.
+  // Range guard with m <= 65536 (every config's local height): the cluster kernel at any width
+  // (one HBM read; at config 3 it beat the per-column two-pass kernel for w >= 1024 as well:
+  // K1 3.81 -> 3.57 ms per factor, profiles/r01_bench_cfg3_v14_*).  Otherwise few columns x many
+  // rows: split rows (2-D grid, pass 1 = column max via atomicMax); many columns: one CTA per
+  // column (two passes over the column).
+  static int use_cluster = -1;  // env TCQR_CAST_CLUSTER=0: the paths below
+  if (use_cluster < 0) {
+    const char* ev = getenv("TCQR_CAST_CLUSTER");
+    use_cluster = ev ? atoi(ev) : 1;
+  }
+  const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
+                   ((ldh & 3) == 0) && ((reinterpret_cast<uintptr_t>(Xh) & 7) == 0);
+  if (use_cluster && vec && (scaling || status)) {
+    if (m <= 8 * 4096) return launch_cast_cluster<4>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
+                                                     col_base, (m + 4095) / 4096, st);
+    if (m <= 8 * 8192) return launch_cast_cluster<8>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
+                                                     col_base, (m + 8191) / 8192, st);
+  }
   static int col_min = -1;  // per-column kernel from this width on (env TCQR_CAST_COL_MIN)
   if (col_min < 0) {
     const char* e = getenv("TCQR_CAST_COL_MIN");
@@ -244,19 +260,6 @@ cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, 
     cast_scale_kernel<<<w, kCastThreads, 0, st>>>(m, X, ldx, Xh, ldh, inv_s, scaling, status,
                                                    col_base);
     return cudaGetLastError();
-  }
-  static int use_cluster = -1;  // env TCQR_CAST_CLUSTER=0: the two-kernel path below
-  if (use_cluster < 0) {
-    const char* ev = getenv("TCQR_CAST_CLUSTER");
-    use_cluster = ev ? atoi(ev) : 1;
-  }
-  const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
-                   ((ldh & 3) == 0) && ((reinterpret_cast<uintptr_t>(Xh) & 7) == 0);
-  if (use_cluster && vec) {
-    if (m <= 8 * 4096) return launch_cast_cluster<4>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
-                                                     col_base, (m + 4095) / 4096, st);
-    if (m <= 8 * 8192) return launch_cast_cluster<8>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
-                                                     col_base, (m + 8191) / 8192, st);
   }
   cudaError_t e = cudaMemsetAsync(cmax, 0, sizeof(unsigned int) * w, st);
   if (e != cudaSuccess) return e;
