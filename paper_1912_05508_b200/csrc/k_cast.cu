@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* _
   namespace cg = cooperative_groups;
   constexpr int RPC = 256 * 4 * V;  // rows per CTA
   __shared__ float red[32];
-  __shared__ float cm;
+  __shared__ float cmv[8];  // cmv[r] = max |x| over CTA r's rows, pushed by CTA r
   cg::cluster_group cluster = cg::this_cluster();
   const int j = blockIdx.y;
   const int rank = (int)cluster.block_rank();
@@ -177,12 +177,14 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* _
   float s = 1.f;
   if (scaling) {
     mx = block_max(mx, red);
-    if (threadIdx.x == 0) cm = mx;
+    const int nblk = (int)cluster.num_blocks();
+    // push this CTA's max into every peer's slot: after the one cluster barrier (release /
+    // acquire) each CTA reads only its own shared memory, so no second barrier keeps peers alive
+    if ((int)threadIdx.x < nblk) *cluster.map_shared_rank(&cmv[rank], (int)threadIdx.x) = mx;
     cluster.sync();
     float g = 0.f;
-    for (int r = 0; r < (int)cluster.num_blocks(); ++r) g = fmaxf(g, *cluster.map_shared_rank(&cm, r));
+    for (int r = 0; r < nblk; ++r) g = fmaxf(g, cmv[r]);
     s = pow2_scale_for(g);
-    cluster.sync();  // the peers' cm stays live until every CTA has read it
   }
   if (rank == 0 && threadIdx.x == 0 && inv_s) inv_s[j] = 1.f / s;
   __half* xh = Xh + (long long)j * ldh;
