@@ -242,7 +242,14 @@ cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, 
   const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
                    ((ldh & 3) == 0) && ((reinterpret_cast<uintptr_t>(Xh) & 7) == 0);
   if (use_cluster && vec && (scaling || status)) {
-    if (m <= 8 * 4096) return launch_cast_cluster<4>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
+    // 8192-row CTAs (8 float4 loads in flight per thread) by default: at config 3 K1 3.03 ->
+    // 2.76 ms against 4096-row CTAs (profiles/r01_bench_cfg3_v19_*); env TCQR_CAST_V8=0 for those
+    static int v8 = -1;
+    if (v8 < 0) {
+      const char* ev = getenv("TCQR_CAST_V8");
+      v8 = ev ? atoi(ev) : 1;
+    }
+    if (m <= 8 * 4096 && !v8) return launch_cast_cluster<4>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
                                                      col_base, (m + 4095) / 4096, st);
     if (m <= 8 * 8192) return launch_cast_cluster<8>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
                                                      col_base, (m + 8191) / 8192, st);
