@@ -181,10 +181,36 @@ __device__ __forceinline__ void mgs_block(Smem& s, int nrows, int c0, int pw) {
     mgs_step_any<NT, RPT>(x, nrows, pw, k, qp, 1, s.Rb, 32, 1, false, nullptr, 0, s.red, buf);
 }
 
+// Columns [32, kCols) of block row r (zero-filled past the block and past the leaf): 4-byte
+// cp.async down each column (a warp covers 32 consecutive rows), waited for by the first PROJ.
+__device__ __forceinline__ void leaf_issue_rest(const LeafArgs& a, Smem& s, int nrows, int r) {
+  const int row0 = leaf_row(blockIdx.x, a.m, a.nb);
+  const float* src = a.X + row0 + min(r, nrows - 1);
+  float* dst = s.L + r * kLd;
+  const uint32_t sz = r < nrows ? 4u : 0u;  // 0: zero fill
+#pragma unroll 8
+  for (int j = 32; j < kCols; ++j) {
+    if (j < a.wl) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + j)),
+                   "l"(src + (long long)j * a.ldx), "r"(sz)
+                   : "memory");
+    } else {
+      dst[j] = 0.f;
+    }
+  }
+}
+
 // ---- PANEL ------------------------------------------------------------------------------------
 __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, int c0, int pw,
-                                        int& slot) {
+                                        int& slot, bool first) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  // first panel with the 128-thread MGS: the idle upper half issues the async loads of the leaf's
+  // later columns (two rows per thread) beside the MGS instead of before it
+  if (first && a.mgs_rpt == 2 && t >= kNT / 2) {
+    leaf_issue_rest(a, s, nrows, t - kNT / 2);
+    leaf_issue_rest(a, s, nrows, t);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   // (1) Alg. 4 on the block: RPT rows per thread over the first kNT / RPT threads (rows >= nrows
   // are zero and store nothing)
   if (a.mgs_rpt == 2) {
@@ -500,20 +526,8 @@ __global__ void __launch_bounds__(kNT, 1) leaf_kernel(const __grid_constant__ Le
 #pragma unroll 8
     for (int j = 0; j < 32; ++j) dst[j] = (ok && j < a.wl) ? src[(long long)j * a.ldx] : 0.f;
   }
-  {
-    const float* src = a.X + row0 + min(t, nrows - 1);
-    float* dst = s.L + t * kLd;
-    const uint32_t sz = t < nrows ? 4u : 0u;  // 0: zero fill
-#pragma unroll 8
-    for (int j = 32; j < kCols; ++j) {
-      if (j < a.wl) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + j)),
-                     "l"(src + (long long)j * a.ldx), "r"(sz)
-                     : "memory");
-      } else {
-        dst[j] = 0.f;
-      }
-    }
+  if (a.mgs_rpt != 2 || a.ops[0].kind != 0) {  // otherwise issued beside the first MGS
+    leaf_issue_rest(a, s, nrows, t);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   __syncthreads();
@@ -521,7 +535,7 @@ __global__ void __launch_bounds__(kNT, 1) leaf_kernel(const __grid_constant__ Le
   for (int o = 0; o < a.nops; ++o) {
     const LeafOp op = a.ops[o];
     if (op.kind == 0) {
-      leaf_panel(a, s, nrows, op.c0, op.h, slot);
+      leaf_panel(a, s, nrows, op.c0, op.h, slot, o == 0);
     } else if (op.h == 64) {
       if (op.w2 > 32)
         leaf_proj<64, 64>(a, s, nrows, op.c0, op.w2, slot);

@@ -34,7 +34,8 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
 
 // ---- K1 and friends (k_cast.cu) ----
 // Xh = fl16(X diag(s)); inv_s[j] = 1/s_j; status: atomicMin(1-based first non-finite column).
-// cmax: w uints of scratch for the split-row column max (may be null -> one CTA per column).
+// m <= 65536 with aligned pointers: one thread-block cluster per column (cmax unused).  Taller:
+// cmax = w uints of scratch for the split-row column max (may be null -> one CTA per column).
 cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
                        float* inv_s, int scaling, int* status, int col_base, unsigned int* cmax,
                        cudaStream_t st);
