@@ -200,9 +200,26 @@ __device__ __forceinline__ void leaf_issue_rest(const LeafArgs& a, Smem& s, int 
   }
 }
 
+// Row r of the block's final Q columns [c0, c0 + pw) to global (FP32 and the FP16 shadow).
+__device__ __forceinline__ void leaf_store_row(const LeafArgs& a, const Smem& s, int r, int c0,
+                                               int pw) {
+  const int row0 = leaf_row(blockIdx.x, a.m, a.nb);
+  const float* srcr = s.L + r * kLd + c0;
+  float* dst = a.X + row0 + r + (long long)c0 * a.ldx;
+  __half* dh = a.Xh ? a.Xh + row0 + r + (long long)c0 * a.ldh : nullptr;
+#pragma unroll 8
+  for (int j = 0; j < 32; ++j) {
+    if (j < pw) {
+      const float v = srcr[j];
+      __stcg(dst + (long long)j * a.ldx, v);
+      if (dh) dh[(long long)j * a.ldh] = __float2half_rn(v);
+    }
+  }
+}
+
 // ---- PANEL ------------------------------------------------------------------------------------
 __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, int c0, int pw,
-                                        int& slot, bool first) {
+                                        int& slot, bool first, int st_c0, int st_pw, bool defer) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   // first panel with the 128-thread MGS: the idle upper half issues the async loads of the leaf's
   // later columns (two rows per thread) beside the MGS instead of before it
@@ -210,6 +227,11 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     leaf_issue_rest(a, s, nrows, t - kNT / 2);
     leaf_issue_rest(a, s, nrows, t);
     asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // the previous panel's deferred Q stores, also beside this MGS (those columns are final)
+  if (st_pw > 0 && t >= kNT / 2) {
+    if (t - kNT / 2 < nrows) leaf_store_row(a, s, t - kNT / 2, st_c0, st_pw);
+    if (t < nrows) leaf_store_row(a, s, t, st_c0, st_pw);
   }
   // (1) Alg. 4 on the block: RPT rows per thread over the first kNT / RPT threads (rows >= nrows
   // are zero and store nothing)
@@ -353,22 +375,10 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
     a.dbg[104] = v;
   }
-  // these pw columns of Q are final (later ops only read them): stream them out now (FP32 and
-  // the FP16 shadow), coalesced down each column, overlapping the rest of the leaf
-  if (t < nrows) {
-    const int row0 = leaf_row(blockIdx.x, a.m, a.nb);
-    const float* srcr = s.L + t * kLd + c0;
-    float* dst = a.X + row0 + t + (long long)c0 * a.ldx;
-    __half* dh = a.Xh ? a.Xh + row0 + t + (long long)c0 * a.ldh : nullptr;
-#pragma unroll 8
-    for (int j = 0; j < 32; ++j) {
-      if (j < pw) {
-        const float v = srcr[j];
-        __stcg(dst + (long long)j * a.ldx, v);
-        if (dh) dh[(long long)j * a.ldh] = __float2half_rn(v);
-      }
-    }
-  }
+  // these pw columns of Q are final (later ops only read them): stream them out (FP32 and the
+  // FP16 shadow), coalesced down each column -- now, or (defer) by the idle upper half of the CTA
+  // beside the next panel's MGS
+  if (!defer && t < nrows) leaf_store_row(a, s, t, c0, pw);
   leaf_ts(a, slot);
 }
 
@@ -532,10 +542,17 @@ __global__ void __launch_bounds__(kNT, 1) leaf_kernel(const __grid_constant__ Le
   }
   __syncthreads();
   leaf_ts(a, slot);
+  int last_panel = 0;
+  for (int o = 0; o < a.nops; ++o)
+    if (a.ops[o].kind == 0) last_panel = o;
+  int st_c0 = 0, st_pw = 0;  // a panel's Q columns whose stores wait for the next panel's MGS
   for (int o = 0; o < a.nops; ++o) {
     const LeafOp op = a.ops[o];
     if (op.kind == 0) {
-      leaf_panel(a, s, nrows, op.c0, op.h, slot, o == 0);
+      const bool defer = a.mgs_rpt == 2 && o != last_panel;
+      leaf_panel(a, s, nrows, op.c0, op.h, slot, o == 0, st_c0, st_pw, defer);
+      st_c0 = op.c0;
+      st_pw = defer ? op.h : 0;
     } else if (op.h == 64) {
       if (op.w2 > 32)
         leaf_proj<64, 64>(a, s, nrows, op.c0, op.w2, slot);
