@@ -228,11 +228,7 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     leaf_issue_rest(a, s, nrows, t);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  // the previous panel's deferred Q stores, also beside this MGS (those columns are final)
-  if (st_pw > 0 && t >= kNT / 2) {
-    if (t - kNT / 2 < nrows) leaf_store_row(a, s, t - kNT / 2, st_c0, st_pw);
-    if (t < nrows) leaf_store_row(a, s, t, st_c0, st_pw);
-  }
+
   // (1) Alg. 4 on the block: RPT rows per thread over the first kNT / RPT threads (rows >= nrows
   // are zero and store nothing)
   if (a.mgs_rpt == 2) {
@@ -318,6 +314,12 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     }
 #pragma unroll 1
     for (int j = pw; j < 32; ++j) s.Sf[lane * 32 + j] = 0.f;
+  } else if (st_pw > 0 && warp != 4) {
+    // the previous panel's deferred Q stores (those columns are final) beside the one-warp
+    // Cholesky chain, on the six warps that do not share its scheduler (warp 4 does)
+    const int idx = (warp < 4 ? warp - 1 : warp - 2) * 32 + lane;
+    if (idx < nrows) leaf_store_row(a, s, idx, st_c0, st_pw);
+    if (idx + 192 < nrows) leaf_store_row(a, s, idx + 192, st_c0, st_pw);
   }
   __syncthreads();
   if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: Cholesky end
