@@ -71,7 +71,7 @@ typedef struct tcqr_config {
                         (Alg. 5 line 4); pass 1 then iterates on r0 = b - A x0 (default 0)      */
   int leaf_kernel;   /* 1: every leaf (w <= min(cutoff, 128), one GPU, m <= 148 * 256) runs as ONE
                         cooperative launch with 256-row blocks resident in shared memory and the
-                        Eq. (6) stack factored through its FP64 Gram matrix (reading R-A28);
+                        Eq. (6) stack factored through its FP64 Gram matrix (reading R-B1);
                         0: one pipelined MGS-root panel launch per 32 columns plus FP32
                         projection launches (default 1)                                         */
   int fp16_split;    /* 1: error-compensated FP16 split for the tensor-core split nodes (NEXT-4,

@@ -138,6 +138,25 @@ def _ptr(x):
     return ctypes.c_void_p(x.data_ptr())
 
 
+def _need(x, what, dtype, shape, device=None, ld=None):
+    """Validate a tensor argument before it reaches the C ABI (which trusts sizes and layouts):
+    CUDA residency, dtype, shape, and for matrices the column-major leading dimension."""
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise ValueError(f"{what}: expected a CUDA tensor")
+    if x.dtype != dtype:
+        raise ValueError(f"{what}: expected {dtype}, got {x.dtype}")
+    if tuple(x.shape) != tuple(shape):
+        raise ValueError(f"{what}: expected shape {tuple(shape)}, got {tuple(x.shape)}")
+    if device is not None and x.device != device:
+        raise ValueError(f"{what}: on {x.device}, expected {device}")
+    if len(shape) == 1:
+        if x.numel() > 1 and x.stride(0) != 1:
+            raise ValueError(f"{what}: expected a contiguous vector, got stride {x.stride()}")
+    elif ld is not None and _ld(x) != ld:
+        raise ValueError(f"{what}: expected leading dimension {ld}, got {_ld(x)}")
+
+
 _state = {"inited": False, "device": None, "ws": None}
 
 
@@ -219,13 +238,18 @@ def factor(A, Q=None, R=None, in_place=False):
     torch = _torch()
     _ensure()
     m, n = A.shape
+    _need(A, "A", torch.float32, (m, n))
     lda = _ld(A)
     if in_place:
+        if lda != m:
+            raise ValueError("in_place needs A with leading dimension m")
         Q = A
     elif Q is None:
         Q = colmajor_empty(m, n, device=A.device)
     if R is None:
         R = colmajor_empty(n, n, device=A.device)
+    _need(Q, "Q", torch.float32, (m, n), A.device, ld=m)
+    _need(R, "R", torch.float32, (n, n), A.device, ld=n)
     reserve_workspace(m, n, op=0)
     _check("tcqr_factor", lib().tcqr_factor(m, n, _ptr(A), lda, _ptr(Q), _ptr(R)))
     return Q, R
@@ -237,8 +261,11 @@ def lls_solve(A, b, tol=1e-10, maxit=200, x=None):
     torch = _torch()
     _ensure()
     m, n = A.shape
+    _need(A, "A", torch.float32, (m, n))
+    _need(b, "b", torch.float64, (m,), A.device)
     if x is None:
         x = torch.empty(n, dtype=torch.float64, device=A.device)
+    _need(x, "x", torch.float64, (n,), A.device)
     info = TcqrLlsInfo()
     reserve_workspace(m, n, op=1)
     _check("tcqr_lls_solve", lib().tcqr_lls_solve(m, n, _ptr(A), _ld(A), _ptr(b), _ptr(x),
@@ -252,8 +279,12 @@ def qr_solve(Q, R, b, x=None):
     torch = _torch()
     _ensure()
     m, n = Q.shape
+    _need(Q, "Q", torch.float32, (m, n))
+    _need(R, "R", torch.float32, (n, n), Q.device)
+    _need(b, "b", torch.float64, (m,), Q.device)
     if x is None:
         x = torch.empty(n, dtype=torch.float64, device=Q.device)
+    _need(x, "x", torch.float64, (n,), Q.device)
     _check("tcqr_qr_solve", lib().tcqr_qr_solve(m, n, _ptr(Q), _ld(Q), _ptr(R), _ld(R), _ptr(b),
                                                 _ptr(x)))
     return x

@@ -153,6 +153,10 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* _
   const int rank = (int)cluster.block_rank();
   const long long r0 = (long long)rank * RPC;
   const float* x = X + (long long)j * ldx;
+  // every CTA of the cluster must be running before any CTA touches a peer's shared memory: a
+  // relaxed arrive now, the matching wait just before the distributed stores (it overlaps the
+  // HBM loads below)
+  if (scaling) cluster.barrier_arrive();
   float4 v[V];
   float mx = 0.f;
   bool bad = false;
@@ -178,8 +182,10 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* _
   if (scaling) {
     mx = block_max(mx, red);
     const int nblk = (int)cluster.num_blocks();
-    // push this CTA's max into every peer's slot: after the one cluster barrier (release /
-    // acquire) each CTA reads only its own shared memory, so no second barrier keeps peers alive
+    // push this CTA's max into every peer's slot (all peers are running: the entry arrive /
+    // this wait); after the cluster barrier (release / acquire) each CTA reads only its own
+    // shared memory, so no further barrier keeps peers alive
+    cluster.barrier_wait();
     if ((int)threadIdx.x < nblk) *cluster.map_shared_rank(&cmv[rank], (int)threadIdx.x) = mx;
     cluster.sync();
     float g = 0.f;

@@ -14,7 +14,7 @@
 //         G = sum_b R_b' R_b (each product exact in FP64, fixed-order sums), R = chol(G), and the
 //         stack's Q slice of block b is S_b = R_b R^-1 (forward substitution, IEEE division).
 //         This is a QR of the stacked R's (G = R'R, diag(R) > 0 -- the unique R of Eq. (6) step
-//         (3)); reading R-A28 in DESIGN.md: the paper factors the stack with the same MGS kernel,
+//         (3)); reading R-B1 in DESIGN.md: the paper factors the stack with the same MGS kernel,
 //         here the FP64 Gram route takes the 32-step dependency chain out of FP32 block
 //         reductions (R is more accurate than the FP32 MGS R for kappa < ~1e7);
 //     (4) Q_b <- Q_b S_b in shared memory.
@@ -322,17 +322,11 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     if (idx + 192 < nrows) leaf_store_row(a, s, idx + 192, st_c0, st_pw);
   }
   __syncthreads();
-  if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: Cholesky end
+  if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: Cholesky + S end
     unsigned long long v;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
     a.dbg[102] = v;
   }
-  if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: S end
-    unsigned long long v;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
-    a.dbg[103] = v;
-  }
-  __syncthreads();
   leaf_ts(a, slot);
   if (blockIdx.x == 0) {  // the panel's R block (upper triangle; the lower one stays zero)
     for (int e = t; e < pw * pw; e += kNT) {
