@@ -223,6 +223,31 @@ int tcqr_profile_read(int cls, double* ms, double* flops, double* bytes, int* la
 /* Kernels launched by the most recent graph-replayed tcqr_factor (kernel nodes of its graph). */
 int tcqr_last_launch_count(void);
 
+/* Collectives (allreduce / allgather) enqueued by the calling context's most recent
+ * tcqr_factor or tcqr_lls_solve (0 at one rank). */
+int tcqr_last_collective_count(void);
+
+/* ---------------------------------------------------------------------------------------------
+ * Virtual ranks (test seam): the row-partitioned multi-GPU path of tcqr_factor /
+ * tcqr_lls_solve / tcqr_qr_solve run by P ranks inside ONE process on ONE device.  Each rank is a
+ * host thread with its own context (tcqr_init_virtual binds it to the calling thread; every
+ * tcqr_* call from that thread uses it; tcqr_finalize destroys it).  The collectives are the same
+ * calls in the same order as with NCCL (Eq. (6) with the ranks as the top tree level,
+ * PAPER.md:414-440, reading R-A26; R12 / A'r / ||q||^2 allreduces), carried out through the group's
+ * device staging slots: every rank combines the P contributions in rank order, so results are
+ * bitwise identical across ranks.  Each virtual rank's grids use 1/P of the SMs.  No CUDA graphs.
+ *   tcqr_vgroup_create: nranks in [1, 8]; slot_bytes >= the largest collective message (e.g.
+ *     4 n^2 for an n-column factor: the top R12 block is n^2/4 floats).  Allocates 2 * nranks
+ *     device slots on the current device.  Returns NULL on failure.
+ *   tcqr_init_virtual: rank in [0, nranks); the other arguments as tcqr_init.  Errors -3 group,
+ *     -4 rank, or tcqr_init's.  A rank whose call fails aborts the group: its peers' pending
+ *     collectives return TCQR_ERR_NCCL instead of waiting (host barrier timeout 120 s).
+ *   tcqr_vgroup_destroy: after every rank has called tcqr_finalize.
+ * ------------------------------------------------------------------------------------------- */
+void* tcqr_vgroup_create(int nranks, size_t slot_bytes);
+int tcqr_init_virtual(int device, void* cuda_stream, void* group, int rank);
+int tcqr_vgroup_destroy(void* group);
+
 /* Library build/version string. */
 const char* tcqr_version(void);
 

@@ -78,6 +78,10 @@ _SIGS = {
                                          ctypes.POINTER(ctypes.c_double),
                                          ctypes.POINTER(ctypes.c_int)]),
     "tcqr_last_launch_count": (ctypes.c_int, []),
+    "tcqr_last_collective_count": (ctypes.c_int, []),
+    "tcqr_vgroup_create": (ctypes.c_void_p, [ctypes.c_int, ctypes.c_size_t]),
+    "tcqr_init_virtual": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int]),
+    "tcqr_vgroup_destroy": (ctypes.c_int, [_P]),
 }
 PROFILE_CLASSES = ["copy", "k1_cast", "k3_tn", "k3_finalize", "k4_nn", "k2_mgs", "k2_apply",
                    "k2b_tn", "k2b_nn", "k5_gemv", "k6_tri", "k7_scalar", "trinv", "k2_leaf"]
@@ -406,6 +410,56 @@ def profile_read():
 
 def last_launch_count():
     return lib().tcqr_last_launch_count()
+
+
+def last_collective_count():
+    return lib().tcqr_last_collective_count()
+
+
+def run_virtual_ranks(nranks, fn, slot_bytes=64 << 20, device=0, timeout=600):
+    """Test seam (include/tcqr.h "Virtual ranks"): run ``fn(rank)`` on ``nranks`` host threads,
+    each bound to its own library context (tcqr_init_virtual) on ``device`` with its own CUDA
+    stream, sharing one virtual group whose collectives stand in for NCCL. ``fn`` calls the
+    C ABI through ``lib()`` directly (the module-level helpers use the process context).
+    Returns the list of fn's results; re-raises the first exception of any rank."""
+    import threading
+    torch = _torch()
+    l = lib()
+    torch.cuda.set_device(device)
+    g = l.tcqr_vgroup_create(int(nranks), int(slot_bytes))
+    if not g:
+        raise TcqrError("tcqr_vgroup_create", -1)
+    results, errors = [None] * nranks, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(device)
+            stream = torch.cuda.Stream(device=device)
+            _check("tcqr_init_virtual", l.tcqr_init_virtual(device, ctypes.c_void_p(
+                stream.cuda_stream), ctypes.c_void_p(g), r))
+            try:
+                with torch.cuda.stream(stream):
+                    results[r] = fn(r)
+                stream.synchronize()
+            finally:
+                l.tcqr_finalize()
+        except BaseException as e:  # noqa: BLE001 -- re-raised in the caller
+            errors.append((r, e))
+
+    threads = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(nranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout)
+    hung = [i for i, t in enumerate(threads) if t.is_alive()]
+    if not hung:
+        l.tcqr_vgroup_destroy(ctypes.c_void_p(g))
+    if hung:
+        raise TimeoutError(f"virtual ranks {hung} still running after {timeout} s")
+    if errors:
+        r, e = sorted(errors, key=lambda x: x[0])[0]
+        raise RuntimeError(f"virtual rank {r}: {e!r}") from e
+    return results
 
 
 def version():

@@ -28,10 +28,23 @@ cudaError_t cg_launch_tri_n(int n, const double* M, long long ldm, const double*
                             double* part, const int* done, cudaStream_t st);
 cudaError_t cg_launch_tri_t(int n, const double* M, long long ldm, const double* v, double* s,
                             const int* done, cudaStream_t st);
+// FP32 copy of the preconditioner M = R^-1 (reading R-A13): same products, FP64 accumulation.
+cudaError_t cg_launch_tri_n(int n, const float* M, long long ldm, const double* p, double* t,
+                            double* part, const int* done, cudaStream_t st);
+cudaError_t cg_launch_tri_t(int n, const float* M, long long ldm, const double* v, double* s,
+                            const int* done, cudaStream_t st);
+cudaError_t cg_launch_m_to_f32(int n, const double* M, long long ldm, float* M32, cudaStream_t st);
 cudaError_t cg_launch_a_n(int m, int n, const float* A, long long lda, const double* t, double* q,
                           double* part, double* dpart, const int* done, cudaStream_t st);
+// v = A' r (part: cg_gemv_t_part_count(m, n) doubles).  With q and cst: v = A' (r - alpha q),
+// alpha = cst->gamma / cst->delta, and r - alpha q is written to r_out (Alg. 5 line 17 fused).
+int cg_gemv_t_part_count(int m, int n);
 cudaError_t cg_launch_a_t(int m, int n, const float* A, long long lda, const double* r, double* v,
-                          const int* done, cudaStream_t st);
+                          double* part, const int* done, cudaStream_t st,
+                          const double* q = nullptr, const CgState* cst = nullptr,
+                          double* r_out = nullptr);
+// x += alpha t (alpha = gamma / delta), Alg. 5 line 16.
+cudaError_t cg_launch_update_x(int n, CgState* s, double* x, const double* t, cudaStream_t st);
 cudaError_t cg_launch_sum_parts(int np, const double* parts, double* out, const int* done,
                                 cudaStream_t st);
 cudaError_t cg_launch_update_xr(int m, int n, CgState* s, double* x, const double* t, double* r,

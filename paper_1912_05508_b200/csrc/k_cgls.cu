@@ -13,6 +13,8 @@
 //       the host only polls a done flag.
 #include "common.cuh"
 #include "kernels.h"
+#include <algorithm>
+
 #include "cgls_state.h"
 
 namespace tcqr {
@@ -377,9 +379,10 @@ cudaError_t trinv_f64(int n, const float* R, long long ldr, double* M, long long
 // Dense FP32 GEMVs with FP64 accumulation (K5)
 // ------------------------------------------------------------------------------------------
 constexpr int kGvRows = 256;  // rows per CTA (one per thread)
-constexpr int kGvCols = 128;  // columns per CTA chunk
+constexpr int kGvCols = 512;  // columns per CTA chunk (partials: m x n/512 doubles)
 
-// part[cb][i] = sum_{j in chunk cb} A[i, j] v[j]    (grid: row blocks x column chunks)
+// part[cb][i] = sum_{j in chunk cb} A[i, j] v[j]    (grid: row blocks x column chunks); eight
+// column loads in flight per thread, four FP64 accumulators (fixed order)
 __global__ void __launch_bounds__(kGvRows) gemv_n_part_kernel(int m, int n,
                                                               const float* __restrict__ A,
                                                               long long lda,
@@ -396,18 +399,17 @@ __global__ void __launch_bounds__(kGvRows) gemv_n_part_kernel(int m, int n,
   const long long i = (long long)blockIdx.x * kGvRows + threadIdx.x;
   if (i >= m) return;
   const float* a = A + i + (long long)j0 * lda;
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   int j = 0;
-  for (; j + 4 <= nc; j += 4) {
-    const float a0 = a[(long long)(j + 0) * lda], a1 = a[(long long)(j + 1) * lda];
-    const float a2 = a[(long long)(j + 2) * lda], a3 = a[(long long)(j + 3) * lda];
-    acc0 = fma((double)a0, vs[j + 0], acc0);
-    acc1 = fma((double)a1, vs[j + 1], acc1);
-    acc2 = fma((double)a2, vs[j + 2], acc2);
-    acc3 = fma((double)a3, vs[j + 3], acc3);
+  for (; j + 8 <= nc; j += 8) {
+    float av[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) av[u] = __ldg(a + (long long)(j + u) * lda);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u & 3] = fma((double)av[u], vs[j + u], acc[u & 3]);
   }
-  for (; j < nc; ++j) acc0 = fma((double)a[(long long)j * lda], vs[j], acc0);
-  part[(long long)cb * m + i] = (acc0 + acc1) + (acc2 + acc3);
+  for (; j < nc; ++j) acc[0] = fma((double)a[(long long)j * lda], vs[j], acc[0]);
+  part[(long long)cb * m + i] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 // y[i] = sum_cb part[cb][i] (fixed order); optional: dpart[block] = sum of y^2 over the block,
@@ -437,35 +439,105 @@ __global__ void __launch_bounds__(256) gemv_n_reduce_kernel(int m, int nchunks,
   }
 }
 
-// y[j] = sum_i A[i, j] v[i]: one warp per column, float4 loads, FP64 accumulate, butterfly sum.
-__global__ void __launch_bounds__(256) gemv_t_kernel(int m, int n, const float* __restrict__ A,
-                                                     long long lda, const double* __restrict__ v,
-                                                     double* __restrict__ y,
-                                                     const int* __restrict__ done) {
+// y[j] = sum_i A[i, j] v[i], column-blocked: a CTA takes 64 columns (8 per warp) of one row split;
+// v is staged in shared memory 1024 rows at a time and each of its values feeds the warp's 8
+// columns from registers (one warp per column re-read v from L2 once per column: 2x the bytes of
+// A).  Lanes read A down the columns in 16-byte pieces; FP64 accumulation; per-split partials
+// part[s * n + j] summed in split order by gemv_t_reduce_kernel (deterministic).
+// CGLS form (q != null): the staged values are r - alpha q (alpha = gamma / delta, Alg. 5 line 17
+// fused into the A' r pass), written to r_out by the CTAs of column block 0.
+constexpr int kGtCols = 64;
+constexpr int kGtChunk = 1024;
+
+__global__ void __launch_bounds__(256) gemv_t_part_kernel(int m, int n, const float* __restrict__ A,
+                                                          long long lda, const double* __restrict__ v,
+                                                          const double* __restrict__ q,
+                                                          const CgState* __restrict__ st,
+                                                          double* __restrict__ v_out, int rps,
+                                                          double* __restrict__ part,
+                                                          const int* __restrict__ done) {
   if (done && *done) return;
-  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (j >= n) return;
-  const float* a = A + (long long)j * lda;
-  double acc0 = 0.0, acc1 = 0.0;
+  __shared__ __align__(16) double vs[kGtChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = blockIdx.x * kGtCols + warp * 8;
+  const long long r_begin = (long long)blockIdx.y * rps;
+  const long long r_end = min((long long)m, r_begin + rps);
+  const double alpha = q ? st->gamma / st->delta : 0.0;
   const bool vec = ((lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
-  int i = 0;
-  if (vec) {
-    const int m4 = m & ~127;
-    for (i = lane * 4; i < m4; i += 128) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(a + i));
-      const double2 v0 = *reinterpret_cast<const double2*>(v + i);
-      const double2 v1 = *reinterpret_cast<const double2*>(v + i + 2);
-      acc0 = fma((double)x.x, v0.x, acc0);
-      acc1 = fma((double)x.y, v0.y, acc1);
-      acc0 = fma((double)x.z, v1.x, acc0);
-      acc1 = fma((double)x.w, v1.y, acc1);
+  double acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+  for (long long c = r_begin; c < r_end; c += kGtChunk) {
+    const int cn = (int)min((long long)kGtChunk, r_end - c);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn; i += 256) {
+      double x = v[c + i];
+      if (q) {
+        x = fma(-alpha, q[c + i], x);
+        if (blockIdx.x == 0) v_out[c + i] = x;
+      }
+      vs[i] = x;
     }
-    i = m4;
+    __syncthreads();
+    if (vec && cn == kGtChunk) {
+#pragma unroll 2
+      for (int i = lane * 4; i < kGtChunk; i += 128) {
+        const double2 v01 = *reinterpret_cast<const double2*>(vs + i);
+        const double2 v23 = *reinterpret_cast<const double2*>(vs + i + 2);
+        float4 a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          a[u] = (j0 + u < n) ? __ldg(reinterpret_cast<const float4*>(A + (long long)(j0 + u) * lda + c + i))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc[u] = fma((double)a[u].x, v01.x, acc[u]);
+          acc[u] = fma((double)a[u].y, v01.y, acc[u]);
+          acc[u] = fma((double)a[u].z, v23.x, acc[u]);
+          acc[u] = fma((double)a[u].w, v23.y, acc[u]);
+        }
+      }
+    } else {
+      for (int i = lane; i < cn; i += 32) {
+        const double x = vs[i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j0 + u < n) acc[u] = fma((double)A[(long long)(j0 + u) * lda + c + i], x, acc[u]);
+      }
+    }
   }
-  for (int ii = i + lane; ii < m; ii += 32) acc0 = fma((double)a[ii], v[ii], acc0);
-  const double s = warp_sum_d(acc0 + acc1);
-  if (lane == 0) y[j] = s;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double sum = warp_sum_d(acc[u]);
+    if (lane == 0 && j0 + u < n) part[(long long)blockIdx.y * n + j0 + u] = sum;
+  }
+}
+
+__global__ void gemv_t_reduce_kernel(int n, int splits, const double* __restrict__ part,
+                                     double* __restrict__ y, const int* __restrict__ done) {
+  if (done && *done) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double acc = part[j];
+  for (int s = 1; s < splits; ++s) acc += part[(long long)s * n + j];
+  y[j] = acc;
+}
+
+// Row splits of the A' v kernel: enough CTAs for two per SM, splits of whole 1024-row chunks.
+static void gemv_t_plan(int m, int n, int* splits, int* rps) {
+  const int cblocks = (n + kGtCols - 1) / kGtCols;
+  int s = (2 * 148 + cblocks - 1) / cblocks;
+  const int chunks = (m + kGtChunk - 1) / kGtChunk;
+  s = std::max(1, std::min(s, chunks));
+  const int cps = (chunks + s - 1) / s;
+  *rps = cps * kGtChunk;
+  *splits = (m + *rps - 1) / *rps;
+}
+
+int cg_gemv_t_part_count(int m, int n) {
+  int s, rps;
+  gemv_t_plan(m, n, &s, &rps);
+  return s * n;
 }
 
 cudaError_t gemv_f32_n(int m, int n, const float* A, long long lda, const double* v, double* y,
@@ -479,8 +551,12 @@ cudaError_t gemv_f32_n(int m, int n, const float* A, long long lda, const double
 }
 
 cudaError_t gemv_f32_t(int m, int n, const float* A, long long lda, const double* v, double* y,
-                       cudaStream_t st) {
-  gemv_t_kernel<<<(n + 7) / 8, 256, 0, st>>>(m, n, A, lda, v, y, nullptr);
+                       double* part, cudaStream_t st) {
+  int splits, rps;
+  gemv_t_plan(m, n, &splits, &rps);
+  gemv_t_part_kernel<<<dim3((n + kGtCols - 1) / kGtCols, splits), 256, 0, st>>>(
+      m, n, A, lda, v, nullptr, nullptr, nullptr, rps, part, nullptr);
+  gemv_t_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, splits, part, y, nullptr);
   return cudaGetLastError();
 }
 
@@ -490,7 +566,8 @@ cudaError_t gemv_f32_t(int m, int n, const float* A, long long lda, const double
 constexpr int kTriBlk = 256;
 
 // part[cb][i] = sum_{j in chunk cb, j >= i} M[i, j] p[j], only for chunks cb >= row block.
-__global__ void __launch_bounds__(kTriBlk) tri_n_part_kernel(int n, const double* __restrict__ M,
+template <typename TM>
+__global__ void __launch_bounds__(kTriBlk) tri_n_part_kernel(int n, const TM* __restrict__ M,
                                                              long long ldm,
                                                              const double* __restrict__ p,
                                                              double* __restrict__ part,
@@ -505,18 +582,18 @@ __global__ void __launch_bounds__(kTriBlk) tri_n_part_kernel(int n, const double
   __syncthreads();
   const int i = rb * kTriBlk + threadIdx.x;
   if (i >= n) return;
-  const double* mm = M + i + (long long)j0 * ldm;
+  const TM* mm = M + i + (long long)j0 * ldm;
   // 8 loads in flight per thread (with 2 the kernel ran at 3.5 TB/s)
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   int j = 0;
   for (; j + 8 <= nc; j += 8) {
-    double mv[8];
+    TM mv[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) mv[u] = __ldg(mm + (long long)(j + u) * ldm);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u & 3] = fma(mv[u], ps[j + u], acc[u & 3]);
+    for (int u = 0; u < 8; ++u) acc[u & 3] = fma((double)mv[u], ps[j + u], acc[u & 3]);
   }
-  for (; j < nc; ++j) acc[0] = fma(mm[(long long)j * ldm], ps[j], acc[0]);
+  for (; j < nc; ++j) acc[0] = fma((double)mm[(long long)j * ldm], ps[j], acc[0]);
   part[(long long)cb * n + i] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
@@ -564,6 +641,54 @@ __global__ void __launch_bounds__(256) tri_t_kernel(int n, const double* __restr
   for (i += lane; i <= j; i += 32) a0 = fma(mm[i], v[i], a0);
   const double r = warp_sum_d(a0 + a1);
   if (lane == 0) s[j] = r;
+}
+
+// The same with M stored in FP32 (the CGLS preconditioner, reading R-A13): 16-byte loads of four
+// rows, two in flight per lane (256 rows per warp step).
+__global__ void __launch_bounds__(256) tri_t_f32_kernel(int n, const float* __restrict__ M,
+                                                        long long ldm, const double* __restrict__ v,
+                                                        double* __restrict__ s,
+                                                        const int* __restrict__ done) {
+  if (done && *done) return;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const float* mm = M + (long long)j * ldm;
+  double a0 = 0.0, a1 = 0.0;
+  int i = 0;
+  if ((ldm & 3) == 0 && (reinterpret_cast<uintptr_t>(M) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+    const int j256 = ((j + 1) / 256) * 256;
+    for (; i < j256; i += 256) {
+      float4 mv[2];
+      double2 vv[4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        mv[u] = __ldg(reinterpret_cast<const float4*>(mm + i + 128 * u + 4 * lane));
+        vv[2 * u] = *reinterpret_cast<const double2*>(v + i + 128 * u + 4 * lane);
+        vv[2 * u + 1] = *reinterpret_cast<const double2*>(v + i + 128 * u + 4 * lane + 2);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        a0 = fma((double)mv[u].x, vv[2 * u].x, a0);
+        a1 = fma((double)mv[u].y, vv[2 * u].y, a1);
+        a0 = fma((double)mv[u].z, vv[2 * u + 1].x, a0);
+        a1 = fma((double)mv[u].w, vv[2 * u + 1].y, a1);
+      }
+    }
+  }
+  for (i += lane; i <= j; i += 32) a0 = fma((double)mm[i], v[i], a0);
+  const double r = warp_sum_d(a0 + a1);
+  if (lane == 0) s[j] = r;
+}
+
+// M32 = fl32(M) on the upper triangle (zero below): the FP32 copy of the CGLS preconditioner.
+__global__ void m_to_f32_kernel(int n, const double* __restrict__ M, long long ldm,
+                                float* __restrict__ M32) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * n) return;
+  const int i = (int)(e % n), j = (int)(e / n);
+  M32[e] = i <= j ? (float)M[i + (long long)j * ldm] : 0.f;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -713,7 +838,16 @@ cudaError_t cg_launch_tri_n(int n, const double* M, long long ldm, const double*
                             double* part, const int* done, cudaStream_t st) {
   const int nch = cg_tri_chunks(n);
   dim3 g(nch, nch);
-  tri_n_part_kernel<<<g, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
+  tri_n_part_kernel<double><<<g, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
+  tri_n_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, nch, part, t, done);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_tri_n(int n, const float* M, long long ldm, const double* p, double* t,
+                            double* part, const int* done, cudaStream_t st) {
+  const int nch = cg_tri_chunks(n);
+  dim3 g(nch, nch);
+  tri_n_part_kernel<float><<<g, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
   tri_n_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, nch, part, t, done);
   return cudaGetLastError();
 }
@@ -721,6 +855,23 @@ cudaError_t cg_launch_tri_n(int n, const double* M, long long ldm, const double*
 cudaError_t cg_launch_tri_t(int n, const double* M, long long ldm, const double* v, double* s,
                             const int* done, cudaStream_t st) {
   tri_t_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, M, ldm, v, s, done);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_tri_t(int n, const float* M, long long ldm, const double* v, double* s,
+                            const int* done, cudaStream_t st) {
+  tri_t_f32_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, M, ldm, v, s, done);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_m_to_f32(int n, const double* M, long long ldm, float* M32, cudaStream_t st) {
+  const long long nn = (long long)n * n;
+  m_to_f32_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(n, M, ldm, M32);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_launch_update_x(int n, CgState* s, double* x, const double* t, cudaStream_t st) {
+  cg_update_xr_kernel<<<(n + 255) / 256, 256, 0, st>>>(0, n, s, x, t, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -735,8 +886,13 @@ cudaError_t cg_launch_a_n(int m, int n, const float* A, long long lda, const dou
 }
 
 cudaError_t cg_launch_a_t(int m, int n, const float* A, long long lda, const double* r, double* v,
-                          const int* done, cudaStream_t st) {
-  gemv_t_kernel<<<(n + 7) / 8, 256, 0, st>>>(m, n, A, lda, r, v, done);
+                          double* part, const int* done, cudaStream_t st, const double* q,
+                          const CgState* cst, double* r_out) {
+  int splits, rps;
+  gemv_t_plan(m, n, &splits, &rps);
+  gemv_t_part_kernel<<<dim3((n + kGtCols - 1) / kGtCols, splits), 256, 0, st>>>(
+      m, n, A, lda, r, q, cst, r_out, rps, part, done);
+  gemv_t_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, splits, part, v, done);
   return cudaGetLastError();
 }
 

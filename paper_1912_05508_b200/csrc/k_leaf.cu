@@ -7,17 +7,20 @@
 // host flattens it into a short program of ops that the kernel runs in order:
 //
 //   PANEL(c0, pw)   Eq. (6) on columns [c0, c0+pw):
-//     (1) every CTA runs Alg. 4 (MGS) on its 256 x pw block -- the paper's
-//         256 x 32 submatrix with one row per thread -- Q_b in place in shared
-//         memory, R_b (pw x pw) in shared memory;
+//     (1) Alg. 4 (MGS) on every 64 x pw block of the CTA's rows -- four blocks
+//         per CTA, one warp each (the paper's 256 x 32 submatrices, cut to 64
+//         rows so a block's reductions stay inside one warp: lane j holds column j of the block,
+//         the pivot column and the normalized q_k are broadcast through shared memory, every
+//         norm and dot is a lane-local FFMA2 chain; no CTA barrier per MGS step).  Q_b in place
+//         in shared memory, R_b (pw x pw, FP64) in shared memory;
 //     (2)-(3) the stack [R_1; ...; R_nb] is factored through its Gram matrix in FP64:
-//         G = sum_b R_b' R_b (each product exact in FP64, fixed-order sums), R = chol(G), and the
-//         stack's Q slice of block b is S_b = R_b R^-1 (forward substitution, IEEE division).
-//         This is a QR of the stacked R's (G = R'R, diag(R) > 0 -- the unique R of Eq. (6) step
-//         (3)); reading R-B1 in DESIGN.md: the paper factors the stack with the same MGS kernel,
-//         here the FP64 Gram route takes the 32-step dependency chain out of FP32 block
-//         reductions (R is more accurate than the FP32 MGS R for kappa < ~1e7);
-//     (4) Q_b <- Q_b S_b in shared memory.
+//         G = sum_b R_b' R_b (each product exact in FP64, fixed-order sums), R = chol(G) (one
+//         warp, redundantly in every CTA), and the stack's Q slice of block b is S_b = R_b R^-1
+//         (forward substitution, one warp per block, after the Cholesky).  This is a QR of the
+//         stacked R's (G = R'R, diag(R) > 0 -- the unique R of Eq. (6) step (3)); reading R-B1 in
+//         the paper factors the stack with the same MGS kernel, here the FP64 Gram
+//         route takes the 32-step dependency chain out of FP32 block reductions;
+//     (4) Q_b <- Q_b S_b in shared memory (S_b upper triangular: only its nonzero terms).
 //   PROJ(c0, h, w2) Alg. 2 lines 8-9 in FP32 below the cutoff: R12 = Q1' A2 (per-CTA partial over
 //     its rows, fixed-order sum over the CTAs), R block <- R12, A2 -= Q1 R12.
 //
@@ -29,18 +32,21 @@
 
 #include "common.cuh"
 #include "kernels.h"
-#include "mgs.cuh"
 
 namespace tcqr {
 
 namespace {
 
-constexpr int kNT = 256;      // threads per CTA; thread t owns row t of the block
+constexpr int kNT = 256;      // threads per CTA
 constexpr int kRows = 256;    // rows per CTA (max)
 constexpr int kCols = 128;    // leaf width (max)
 constexpr int kLd = 132;      // shared row stride in floats: 16-byte rows, 4 floats of skew
 constexpr int kMaxOps = 16;
 constexpr int kNW = kNT / 32;
+constexpr int kBR = 64;       // rows per MGS block (4^3: powers of 4 keep the planted pin exact)
+constexpr int kMW = kRows / kBR;  // MGS blocks (= warps) per CTA: one per SM sub-partition
+constexpr int kLdR = 33;      // ld of the blocks' R_b (FP64) in shared memory
+constexpr int kLdS = 34;      // ld of the blocks' S_b (FP32; even: 8-byte pairs for FFMA2)
 
 struct LeafOp {
   int kind;  // 0 panel (c0, h = width), 1 projection (c0, h, w2)
@@ -61,37 +67,56 @@ struct LeafArgs {
   float* ppart;   // nb x 4096 projection partials
   float* r12;     // 4096
   unsigned* bar;  // grid barrier arrival counter (zeroed before the factorization's first leaf)
-  unsigned bar_base;  // barriers completed before this launch (the host counts them)
-  int* status;
+  unsigned bar_base;  // counter arrivals of the earlier launches (the host counts them)
+  int* status;    // breakdown status (null: local leaf of a rank, zero norms allowed, R-A8)
   int col0;       // global column of the leaf's column 0 (breakdown codes)
   unsigned long long* dbg;  // optional phase timestamps of CTA 0 (globaltimer ns), 128 slots
-  int mgs_rpt;    // rows per thread of the block MGS (2: 128 threads (default), 1: 256 threads)
 };
 
 struct Smem {
-  float L[kRows * kLd];  // the block's rows of the leaf, row-major
-  float Rb[32 * 32];     // R_b of the current panel, row-major
-  float Sf[32 * 32];     // S_b (FP32), row-major [l][j]
-  double Rd[32 * 34 + 34];  // the panel's R in FP64, row-major (ld 34; one row of slack)
-  double Rbd[32 * 32];   // R_b widened to FP64, row-major
-  float T[4096];         // R12 (row-major [i][w2p]) / projection group partials
-  float red[2 * kNW * 32];
-  float wsum[kNW * 32];  // per-warp partial sums of the cross-CTA reductions
-  unsigned barseq;       // grid barriers passed by this CTA in this launch (thread 0)
+  float L[kRows * kLd];        // the block's rows of the leaf, row-major
+  double Rbd[kMW][32 * kLdR];  // R_b of each MGS block of the current panel, row-major (FP64)
+  union {
+    float T[4096];             // PROJ: R12 (row-major [i][w2p]) / group partials; Gram wsum
+    float Sf[kMW][32 * kLdS];  // PANEL: S_b of each block (FP32), row-major [l][j]
+    double Gp[kMW][528];       // PANEL: each block's Gram R_b' R_b, packed upper triangle
+  } u;
+  double Rd[32 * 34 + 34];     // the panel's R in FP64, row-major (ld 34; one row of slack)
+  double rowb[kMW][2][64];     // Cholesky: row k of R twice over, per chain warp (step parity)
+  float colbuf[kMW][kBR];      // MGS: the pivot column of each block
+  float qbuf[kMW][kBR];        // MGS: q_k of each block
+  float wsum[kNW * 32];        // per-warp partial sums of the cross-CTA reductions
+  unsigned barseq;             // grid barriers passed by this CTA in this launch (thread 0)
 };
 
 // Grid barrier on a monotonic arrival counter: barrier i of this launch completes when the
-// counter reaches (bar_base + i) * nb.  Fire-and-forget release arrival, relaxed polling, one
-// acquire load at the end (the CTA barriers carry the ordering to the other threads).
+// counter reaches bar_base + i * nb (bar_base = the arrivals of every earlier launch of the
+// factorization, whatever their grid sizes).  Fire-and-forget release arrival, relaxed polling,
+// one acquire load at the end (the CTA barriers carry the ordering to the other threads).
+// Watchdog: a barrier still open after 2 s (a co-residency failure) is abandoned and the launch
+// reports TCQR_ERR_CUDA through the status word, so a bug fails the call instead of hanging the
+// device.
 __device__ __forceinline__ void leaf_barrier(const LeafArgs& a, Smem& s) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned target = (a.bar_base + (++s.barseq)) * (unsigned)a.nb;
+    const unsigned target = a.bar_base + (++s.barseq) * (unsigned)a.nb;
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
     unsigned v;
-    do {
+    unsigned long long t0 = 0;
+    for (unsigned it = 0;; ++it) {
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
-    } while (v < target);
+      if ((int)(v - target) >= 0) break;
+      if ((it & 4095) == 0) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > 2000000000ull) {
+          if (a.status) atomicMin(a.status, -1001);
+          break;
+        }
+      }
+    }
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
   }
   __syncthreads();
@@ -150,35 +175,92 @@ __device__ __forceinline__ void cross_sum(const T* part, long long pstride, int 
   }
 }
 
-// Alg. 4 on the block's rows of columns [c0, c0 + pw): thread t < kNT / RPT holds rows
-// t + r kNT / RPT; Q_b in place in shared memory, R_b row-major into s.Rb.
-template <int RPT>
-__device__ __forceinline__ void mgs_block(Smem& s, int nrows, int c0, int pw) {
-  constexpr int NT = kNT / RPT;
-  const int t = threadIdx.x;
-  if (t >= NT) return;
-  float x[RPT][32];
-  float* qp[RPT];
+// Alg. 4 on MGS block `blk` = rows [64 blk, 64 blk + 64) of the CTA, columns
+// [c0, c0 + pw), by one warp.  Lane j holds column j of the block (rows in FP32 pairs, FFMA2).
+// Step k: the pivot column x_k (published in colbuf by lane k) is broadcast to every lane; lane j
+// forms a_k' a_j over the block's 64 rows (lane k: the norm^2); R(k, k) = sqrt, one correctly
+// rounded reciprocal (reading R-B2); R(k, j) = (a_k' a_j) / R(k, k) (R-A7); q_k = x_k / R(k, k)
+// (line 6) is formed once per row (lane r: rows r, r + 32), broadcast through qbuf and written to
+// L as the block's final Q column k; lines 7-8 update every lane's column by FFMA2.  A locally
+// zero norm gives q = 0, r = 0 (R-A8; only the stack's Cholesky reports breakdowns).  Afterwards
+// the warp forms the block's Gram R_b' R_b (FP64, packed upper triangle) for the stack.
+__device__ __forceinline__ void mgs_warp(Smem& s, int blk, int c0, int pw) {
+  const int lane = threadIdx.x & 31;
+  const int r0 = blk * kBR;
+  float* colb = s.colbuf[blk];
+  float* qb = s.qbuf[blk];
+  double* Rb = s.Rbd[blk];
+  float2 x[kBR / 2];  // x[i] = rows (r0 + 2i, r0 + 2i + 1) of column c0 + lane
 #pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int row = t + r * NT;
-    const float* src = s.L + row * kLd + c0;
+  for (int i = 0; i < kBR / 2; ++i)
+    x[i] = make_float2(s.L[(r0 + 2 * i) * kLd + c0 + lane], s.L[(r0 + 2 * i + 1) * kLd + c0 + lane]);
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) Rb[k * kLdR + lane] = 0.0;
+  if (lane == 0) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 v = *reinterpret_cast<const float4*>(src + 4 * q);
-      x[r][4 * q] = v.x;
-      x[r][4 * q + 1] = v.y;
-      x[r][4 * q + 2] = v.z;
-      x[r][4 * q + 3] = v.w;
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j >= pw) x[r][j] = 0.f;
-    qp[r] = row < nrows ? s.L + row * kLd + c0 : nullptr;
+    for (int i = 0; i < kBR / 4; ++i)
+      *reinterpret_cast<float4*>(colb + 4 * i) = make_float4(x[2 * i].x, x[2 * i].y, x[2 * i + 1].x,
+                                                             x[2 * i + 1].y);
   }
-  int buf = 0;
-  for (int k = 0; k < pw; ++k)
-    mgs_step_any<NT, RPT>(x, nrows, pw, k, qp, 1, s.Rb, 32, 1, false, nullptr, 0, s.red, buf);
+  __syncwarp();
+#pragma unroll 1
+  for (int k = 0; k < pw; ++k) {
+    float2 v[kBR / 2];
+#pragma unroll
+    for (int i = 0; i < kBR / 4; ++i) {
+      const float4 c4 = *reinterpret_cast<const float4*>(colb + 4 * i);
+      v[2 * i] = make_float2(c4.x, c4.y);
+      v[2 * i + 1] = make_float2(c4.z, c4.w);
+    }
+    float2 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < kBR / 2; ++i) acc[i & 3] = ffma2(v[i], x[i], acc[i & 3]);
+    const float tot = ((acc[0].x + acc[0].y) + (acc[1].x + acc[1].y)) +
+                      ((acc[2].x + acc[2].y) + (acc[3].x + acc[3].y));
+    const float rkk = sqrtf(__shfl_sync(0xffffffffu, tot, k));
+    const bool zero = !(rkk > 0.f) || !isfinite(rkk);
+    const float inv = zero ? 0.f : 1.0f / rkk;  // correctly rounded: the bits of __frcp_rn
+    const float rkj = zero ? 0.f : (lane == k ? rkk : tot * inv);
+    if (lane >= k && lane < pw) Rb[k * kLdR + lane] = (double)rkj;
+    const float q0 = colb[lane] * inv, q1 = colb[lane + 32] * inv;
+    __syncwarp();  // every lane has read colb before lane k + 1 republishes it below
+    qb[lane] = q0;
+    qb[lane + 32] = q1;
+    s.L[(r0 + lane) * kLd + c0 + k] = q0;
+    s.L[(r0 + lane + 32) * kLd + c0 + k] = q1;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < kBR / 4; ++i) {
+      const float4 q4 = *reinterpret_cast<const float4*>(qb + 4 * i);
+      v[2 * i] = make_float2(q4.x, q4.y);
+      v[2 * i + 1] = make_float2(q4.z, q4.w);
+    }
+    const float2 nr = make_float2(-rkj, -rkj);
+#pragma unroll
+    for (int i = 0; i < kBR / 2; ++i) x[i] = ffma2(v[i], nr, x[i]);  // x_j - q_k R(k, j)
+    if (lane == k + 1) {
+#pragma unroll
+      for (int i = 0; i < kBR / 4; ++i)
+        *reinterpret_cast<float4*>(colb + 4 * i) =
+            make_float4(x[2 * i].x, x[2 * i].y, x[2 * i + 1].x, x[2 * i + 1].y);
+    }
+    __syncwarp();
+  }
+  // the block's Gram G_b(i, j) = sum_{l <= i} R_b(l, i) R_b(l, j), i <= j (lane j: column j of
+  // R_b in registers, R_b(l, i) broadcast), packed upper triangle into u.Gp[blk]
+  double rj[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) rj[l] = Rb[l * kLdR + lane];
+  double* gp = s.u.Gp[blk];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double g = 0.0;
+#pragma unroll
+    for (int l = 0; l <= i; ++l) g = fma(Rb[l * kLdR + i], rj[l], g);
+    if (i <= lane) gp[lane * (lane + 1) / 2 + i] = g;
+  }
 }
 
 // Columns [32, kCols) of block row r (zero-filled past the block and past the leaf): 4-byte
@@ -221,40 +303,33 @@ __device__ __forceinline__ void leaf_store_row(const LeafArgs& a, const Smem& s,
 __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, int c0, int pw,
                                         int& slot, bool first, int st_c0, int st_pw, bool defer) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  // first panel with the 128-thread MGS: the idle upper half issues the async loads of the leaf's
-  // later columns (two rows per thread) beside the MGS instead of before it
-  if (first && a.mgs_rpt == 2 && t >= kNT / 2) {
+  // first panel: the upper half (warps 4-7, idle during the MGS) issues the async loads of the
+  // leaf's later columns (two rows per thread) beside the MGS instead of before it
+  if (first && t >= kNT / 2) {
     leaf_issue_rest(a, s, nrows, t - kNT / 2);
     leaf_issue_rest(a, s, nrows, t);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-
-  // (1) Alg. 4 on the block: RPT rows per thread over the first kNT / RPT threads (rows >= nrows
-  // are zero and store nothing)
-  if (a.mgs_rpt == 2) {
-    mgs_block<2>(s, nrows, c0, pw);
-  } else {
-    mgs_block<1>(s, nrows, c0, pw);
-  }
+  // (1) Alg. 4 on the CTA's four 64-row blocks, one warp each (rows >= nrows are zero), and each
+  // block's Gram R_b' R_b
+  if (warp < kMW) mgs_warp(s, warp, c0, pw);
   __syncthreads();
   leaf_ts(a, slot);
-  // (2) this block's Gram G_b = R_b' R_b (upper triangle), FP64.  R_b is widened to FP64 once
-  // (the FP32 -> FP64 conversions run at 1/8 of the FMA rate: widening inside the product loop
-  // cost ~1 us per panel)
-  for (int e = t; e < 1024; e += kNT) s.Rbd[e] = (double)s.Rb[e];
-  __syncthreads();
+  // (2) the CTA's part of the stack's Gram: G = (G_0 + G_1) + (G_2 + G_3) (FP64, fixed order;
+  // zero below the diagonal and past the panel)
   for (int e = t; e < 1024; e += kNT) {
     const int i = e >> 5, j = e & 31;
     double g = 0.0;
     if (i <= j && j < pw) {
-      for (int l = 0; l <= i; ++l) g = fma(s.Rbd[l * 32 + i], s.Rbd[l * 32 + j], g);
+      const int pk = j * (j + 1) / 2 + i;
+      g = (s.u.Gp[0][pk] + s.u.Gp[1][pk]) + (s.u.Gp[2][pk] + s.u.Gp[3][pk]);
     }
     a.gpart[(long long)blockIdx.x * 1024 + e] = g;
   }
   leaf_barrier(a, s);
   leaf_ts(a, slot);
-  cross_sum<double>(a.gpart, 1024, 1024, a.nb, a.gsum, reinterpret_cast<double*>(s.T), nullptr, 0,
-                    0, 0, 1, 0, false);
+  cross_sum<double>(a.gpart, 1024, 1024, a.nb, a.gsum, reinterpret_cast<double*>(s.u.T), nullptr,
+                    0, 0, 0, 1, 0, false);
   leaf_ts(a, slot);
   leaf_barrier(a, s);
   leaf_ts(a, slot);
@@ -263,27 +338,25 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
     a.dbg[100] = v;
   }
-  // (3) R = chol(G) and S_b = R_b R^-1 in warp 0, one ROLLED pass over k (the fully unrolled
-  // 32-step chain was ~100 KB of straight-line code run once per panel: instruction-fetch bound).
-  // Lane j holds column j of the trailing Gram, c[i] = W(k+i, j) (shifted down one slot per step,
-  // so the pivot is always c[0]), and row j of S_b under forward substitution, r[i] = the running
-  // value of column k+i.  Step k: the pivot G(k,k) from lane k by shuffle, one FP64 reciprocal
-  // square root (1/R(k,k), <= 1 ulp: R(k,j) = W(k,j) / R(k,k) and the S_b quotients become
-  // products; FP64 values within an ulp round to the same FP32 R and Q, exact inputs stay exact
-  // -- the planted pin), row k of R broadcast through shared memory.
-  if (warp == 0) {
+  // (3) R = chol(G) and S_b = R_b R^-1, in warps 0-3 (one per SM sub-partition): warp b runs the
+  // Cholesky redundantly (same inputs, same code: the same R bits in every warp and CTA) with the
+  // forward substitution of ITS block's R_b fused in.  One ROLLED pass over k (a fully unrolled
+  // 32-step chain is instruction-fetch bound).  Lane j holds column j of the trailing Gram, c[i] =
+  // W(k+i, j) (shifted down one slot per step, so the pivot is always c[0]), and row j of S_b, r[i]
+  // = the running value of column k+i.  Step k: the pivot G(k,k) by shuffle, one FP64 reciprocal
+  // square root ri = 1/R(k,k) (<= 1 ulp; R(k,j) = W(k,j) ri and the substitution's quotients
+  // become products; FP64 values within an ulp round to the same FP32 R and Q, exact inputs stay
+  // exact -- the planted pin), row k of R broadcast through the warp's row buffer.  The pivot of
+  // step k+1 comes from lane k+1's own values (its update of W(k+1,k+1) with its own R(k,k+1)), so
+  // shuffle -> rsqrt starts before the row is in shared memory.
+  if (warp < kMW) {
+    const double* Rb = s.Rbd[warp];
+    float* Sf = s.u.Sf[warp];
     double c[32], r[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) c[i] = (i <= lane && lane < pw) ? __ldcg(a.gsum + i * 32 + lane) : 0.0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) r[j] = (lane < pw && j < pw) ? s.Rbd[lane * 32 + j] : 0.0;
-    if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: Cholesky inputs loaded
-      unsigned long long v;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v) : "d"(c[31]), "d"(r[31]));
-      a.dbg[101] = v;
-    }
-    // software-pipelined: the pivot of step k+1 (lane k+1's first update -> shuffle -> rsqrt) is
-    // issued at the top of step k's trailing updates; branch-free so it all schedules together
+    for (int j = 0; j < 32; ++j) r[j] = (lane < pw && j < pw) ? Rb[lane * kLdR + j] : 0.0;
     double d = __shfl_sync(0xffffffffu, c[0], 0);
     bool ok = d > 0.0 && d <= 1.7976931348623157e308;
     double ri = rsqrt_nr(ok ? d : 1.0);
@@ -291,20 +364,25 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     for (int k = 0; k < pw; ++k) {
       ri = ok ? ri : 0.0;
       const double rkj = lane == k ? d * ri : (lane > k ? c[0] * ri : 0.0);
-      s.Rd[k * 34 + lane] = rkj;
-      if (!ok && lane == 0 && blockIdx.x == 0 && a.status) atomicMin(a.status, a.col0 + c0 + k + 1);
-      const double sk = r[0] * ri;
-      s.Sf[lane * 32 + k] = (float)sk;
-      __syncwarp();
-      const double* rk = s.Rd + k * 34 + k + 1;  // R(k, k+1+i); entries past column 31 are unused
-      const double v0 = rk[0];
-      c[0] = fma(-v0, rkj, c[1]);
-      r[0] = fma(-sk, v0, r[1]);
-      d = __shfl_sync(0xffffffffu, c[0], (k + 1) & 31);  // next pivot (unused after the last step)
+      const double dn = fma(-rkj, rkj, c[1]);  // lane k+1: W(k+1,k+1) - R(k,k+1)^2
+      d = __shfl_sync(0xffffffffu, dn, (k + 1) & 31);  // next pivot (unused after the last step)
+      double* rowk = s.rowb[warp][k & 1];
+      rowk[lane] = rkj;  // twice: rowk[k + 1 + i] is R(k, k+1+i), and 0 past column 31
+      rowk[lane + 32] = rkj;
+      if (warp == 0) {
+        s.Rd[k * 34 + lane] = rkj;
+        if (!ok && lane == 0 && blockIdx.x == 0 && a.status)
+          atomicMin(a.status, a.col0 + c0 + k + 1);
+      }
+      const double sk = r[0] * ri;  // S_b(lane, k)
+      Sf[lane * kLdS + k] = (float)sk;
       ok = d > 0.0 && d <= 1.7976931348623157e308;
       ri = rsqrt_nr(ok ? d : 1.0);
+      __syncwarp();
+      // R(k, k+1+i); slots past column 31 read R(k, 0..k-1) = 0 from the second copy
+      const double* rk = rowk + k + 1;
 #pragma unroll
-      for (int i = 1; i < 31; ++i) {
+      for (int i = 0; i < 31; ++i) {
         const double v = rk[i];
         c[i] = fma(-v, rkj, c[i + 1]);
         r[i] = fma(-sk, v, r[i + 1]);
@@ -313,13 +391,13 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
       r[31] = 0.0;
     }
 #pragma unroll 1
-    for (int j = pw; j < 32; ++j) s.Sf[lane * 32 + j] = 0.f;
-  } else if (st_pw > 0 && warp != 4) {
-    // the previous panel's deferred Q stores (those columns are final) beside the one-warp
-    // Cholesky chain, on the six warps that do not share its scheduler (warp 4 does)
-    const int idx = (warp < 4 ? warp - 1 : warp - 2) * 32 + lane;
-    if (idx < nrows) leaf_store_row(a, s, idx, st_c0, st_pw);
-    if (idx + 192 < nrows) leaf_store_row(a, s, idx + 192, st_c0, st_pw);
+    for (int j = pw; j < 32; ++j) Sf[lane * kLdS + j] = 0.f;
+  } else if (st_pw > 0) {
+    // the previous panel's deferred Q stores (those columns are final) on the four warps that run
+    // no chain
+    const int idx = (warp - kMW) * 32 + lane;
+#pragma unroll 1
+    for (int rr = idx; rr < nrows; rr += 128) leaf_store_row(a, s, rr, st_c0, st_pw);
   }
   __syncthreads();
   if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: Cholesky + S end
@@ -334,36 +412,37 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
       if (i <= j) a.R[(c0 + i) + (long long)(c0 + j) * a.ldr] = (float)s.Rd[i * 34 + j];
     }
   }
-  // (4) Q_b <- Q_b S_b (S_b upper triangular: the zero terms add exactly nothing).  Rolled over
-  // groups of four l: Q_b(t, l..l+3) is one conflict-free 16-byte shared load (the scalar load per
-  // l hit 8 banks per warp), then four unrolled rank-1 steps in the same l order as before.  Rows
-  // l >= pw of S_b are zero (lanes >= pw above), so the padded tail adds exact zeros.
+  // (4) Q_b <- Q_b S_b: thread t = row t (block t / 64).  S_b is upper triangular, so column j
+  // takes the terms l <= j only, summed in increasing l from zero (the same value as the full
+  // product: the skipped terms are exact zeros); FFMA2 on column pairs (the pair's extra term
+  // S(l, l-1) of an odd l is an exact zero too).  Rows l >= pw of S_b are zero.
   if (t < nrows) {
     float* row = s.L + t * kLd + c0;
-    float y[32];
+    const float* Sf = s.u.Sf[t / kBR];
+    float q[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) y[j] = 0.f;
-#pragma unroll 1
-    for (int l4 = 0; l4 < pw; l4 += 4) {
-      const float4 q4 = *reinterpret_cast<const float4*>(row + l4);
-      const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
+    for (int i = 0; i < 8; ++i) {
+      const float4 q4 = *reinterpret_cast<const float4*>(row + 4 * i);
+      q[4 * i] = q4.x;
+      q[4 * i + 1] = q4.y;
+      q[4 * i + 2] = q4.z;
+      q[4 * i + 3] = q4.w;
+    }
+    float2 y[16];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float ql = qv[u];
-        const float4* sr = reinterpret_cast<const float4*>(s.Sf + (l4 + u) * 32);
+    for (int j2 = 0; j2 < 16; ++j2) y[j2] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 v = sr[j4];
-          y[4 * j4] = fmaf(ql, v.x, y[4 * j4]);
-          y[4 * j4 + 1] = fmaf(ql, v.y, y[4 * j4 + 1]);
-          y[4 * j4 + 2] = fmaf(ql, v.z, y[4 * j4 + 2]);
-          y[4 * j4 + 3] = fmaf(ql, v.w, y[4 * j4 + 3]);
-        }
-      }
+    for (int l = 0; l < 32; ++l) {
+      const float2 ql = make_float2(q[l], q[l]);
+#pragma unroll
+      for (int j2 = l / 2; j2 < 16; ++j2)
+        y[j2] = ffma2(ql, *reinterpret_cast<const float2*>(Sf + l * kLdS + 2 * j2), y[j2]);
     }
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < pw) row[j] = y[j];
+    for (int j2 = 0; j2 < 16; ++j2) {
+      if (2 * j2 < pw) row[2 * j2] = y[j2].x;
+      if (2 * j2 + 1 < pw) row[2 * j2 + 1] = y[j2].y;
+    }
   }
   __syncthreads();
   if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: apply end (before the Q stores)
@@ -372,8 +451,8 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     a.dbg[104] = v;
   }
   // these pw columns of Q are final (later ops only read them): stream them out (FP32 and the
-  // FP16 shadow), coalesced down each column -- now, or (defer) by the idle upper half of the CTA
-  // beside the next panel's MGS
+  // FP16 shadow), coalesced down each column -- now, or (defer) by the warps that idle beside the
+  // next panel's Cholesky
   if (!defer && t < nrows) leaf_store_row(a, s, t, c0, pw);
   leaf_ts(a, slot);
 }
@@ -402,11 +481,18 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
     for (int r = grp; r < nrows; r += G) {
       const float4 qv = *reinterpret_cast<const float4*>(q1 + r * kLd);
       const float4 av = *reinterpret_cast<const float4*>(a2 + r * kLd);
-      const float qq[4] = {qv.x, qv.y, qv.z, qv.w}, aa[4] = {av.x, av.y, av.z, av.w};
+      const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
+      const float2 a01 = make_float2(av.x, av.y), a23 = make_float2(av.z, av.w);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(qq[i], aa[j], acc[i][j]);
+      for (int i = 0; i < 4; ++i) {  // FFMA2: the same fmaf sequence per entry, two per instruction
+        const float2 qi = make_float2(qq[i], qq[i]);
+        float2 c01 = ffma2(qi, a01, make_float2(acc[i][0], acc[i][1]));
+        float2 c23 = ffma2(qi, a23, make_float2(acc[i][2], acc[i][3]));
+        acc[i][0] = c01.x;
+        acc[i][1] = c01.y;
+        acc[i][2] = c23.x;
+        acc[i][3] = c23.y;
+      }
     }
   }
   float* pp = a.ppart + (long long)blockIdx.x * 4096;
@@ -419,13 +505,13 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
     // row groups: combine in group order through shared memory
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      *reinterpret_cast<float4*>(s.T + grp * (H * W2P) + (4 * ti + i) * W2P + 4 * tj) =
+      *reinterpret_cast<float4*>(s.u.T + grp * (H * W2P) + (4 * ti + i) * W2P + 4 * tj) =
           make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
     __syncthreads();
     for (int e = t; e < H * W2P; e += kNT) {
-      float v = s.T[e];
+      float v = s.u.T[e];
 #pragma unroll
-      for (int g = 1; g < G; ++g) v += s.T[g * (H * W2P) + e];
+      for (int g = 1; g < G; ++g) v += s.u.T[g * (H * W2P) + e];
       pp[e] = v;
     }
   }
@@ -437,7 +523,7 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
   leaf_ts(a, slot);
   leaf_barrier(a, s);
   leaf_ts(a, slot);
-  for (int e = t; e < H * W2P; e += kNT) s.T[e] = __ldcg(a.r12 + e);
+  for (int e = t; e < H * W2P; e += kNT) s.u.T[e] = __ldcg(a.r12 + e);
   __syncthreads();
   // A2 -= Q1 R12: thread = rows (t % 128, t % 128 + 128), columns [jh * W2P/2, (jh+1) * W2P/2)
   constexpr int JC = W2P / 2;
@@ -456,16 +542,21 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
     const float qx[2][4] = {{va.x, va.y, va.z, va.w}, {vb.x, vb.y, vb.z, vb.w}};
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii) {
-      const float4* tr = reinterpret_cast<const float4*>(s.T + (i4 + ii) * W2P + jh * JC);
+      const float4* tr = reinterpret_cast<const float4*>(s.u.T + (i4 + ii) * W2P + jh * JC);
 #pragma unroll
       for (int j4 = 0; j4 < JC / 4; ++j4) {
         const float4 v = tr[j4];
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
-          u[rr][4 * j4] = fmaf(qx[rr][ii], v.x, u[rr][4 * j4]);
-          u[rr][4 * j4 + 1] = fmaf(qx[rr][ii], v.y, u[rr][4 * j4 + 1]);
-          u[rr][4 * j4 + 2] = fmaf(qx[rr][ii], v.z, u[rr][4 * j4 + 2]);
-          u[rr][4 * j4 + 3] = fmaf(qx[rr][ii], v.w, u[rr][4 * j4 + 3]);
+          const float2 qi = make_float2(qx[rr][ii], qx[rr][ii]);
+          const float2 c01 = ffma2(qi, make_float2(v.x, v.y),
+                                   make_float2(u[rr][4 * j4], u[rr][4 * j4 + 1]));
+          const float2 c23 = ffma2(qi, make_float2(v.z, v.w),
+                                   make_float2(u[rr][4 * j4 + 2], u[rr][4 * j4 + 3]));
+          u[rr][4 * j4] = c01.x;
+          u[rr][4 * j4 + 1] = c01.y;
+          u[rr][4 * j4 + 2] = c23.x;
+          u[rr][4 * j4 + 3] = c23.y;
         }
       }
     }
@@ -532,7 +623,7 @@ __global__ void __launch_bounds__(kNT, 1) leaf_kernel(const __grid_constant__ Le
 #pragma unroll 8
     for (int j = 0; j < 32; ++j) dst[j] = (ok && j < a.wl) ? src[(long long)j * a.ldx] : 0.f;
   }
-  if (a.mgs_rpt != 2 || a.ops[0].kind != 0) {  // otherwise issued beside the first MGS
+  if (a.ops[0].kind != 0) {  // otherwise issued beside the first MGS
     leaf_issue_rest(a, s, nrows, t);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
@@ -545,7 +636,7 @@ __global__ void __launch_bounds__(kNT, 1) leaf_kernel(const __grid_constant__ Le
   for (int o = 0; o < a.nops; ++o) {
     const LeafOp op = a.ops[o];
     if (op.kind == 0) {
-      const bool defer = a.mgs_rpt == 2 && o != last_panel;
+      const bool defer = o != last_panel;
       leaf_panel(a, s, nrows, op.c0, op.h, slot, o == 0, st_c0, st_pw, defer);
       st_c0 = op.c0;
       st_pw = defer ? op.h : 0;
@@ -576,7 +667,80 @@ void leaf_plan(int c0, int w, LeafArgs& a) {
   leaf_plan(c0 + h, w2, a);
 }
 
+// X (m x w, ldx) <- X S, S (w x w, lds) a dense FP32 block, w <= 128, in place; the FP16 shadow
+// of the result into Xh when non-null.  CTA = 64 rows: the rows and S are staged in shared memory
+// (the CTA reads all its rows before writing any), thread (warp g, lane) accumulates rows
+// 8g..8g+7 x columns lane + 32u in the fixed l order (deterministic).
+constexpr int kApRows = 64;
+__global__ void __launch_bounds__(256) apply_right_kernel(int m, int w, float* X, long long ldx,
+                                                          const float* S, long long lds,
+                                                          __half* Xh, long long ldh) {
+  extern __shared__ __align__(16) float ap_smem[];
+  float* Ss = ap_smem;                    // [w][128] row l, column j
+  float* Xs = ap_smem + 128 * 128;        // [kApRows][w + 1]
+  const int t = threadIdx.x, lane = t & 31, g = t >> 5;
+  const long long row0 = (long long)blockIdx.x * kApRows;
+  const int rows = (int)(m - row0 < kApRows ? m - row0 : kApRows);
+  const int ldxs = w + 1;
+  for (int e = t; e < w * w; e += 256) {
+    const int l = e % w, j = e / w;  // coalesced down the columns of S
+    Ss[l * 128 + j] = S[l + (long long)j * lds];
+  }
+  for (int e = t; e < kApRows * w; e += 256) {
+    const int r = e % kApRows, l = e / kApRows;
+    Xs[r * ldxs + l] = r < rows ? X[row0 + r + (long long)l * ldx] : 0.f;
+  }
+  __syncthreads();
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[i][u] = 0.f;
+  for (int l = 0; l < w; ++l) {
+    float sv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sv[u] = Ss[l * 128 + lane + 32 * u];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float xv = Xs[(8 * g + i) * ldxs + l];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[i][u] = fmaf(xv, sv[u], acc[i][u]);
+    }
+  }
+  __syncthreads();
+  // transpose through shared memory for column-coalesced stores
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (lane + 32 * u < w) Xs[(8 * g + i) * ldxs + lane + 32 * u] = acc[i][u];
+  __syncthreads();
+  for (int e = t; e < kApRows * w; e += 256) {
+    const int r = e % kApRows, j = e / kApRows;
+    if (r < rows) {
+      const float v = Xs[r * ldxs + j];
+      X[row0 + r + (long long)j * ldx] = v;
+      if (Xh) Xh[row0 + r + (long long)j * ldh] = __float2half_rn(v);
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t apply_right(int m, int w, float* X, long long ldx, const float* S, long long lds,
+                        __half* Xh, long long ldh, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  if (w < 1 || w > 128) return cudaErrorInvalidValue;
+  const int smem = (int)sizeof(float) * (128 * 128 + kApRows * (128 + 1));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(apply_right_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  apply_right_kernel<<<(m + kApRows - 1) / kApRows, 256, smem, st>>>(m, w, X, ldx, S, lds, Xh,
+                                                                      ldh);
+  return cudaGetLastError();
+}
 
 unsigned long long* g_leaf_dbg = nullptr;
 
@@ -621,14 +785,6 @@ cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long 
   a.status = status;
   a.col0 = col0;
   a.dbg = g_leaf_dbg;
-  {
-    static int rpt = -1;
-    if (rpt < 0) {
-      const char* e = getenv("TCQR_LEAF_MGS_RPT");
-      rpt = (e && atoi(e) == 1) ? 1 : 2;  // 128 threads x 2 rows measured faster (14.3 vs 17.2 us)
-    }
-    a.mgs_rpt = rpt;
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nb);
   cfg.blockDim = dim3(kNT);
@@ -640,7 +796,7 @@ cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, leaf_kernel, a);
-  if (e == cudaSuccess) *bar_seq += 2u * (unsigned)a.nops;  // two grid barriers per op
+  if (e == cudaSuccess) *bar_seq += 2u * (unsigned)a.nops * (unsigned)nb;  // 2 barriers per op
   return e;
 }
 

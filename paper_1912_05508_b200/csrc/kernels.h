@@ -88,13 +88,18 @@ extern unsigned long long* g_proj_dbg;  // debug: phase timestamps of the FP32 p
 // The leaf columns [0, wl) of X (m rows, ldx; wl <= 128) factored in one cooperative launch:
 // Q in place (and its FP16 shadow into Xh when non-null), R(i, j) of the leaf at R[i + j ldr].
 // scratch: leaf_scratch_bytes() of device memory; bar: an arrival counter zeroed together with
-// *bar_seq = 0 (the host's count of completed grid barriers, advanced by each launch).
+// *bar_seq = 0 (the host's count of counter arrivals, advanced by each launch).
 // cudaErrorNotSupported when the blocks do not fit the co-resident grid.
 size_t leaf_scratch_bytes();
 extern unsigned long long* g_leaf_dbg;  // debug: CTA-0 phase timestamps of the leaf kernel
 cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long long ldh, float* R,
                        long long ldr, int col0, int* status, void* scratch, size_t scratch_bytes,
                        unsigned* bar, unsigned* bar_seq, int num_sms, cudaStream_t st);
+
+// X (m x w, ldx; w <= 128) <- X S (S w x w, lds; FP32), FP16 shadow of the result into Xh if
+// non-null: Eq. (6) step 4 for the per-leaf TSQR across ranks.
+cudaError_t apply_right(int m, int w, float* X, long long ldx, const float* S, long long lds,
+                        __half* Xh, long long ldh, cudaStream_t st);
 
 // ---- K2b FP32 intra-leaf products (k_f32.cu) ----
 // T (h x w2, ld h) = Q1' A2 over m rows (deterministic split-K with partials in P).
@@ -116,7 +121,8 @@ cudaError_t trinv_f64(int n, const float* R, long long ldr, double* M, long long
                       int num_sms, cudaStream_t st);
 cudaError_t gemv_f32_n(int m, int n, const float* A, long long lda, const double* v, double* y,
                        double* part, long long part_cap, cudaStream_t st);
+// part: cg_gemv_t_part_count(m, n) doubles of scratch
 cudaError_t gemv_f32_t(int m, int n, const float* A, long long lda, const double* v, double* y,
-                       cudaStream_t st);
+                       double* part, cudaStream_t st);
 
 }  // namespace tcqr

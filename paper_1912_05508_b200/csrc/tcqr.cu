@@ -6,6 +6,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
 #include <map>
 #include <cmath>
 #include <mutex>
@@ -78,6 +80,10 @@ struct Context {
   int num_sms = 148;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
+  struct VGroup* vg = nullptr;  // virtual ranks (test seam): the in-process group, else null
+  unsigned long long vseq = 0;  // collectives this virtual rank has issued
+  int ncoll = 0;                // collectives enqueued by the most recent factor / solve call
+  std::mutex mu;                // serializes the API calls made on this context
   tcqr_config_t cfg;
   // workspace
   void* user_ws = nullptr;
@@ -90,8 +96,13 @@ struct Context {
   int* h_status = nullptr;  // pinned
   std::map<std::string, GraphEntry> graphs;
 };
-static Context g_ctx;
-static std::mutex g_mu;
+// The process-wide context, or (virtual ranks, tcqr_init_virtual) a context bound to the calling
+// thread: every entry point works on the context of the thread that calls it.
+static Context g_ctx_main;
+static thread_local Context* t_ctx = nullptr;
+static inline Context& cur_ctx() { return t_ctx ? *t_ctx : g_ctx_main; }
+#define g_ctx (cur_ctx())
+#define g_mu (cur_ctx().mu)
 
 // Order the call after the caller's pending work, and the caller's stream after the call.
 static void begin_call() {
@@ -141,9 +152,12 @@ struct FactorWs {
   unsigned int* cmax = nullptr;  // column max scratch of the split-row cast (n)
   float* pipeR = nullptr;        // pipelined panel: child R's (NaN between uses)
   float* pipeS = nullptr;        // pipelined panel: root Q slices (NaN between uses)
+  float* rleaf = nullptr;        // per-leaf TSQR (P > 1): this rank's local leaf R (128 x 128)
+  float* gleaf = nullptr;        //   the P gathered local R's (P x 128 x 128)
+  float* tstack = nullptr;       //   their stack (P*128 x 128, ld P*w), factored in place
   float* R2 = nullptr;           // re-orthogonalization: R of the second pass (n x n)
   float* Rt = nullptr;           // re-orthogonalization: R2 * R1 staging (n x n)
-  unsigned leaf_bars = 0;        // grid barriers the leaf kernels completed since iws was zeroed
+  unsigned leaf_bars = 0;        // leaf grid-barrier counter arrivals since iws was zeroed
   // NEXT-4 FP16 split (cfg.fp16_split): low halves of the shadow and of R12, two more R12 stagings
   __half* Ql = nullptr;     // ld ldh, like Qh
   __half* R12l = nullptr;   // like R12h
@@ -175,6 +189,11 @@ static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, Facto
   w.cmax = a.take<unsigned int>((size_t)n + 64);
   w.pipeR = a.take<float>(32 * 32 * 32);
   w.pipeS = a.take<float>(32 * 32 * 32);
+  if (nranks > 1) {
+    w.rleaf = a.take<float>(128 * 128);
+    w.gleaf = a.take<float>((size_t)nranks * 128 * 128);
+    w.tstack = a.take<float>((size_t)nranks * 128 * 128);
+  }
   if (reorth) {
     w.R2 = a.take<float>((size_t)n * n);
     w.Rt = a.take<float>((size_t)n * n);
@@ -190,7 +209,10 @@ static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, Facto
 struct LlsWs {
   float* Aw = nullptr;  // working copy of A (m x n, ld m)
   float* R = nullptr;   // n x n
-  double* M = nullptr;  // inv(R), n x n
+  double* M = nullptr;  // inv(R), n x n (FP64: the direct solve)
+  float* M32 = nullptr; // fl32(inv(R)), n x n upper triangle: the CGLS preconditioner (R-A13)
+  double* r2 = nullptr; // second residual buffer (the fused r update writes the other one)
+  double* tpart = nullptr;  // A' v split partials (cg_gemv_t_part_count)
   double* W = nullptr;  // trinv workspace
   double *x, *xbest, *t, *s, *p, *v, *r, *q, *b2, *x1;
   double* part = nullptr;
@@ -215,6 +237,9 @@ static void plan_lls_ws(Arena& a, long long m, long long n, int nranks, int maxi
   w.Aw = a.take<float>((size_t)m * n);
   w.R = a.take<float>((size_t)n * n);
   w.M = a.take<double>((size_t)n * n);
+  w.M32 = a.take<float>((size_t)n * n);
+  w.r2 = a.take<double>(m);
+  w.tpart = a.take<double>((size_t)cg_gemv_t_part_count((int)m, (int)n) + 64);
   w.W = a.take<double>((size_t)trinv_w_count(n));
   w.x = a.take<double>(n);
   w.xbest = a.take<double>(n);
@@ -287,11 +312,127 @@ static char* get_ws(size_t bytes) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Collectives (no-ops at nranks == 1)
+// Collectives (no-ops at nranks == 1).  Two transports behind the same calls, in the same order:
+//  * NCCL (one process per GPU, tcqr_init with an ncclUniqueId);
+//  * virtual ranks (tcqr_init_virtual, the SURVEY.md §4 test seam): P contexts of ONE process on
+//    ONE device, one host thread each.  A collective stages every rank's contribution in the
+//    group's device slots, meets the other ranks at a host barrier (their copies are ordered by
+//    CUDA events recorded before it), then each rank combines the P slots in rank order on its
+//    own stream (vcomm_kernel).  Every rank combines identical inputs in the same order, so the
+//    results are bitwise identical on all ranks, like NCCL's.
 // ------------------------------------------------------------------------------------------
+constexpr int kMaxVRanks = 8;
+
+struct VGroup {
+  int n = 0;
+  size_t slot_bytes = 0;
+  void* slot[2][kMaxVRanks] = {};           // staging, by collective parity and rank
+  cudaEvent_t ev_written[4][kMaxVRanks] = {};  // rank's contribution staged (collective k % 4)
+  cudaEvent_t ev_read[4][kMaxVRanks] = {};     // rank finished reading the slots (k % 4)
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  bool aborted = false;
+};
+
+// Host barrier of the virtual group; false (and the whole group aborted) on a peer's abort or
+// after 120 s, so a failing rank never leaves the others waiting forever.
+static bool vbarrier(VGroup& g) {
+  std::unique_lock<std::mutex> lk(g.mu);
+  if (g.aborted) return false;
+  const unsigned long long my = g.gen;
+  if (++g.arrived == g.n) {
+    g.arrived = 0;
+    ++g.gen;
+    g.cv.notify_all();
+    return true;
+  }
+  const bool ok = g.cv.wait_for(lk, std::chrono::seconds(120),
+                                [&] { return g.gen != my || g.aborted; });
+  if (!ok || g.aborted) {
+    g.aborted = true;
+    g.cv.notify_all();
+    return false;
+  }
+  return true;
+}
+static void vabort(VGroup* g) {
+  if (!g) return;
+  std::lock_guard<std::mutex> lk(g->mu);
+  g->aborted = true;
+  g->cv.notify_all();
+}
+
+enum VOp { kVSumF32 = 0, kVSumF64 = 1, kVMinI32 = 2, kVGatherF32 = 3 };
+struct VSlots {
+  const void* p[kMaxVRanks];
+};
+// out = combination of the n slots (rank order), element by element; gather: out[r*count + i].
+__global__ void vcomm_kernel(int op, int n, VSlots in, void* out, long long count) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += stride) {
+    if (op == kVSumF32) {
+      float acc = static_cast<const float*>(in.p[0])[i];
+      for (int r = 1; r < n; ++r) acc += static_cast<const float*>(in.p[r])[i];
+      static_cast<float*>(out)[i] = acc;
+    } else if (op == kVSumF64) {
+      double acc = static_cast<const double*>(in.p[0])[i];
+      for (int r = 1; r < n; ++r) acc += static_cast<const double*>(in.p[r])[i];
+      static_cast<double*>(out)[i] = acc;
+    } else if (op == kVMinI32) {
+      int acc = static_cast<const int*>(in.p[0])[i];
+      for (int r = 1; r < n; ++r) acc = min(acc, static_cast<const int*>(in.p[r])[i]);
+      static_cast<int*>(out)[i] = acc;
+    } else {
+      for (int r = 0; r < n; ++r)
+        static_cast<float*>(out)[r * count + i] = static_cast<const float*>(in.p[r])[i];
+    }
+  }
+}
+
+static int vcollective(int op, const void* send, void* recv, size_t count, size_t elem) {
+  Context& c = g_ctx;
+  VGroup& g = *c.vg;
+  const size_t bytes = count * elem;
+  if (bytes > g.slot_bytes) {
+    fprintf(stderr, "tcqr: virtual collective of %zu B exceeds the group's %zu B slots\n", bytes,
+            g.slot_bytes);
+    vabort(&g);
+    return TCQR_ERR_NCCL;
+  }
+  const unsigned long long k = c.vseq++;
+  const int par = (int)(k & 1), e = (int)(k & 3), r = c.rank;
+  // the slot of this parity is free once every rank has read collective k - 2
+  if (k >= 2)
+    for (int q = 0; q < g.n; ++q) cudaStreamWaitEvent(c.stream, g.ev_read[(k - 2) & 3][q], 0);
+  if (cudaMemcpyAsync(g.slot[par][r], send, bytes, cudaMemcpyDeviceToDevice, c.stream) !=
+          cudaSuccess ||
+      cudaEventRecord(g.ev_written[e][r], c.stream) != cudaSuccess) {
+    vabort(&g);
+    return TCQR_ERR_CUDA;
+  }
+  if (!vbarrier(g)) return TCQR_ERR_NCCL;
+  VSlots in{};
+  for (int q = 0; q < g.n; ++q) {
+    cudaStreamWaitEvent(c.stream, g.ev_written[e][q], 0);
+    in.p[q] = g.slot[par][q];
+  }
+  const int grid = (int)std::min<size_t>((count + 255) / 256, 1184);
+  vcomm_kernel<<<std::max(grid, 1), 256, 0, c.stream>>>(op, g.n, in, recv, (long long)count);
+  if (cudaGetLastError() != cudaSuccess ||
+      cudaEventRecord(g.ev_read[e][r], c.stream) != cudaSuccess) {
+    vabort(&g);
+    return TCQR_ERR_CUDA;
+  }
+  return 0;
+}
+
 static int allreduce_f32(float* buf, size_t count) {
   Context& c = g_ctx;
   if (c.nranks <= 1) return 0;
+  ++c.ncoll;
+  if (c.vg) return vcollective(kVSumF32, buf, buf, count, sizeof(float));
   return g_nccl.AllReduce(buf, buf, count, ncclFloat32, ncclSum, c.comm, c.stream) == ncclSuccess
              ? 0
              : TCQR_ERR_NCCL;
@@ -299,14 +440,28 @@ static int allreduce_f32(float* buf, size_t count) {
 static int allreduce_f64(double* buf, size_t count) {
   Context& c = g_ctx;
   if (c.nranks <= 1) return 0;
+  ++c.ncoll;
+  if (c.vg) return vcollective(kVSumF64, buf, buf, count, sizeof(double));
   return g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, c.comm, c.stream) == ncclSuccess
              ? 0
              : TCQR_ERR_NCCL;
 }
-static int allreduce_max_i32(int* buf) {
+// Status codes are encoded so that the most significant one is the smallest (OK = 0x7f7f7f7f).
+static int allreduce_min_i32(int* buf) {
   Context& c = g_ctx;
   if (c.nranks <= 1) return 0;
+  ++c.ncoll;
+  if (c.vg) return vcollective(kVMinI32, buf, buf, 1, sizeof(int));
   return g_nccl.AllReduce(buf, buf, 1, ncclInt32, ncclMin, c.comm, c.stream) == ncclSuccess
+             ? 0
+             : TCQR_ERR_NCCL;
+}
+// recv (nranks * count floats) = the ranks' send buffers in rank order.
+static int allgather_f32(const float* send, float* recv, size_t count) {
+  Context& c = g_ctx;
+  ++c.ncoll;
+  if (c.vg) return vcollective(kVGatherF32, send, recv, count, sizeof(float));
+  return g_nccl.AllGather(send, recv, count, ncclFloat32, c.comm, c.stream) == ncclSuccess
              ? 0
              : TCQR_ERR_NCCL;
 }
@@ -340,11 +495,11 @@ struct PendingEv {
   cudaEvent_t a, b;
   double flops, bytes;
 };
-static bool g_prof = false;
-static ProfAcc g_acc[TCQR_NUM_CLASSES];
-static std::vector<PendingEv> g_pend;
-static std::vector<cudaEvent_t> g_evpool;
-static int g_last_launches = 0;
+static thread_local bool g_prof = false;
+static thread_local ProfAcc g_acc[TCQR_NUM_CLASSES];
+static thread_local std::vector<PendingEv> g_pend;
+static thread_local std::vector<cudaEvent_t> g_evpool;
+static thread_local int g_last_launches = 0;
 
 static cudaEvent_t prof_ev() {
   if (!g_evpool.empty()) {
@@ -455,9 +610,7 @@ static int panel(FactorWs& ws, int m, int w, float* X, long long ldx, float* Rou
   // TSQR (reading R-A26): local tree -> allgather of the P local R's -> redundant factorization of
   // the stack on every rank -> this rank's slice applied to the local Q.
   CKR(caqr_rec(ws, off, m, w, X, ldx, ws.rloc, w, false, col0));
-  if (g_nccl.AllGather(ws.rloc, ws.gather, (size_t)w * w, ncclFloat32, c.comm, c.stream) !=
-      ncclSuccess)
-    return TCQR_ERR_NCCL;
+  CKR(allgather_f32(ws.rloc, ws.gather, (size_t)w * w));
   // gather holds P column-major w x w blocks; restack them as a (P*w) x w matrix.
   const int P = c.nranks;
   float* S = ws.stack + off;
@@ -540,6 +693,47 @@ static int emit_q_lo(FactorJob& J, int c0, int w) {
   return 0;
 }
 
+// Per-leaf TSQR across ranks (reading R-A26 at the leaf width; SURVEY.md §8(e) "better: per-leaf
+// TSQR"): the local leaf by K2L with local zero norms allowed (R-A8: status not checked), ONE
+// allgather of the P local w x w R's, every rank factors the (P w) x w stack with the same K2L
+// launch (identical inputs and code: R bit-identical on all ranks; global breakdowns flagged
+// there), then Q_r <- Q_r Q_stack[r w : (r+1) w, :] (Eq. (6) step 4) with the FP16 shadow.
+// Returns 1 when the local leaf does not fit the co-resident grid (caller falls back).
+static int leaf_tsqr(FactorJob& J, int c0, int w, bool need_h) {
+  Context& c = g_ctx;
+  FactorWs& ws = *J.ws;
+  const int m = J.m, P = c.nranks;
+  float* Qc = J.Q + (long long)c0 * J.ldq;
+  unsigned* bar = reinterpret_cast<unsigned*>(ws.iws + ws.iws_cap - 16);
+  const size_t scratch = sizeof(float) * (size_t)ws.p_cap;
+  CK(cudaMemsetAsync(ws.rleaf, 0, sizeof(float) * (size_t)w * w, c.stream));
+  cudaError_t e = cudaErrorNotSupported;
+  PROF(TCQR_K2_LEAF, 2.0 * m * w * w, 8.0 * m * w,
+       e = leaf_fused(m, w, Qc, J.ldq, nullptr, 0, ws.rleaf, w, c0, nullptr, ws.P, scratch, bar,
+                      &ws.leaf_bars, c.num_sms, c.stream));
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return 1;
+  }
+  CK(e);
+  CKR(allgather_f32(ws.rleaf, ws.gleaf, (size_t)w * w));
+  const long long lds = (long long)P * w;
+  for (int r = 0; r < P; ++r)
+    CK(cudaMemcpy2DAsync(ws.tstack + (long long)r * w, sizeof(float) * lds,
+                         ws.gleaf + (long long)r * w * w, sizeof(float) * w, sizeof(float) * w, w,
+                         cudaMemcpyDeviceToDevice, c.stream));
+  PROF(TCQR_K2_LEAF, 2.0 * lds * w * w, 8.0 * lds * w,
+       e = leaf_fused((int)lds, w, ws.tstack, lds, nullptr, 0, J.R + c0 + (long long)c0 * J.ldr,
+                      J.ldr, c0, c.d_status, ws.P, scratch, bar, &ws.leaf_bars, c.num_sms,
+                      c.stream));
+  CK(e);
+  PROF(TCQR_K2_APPLY, 2.0 * m * w * w, 8.0 * m * w + (need_h ? 2.0 * m * w : 0.0),
+       CK(apply_right(m, w, Qc, J.ldq, ws.tstack + (long long)c.rank * w, lds,
+                      need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, ws.ldh, c.stream)));
+  if (need_h) CKR(emit_q_lo(J, c0, w));
+  return chunk_done(J, c0, w);
+}
+
 static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   Context& c = g_ctx;
   FactorWs& ws = *J.ws;
@@ -554,6 +748,11 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     return rc;
   }
   float* Qc = J.Q + (long long)c0 * J.ldq;
+  if (c.cfg.leaf_kernel && c.nranks > 1 && w <= 128 && w <= c.cfg.cutoff && !J.sp) {
+    need_cols(J, c0, c0 + w);
+    const int rc = leaf_tsqr(J, c0, w, need_h);
+    if (rc != 1) return rc;
+  }
   if (c.cfg.leaf_kernel && c.nranks == 1 && w <= 128 && w <= c.cfg.cutoff) {
     // the whole leaf (every node below the cutoff) in one cooperative launch (k_leaf.cu)
     need_cols(J, c0, c0 + w);
@@ -773,7 +972,7 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
     CK(cudaMemcpyAsync(R, ws.Rt, sizeof(float) * (size_t)n * n, cudaMemcpyDeviceToDevice,
                        c.stream));
   }
-  CKR(allreduce_max_i32(c.d_status));
+  CKR(allreduce_min_i32(c.d_status));
   return 0;
 }
 
@@ -803,7 +1002,8 @@ static std::string graph_key(const char* tag, std::initializer_list<long long> v
 static int run_factor(int m, int n, const float* A, long long lda, float* Q, float* R,
                       FactorWs& ws, const void* ws_base) {
   Context& c = g_ctx;
-  if (!c.cfg.use_graphs || g_prof) return enqueue_factor(m, n, A, lda, Q, R, ws);
+  // virtual ranks: no capture (their collectives order P streams with events and host barriers)
+  if (!c.cfg.use_graphs || g_prof || c.vg) return enqueue_factor(m, n, A, lda, Q, R, ws);
   const std::string key =
       graph_key("f", {m, n, lda, (long long)A, (long long)Q, (long long)R, (long long)ws_base});
   auto it = c.graphs.find(key);
@@ -900,7 +1100,18 @@ int tcqr_nccl_unique_id(void* out) {
   return 0;
 }
 
+static int finalize_ctx();
+
 int tcqr_finalize(void) {
+  const int rc = finalize_ctx();
+  if (t_ctx) {  // a virtual rank's context dies with its finalize
+    delete t_ctx;
+    t_ctx = nullptr;
+  }
+  return rc;
+}
+
+static int finalize_ctx() {
   std::lock_guard<std::mutex> lk(g_mu);
   Context& c = g_ctx;
   if (!c.inited) return 0;
@@ -942,16 +1153,19 @@ int tcqr_finalize(void) {
   c.stream = nullptr;
   c.user_ws = nullptr;
   c.user_ws_bytes = 0;
+  c.vg = nullptr;
+  c.vseq = 0;
   c.inited = false;
   return 0;
 }
 
-int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int rank, int nranks) {
-  if (g_ctx.inited) tcqr_finalize();
+static int init_ctx(int device, void* cuda_stream, const void* nccl_unique_id, int rank,
+                    int nranks, VGroup* vg) {
+  if (g_ctx.inited) finalize_ctx();
   std::lock_guard<std::mutex> lk(g_mu);
   Context& c = g_ctx;
   if (nranks < 1 || rank < 0 || rank >= nranks) return -4;
-  if (nranks > 1 && !nccl_unique_id) return -3;
+  if (nranks > 1 && !nccl_unique_id && !vg) return -3;
   if (cudaSetDevice(device) != cudaSuccess) return -1;
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return TCQR_ERR_CUDA;
@@ -996,12 +1210,17 @@ int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int ran
     c.la_sms = n ? std::max(1, atoi(n)) : 10;
   }
   c.num_sms = prop.multiProcessorCount;
+  // virtual ranks share one device: each gets an even 1/P share of the SMs as its grid budget,
+  // so the P ranks' co-resident (cooperative) grids fit the device together
+  if (vg) c.num_sms = std::max(2, (prop.multiProcessorCount / nranks) & ~1);
   c.rank = rank;
   c.nranks = nranks;
+  c.vg = vg;
+  c.vseq = 0;
   tcqr_default_config(&c.cfg);
   if (cudaMalloc(&c.d_status, 64) != cudaSuccess) return TCQR_ERR_OOM;
   if (cudaMallocHost(&c.h_status, 64) != cudaSuccess) return TCQR_ERR_OOM;
-  if (nranks > 1) {
+  if (nranks > 1 && !vg) {
     if (!g_nccl.load()) return TCQR_ERR_NCCL;
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
@@ -1010,6 +1229,63 @@ int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int ran
   c.inited = true;
   return 0;
 }
+
+int tcqr_init(int device, void* cuda_stream, const void* nccl_unique_id, int rank, int nranks) {
+  return init_ctx(device, cuda_stream, nccl_unique_id, rank, nranks, nullptr);
+}
+
+void* tcqr_vgroup_create(int nranks, size_t slot_bytes) {
+  if (nranks < 1 || nranks > kMaxVRanks || slot_bytes == 0) return nullptr;
+  VGroup* g = new VGroup();
+  g->n = nranks;
+  g->slot_bytes = (slot_bytes + 255) / 256 * 256;
+  bool ok = true;
+  for (int p = 0; p < 2; ++p)
+    for (int r = 0; r < nranks; ++r) ok = ok && cudaMalloc(&g->slot[p][r], g->slot_bytes) == cudaSuccess;
+  for (int e = 0; e < 4; ++e)
+    for (int r = 0; r < nranks; ++r)
+      ok = ok &&
+           cudaEventCreateWithFlags(&g->ev_written[e][r], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&g->ev_read[e][r], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    tcqr_vgroup_destroy(g);
+    return nullptr;
+  }
+  return g;
+}
+
+int tcqr_vgroup_destroy(void* group) {
+  VGroup* g = static_cast<VGroup*>(group);
+  if (!g) return -1;
+  cudaDeviceSynchronize();
+  for (int p = 0; p < 2; ++p)
+    for (int r = 0; r < kMaxVRanks; ++r)
+      if (g->slot[p][r]) cudaFree(g->slot[p][r]);
+  for (int e = 0; e < 4; ++e)
+    for (int r = 0; r < kMaxVRanks; ++r) {
+      if (g->ev_written[e][r]) cudaEventDestroy(g->ev_written[e][r]);
+      if (g->ev_read[e][r]) cudaEventDestroy(g->ev_read[e][r]);
+    }
+  delete g;
+  return 0;
+}
+
+int tcqr_init_virtual(int device, void* cuda_stream, void* group, int rank) {
+  VGroup* g = static_cast<VGroup*>(group);
+  if (!g) return -3;
+  if (rank < 0 || rank >= g->n) return -4;
+  if (t_ctx) tcqr_finalize();
+  t_ctx = new Context();
+  const int rc = init_ctx(device, cuda_stream, nullptr, rank, g->n, g);
+  if (rc != 0) {
+    delete t_ctx;
+    t_ctx = nullptr;
+    vabort(g);
+  }
+  return rc;
+}
+
+int tcqr_last_collective_count(void) { return g_ctx.ncoll; }
 
 int tcqr_workspace_size(int64_t m, int64_t n, int op, size_t* bytes) {
   if (!bytes || m < 1 || n < 1 || (op != 0 && op != 1)) return -1;
@@ -1042,8 +1318,41 @@ int tcqr_factor(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, flo
   Arena a{base, 0};
   FactorWs ws;
   plan_factor_ws(a, m, n, c.nranks, ws, c.cfg.reorth != 0);
-  CKR(run_factor((int)m, (int)n, A, lda, Q, R, ws, base));
-  return read_status();
+  c.ncoll = 0;
+  rc = run_factor((int)m, (int)n, A, lda, Q, R, ws, base);
+  if (rc == 0) rc = read_status();
+  if (rc < 0) vabort(c.vg);
+  return rc;
+}
+
+// `iters` CGLS iterations (Alg. 5 lines 11-23, corrected per R-A10), enqueued without a host
+// synchronization: t = M p; q = A t, delta = ||q||^2 [allreduce]; x += alpha t; v = A'(r - alpha q)
+// with the new residual written to the other buffer [allreduce]; s = M' v; stop tests, beta, p.
+// M is the FP32 copy of R^-1 (reading R-A13).  iters must be even (residual double buffer).
+static int cg_chunk(LlsWs& w, int m, int n, const float* A, long long lda, int iters) {
+  Context& c = g_ctx;
+  const int* done = &w.st->done;
+  const int ndp = (m + 255) / 256;
+  const double tri = 4.0 * (double)n * (n + 1) / 2.0;  // FP32 upper triangle, one pass
+  for (int i = 0; i < iters; ++i) {
+    double* rin = (i & 1) ? w.r2 : w.r;
+    double* rout = (i & 1) ? w.r : w.r2;
+    PROF(TCQR_K6_TRI, (double)n * n, tri,
+         CK(cg_launch_tri_n(n, w.M32, n, w.p, w.t, w.part, done, c.stream)));  // t = inv(R) p
+    PROF(TCQR_K5_GEMV, 2.0 * m * n, 4.0 * m * n + 8.0 * m,
+         CK(cg_launch_a_n(m, n, A, lda, w.t, w.q, w.part, w.dpart, done, c.stream)));  // q = A t
+    PROF(TCQR_K7_SCALAR, 0, 0, CK(cg_launch_sum_parts(ndp, w.dpart, &w.st->delta, done, c.stream)));
+    CKR(allreduce_f64(&w.st->delta, 1));
+    PROF(TCQR_K7_SCALAR, 2.0 * n, 24.0 * n, CK(cg_launch_update_x(n, w.st, w.x, w.t, c.stream)));
+    PROF(TCQR_K5_GEMV, 2.0 * m * n, 4.0 * m * n + 32.0 * m,
+         CK(cg_launch_a_t(m, n, A, lda, rin, w.v, w.tpart, done, c.stream, w.q, w.st, rout)));
+    CKR(allreduce_f64(w.v, n));
+    PROF(TCQR_K6_TRI, (double)n * n, tri,
+         CK(cg_launch_tri_t(n, w.M32, n, w.v, w.s, done, c.stream)));  // s = inv(R)' v
+    PROF(TCQR_K7_SCALAR, 4.0 * n, 40.0 * n,
+         CK(cg_launch_finish(n, w.st, w.s, w.p, w.x, w.xbest, w.hist, c.stream)));  // beta, p
+  }
+  return 0;
 }
 
 static int lls_pass(LlsWs& w, int m, int n, const float* A, long long lda, double tol, int maxit,
@@ -1060,36 +1369,43 @@ static int lls_pass(LlsWs& w, int m, int n, const float* A, long long lda, doubl
   CK(cudaMemcpyAsync(w.st, &hs, sizeof hs, cudaMemcpyHostToDevice, c.stream));
   const int* done = &w.st->done;
   // set-up: s = R^-T (A' r)   (Alg. 5 line 7, R-A10 ii)
-  CK(cg_launch_a_t(m, n, A, lda, w.r, w.v, nullptr, c.stream));
+  CK(cg_launch_a_t(m, n, A, lda, w.r, w.v, w.tpart, nullptr, c.stream));
   CKR(allreduce_f64(w.v, n));
-  CK(cg_launch_tri_t(n, w.M, n, w.v, w.s, nullptr, c.stream));
+  CK(cg_launch_tri_t(n, w.M32, n, w.v, w.s, nullptr, c.stream));
   CK(cg_launch_init(n, w.st, w.s, w.p, w.x, w.xbest, c.stream));
-  const int ndp = (m + 255) / 256;
   int launched = 0;
+  constexpr int kChunk = 8;  // iterations enqueued between host reads of the state (even: the
+                             // residual double buffer is back in w.r after a chunk)
+  const std::string gkey = graph_key("cg", {m, n, (long long)A, lda, (long long)w.st});
   while (true) {
-    const int chunk = 8;
-    for (int i = 0; i < chunk; ++i) {
-      const double tri = 4.0 * (double)n * (n + 1);  // FP64 upper triangle, one pass
-      PROF(TCQR_K6_TRI, (double)n * n, tri,
-           CK(cg_launch_tri_n(n, w.M, n, w.p, w.t, w.part, done, c.stream)));   // t = inv(R) p
-      PROF(TCQR_K5_GEMV, 2.0 * m * n, 4.0 * m * n + 8.0 * m,
-           CK(cg_launch_a_n(m, n, A, lda, w.t, w.q, w.part, w.dpart, done, c.stream)));  // q = A t
-      PROF(TCQR_K7_SCALAR, 0, 0, CK(cg_launch_sum_parts(ndp, w.dpart, &w.st->delta, done, c.stream)));
-      CKR(allreduce_f64(&w.st->delta, 1));
-      PROF(TCQR_K7_SCALAR, 2.0 * (m + n), 24.0 * (m + n),
-           CK(cg_launch_update_xr(m, n, w.st, w.x, w.t, w.r, w.q, c.stream)));  // x, r
-      PROF(TCQR_K5_GEMV, 2.0 * m * n, 4.0 * m * n + 8.0 * m,
-           CK(cg_launch_a_t(m, n, A, lda, w.r, w.v, done, c.stream)));          // A' r
-      CKR(allreduce_f64(w.v, n));
-      PROF(TCQR_K6_TRI, (double)n * n, tri,
-           CK(cg_launch_tri_t(n, w.M, n, w.v, w.s, done, c.stream)));           // s
-      PROF(TCQR_K7_SCALAR, 4.0 * n, 40.0 * n,
-           CK(cg_launch_finish(n, w.st, w.s, w.p, w.x, w.xbest, w.hist, c.stream)));  // beta, p
+    if (c.cfg.use_graphs && !g_prof && !c.vg) {
+      // the chunk's 8 x 9 launches (and the NCCL allreduces at P > 1) as one CUDA graph; every
+      // kernel returns at once after the device-side stop (done)
+      auto it = c.graphs.find(gkey);
+      if (it == c.graphs.end()) {
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = cg_chunk(w, m, n, A, lda, kChunk);
+        cudaError_t e = cudaStreamEndCapture(c.stream, &g);
+        if (rc != 0) {
+          if (g) cudaGraphDestroy(g);
+          return rc;
+        }
+        CK(e);
+        GraphEntry ge;
+        e = cudaGraphInstantiate(&ge.exec, g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+        it = c.graphs.emplace(gkey, ge).first;
+      }
+      CK(cudaGraphLaunch(it->second.exec, c.stream));
+    } else {
+      CKR(cg_chunk(w, m, n, A, lda, kChunk));
     }
-    launched += chunk;
+    launched += kChunk;
     CK(cudaMemcpyAsync(&hs, w.st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
-    if (hs.done || launched >= maxit + chunk) break;
+    if (hs.done || launched >= maxit + kChunk) break;
   }
   *iters = hs.k;
   *reason = hs.reason;
@@ -1106,17 +1422,29 @@ static int lls_pass(LlsWs& w, int m, int n, const float* A, long long lda, doubl
 // doubles; part: cg_tri_chunks(n) * n doubles; st: a CgState whose `done` flag is cleared here
 // (the CGLS kernels reused below return early while it is set).
 static int direct_solve(int m, int n, const float* Q, long long ldq, const double* M, long long ldm,
-                        const double* b, double* x, double* t, double* part, CgState* st) {
+                        const double* b, double* x, double* t, double* part, double* tpart,
+                        CgState* st) {
   Context& c = g_ctx;
   CK(cudaMemsetAsync(&st->done, 0, sizeof(int), c.stream));
-  CK(gemv_f32_t(m, n, Q, ldq, b, t, c.stream));
+  CK(gemv_f32_t(m, n, Q, ldq, b, t, tpart, c.stream));
   CKR(allreduce_f64(t, n));
   CK(cg_launch_tri_n(n, M, ldm, t, x, part, &st->done, c.stream));
   return 0;
 }
 
+static int lls_solve_impl(int64_t m, int64_t n, const float* A, int64_t lda, const double* b,
+                          double* x, double tol, int maxit, tcqr_lls_info_t* info);
+
 int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const double* b, double* x,
                    double tol, int maxit, tcqr_lls_info_t* info) {
+  g_ctx.ncoll = 0;
+  const int rc = lls_solve_impl(m, n, A, lda, b, x, tol, maxit, info);
+  if (rc < 0) vabort(g_ctx.vg);
+  return rc;
+}
+
+static int lls_solve_impl(int64_t m, int64_t n, const float* A, int64_t lda, const double* b,
+                          double* x, double tol, int maxit, tcqr_lls_info_t* info) {
   std::lock_guard<std::mutex> lk(g_mu);
   int rc = check_common(m, n, A, lda);
   if (rc) return rc;
@@ -1151,12 +1479,13 @@ int tcqr_lls_solve(int64_t m, int64_t n, const float* A, int64_t lda, const doub
   // K6 set-up: M = inv(R) in FP64 (reading R-A13).
   PROF(TCQR_TRINV, (double)n * n * n / 3.0, 12.0 * n * n,
        CK(trinv_f64((int)n, w.R, n, w.M, n, w.W, c.num_sms, c.stream)));
+  CK(cg_launch_m_to_f32((int)n, w.M, n, w.M32, c.stream));
   int it1 = 0, reason1 = 0, it2 = 0, reason2 = -1;
   double s01 = 0, fr1 = 0, s02 = 0, fr2 = 0;
   if (c.cfg.warm_start) {
     // NEXT-2: x0 = R^-1 Q' b (Alg. 1 lines 3-4) from the factorization's own Q (the working
     // copy) and M = R^-1; pass 1 then iterates on r0 = b - A x0 and x = x0 + dx.
-    CKR(direct_solve((int)m, (int)n, w.Aw, m, w.M, n, b, w.x1, w.t, w.part, w.st));
+    CKR(direct_solve((int)m, (int)n, w.Aw, m, w.M, n, b, w.x1, w.t, w.part, w.tpart, w.st));
     CK(gemv_f32_n((int)m, (int)n, A, lda, w.x1, w.q, w.part, w.part_cap, c.stream));
     CK(cg_launch_residual((int)m, b, w.q, w.r, c.stream));
   } else {
@@ -1461,15 +1790,17 @@ int tcqr_qr_solve(int64_t m, int64_t n, const float* Q, int64_t ldq, const float
   CK(cudaStreamSynchronize(c.stream));
   for (int64_t k = 0; k < n; ++k)
     if (!(d[k] != 0.f) || !std::isfinite(d[k])) return (int)(k + 1);
-  double *M = nullptr, *W = nullptr, *t = nullptr, *part = nullptr;
+  double *M = nullptr, *W = nullptr, *t = nullptr, *part = nullptr, *tpart = nullptr;
   CgState* st = nullptr;
+  CK(cudaMallocAsync(&tpart, sizeof(double) * cg_gemv_t_part_count((int)m, (int)n), c.stream));
   CK(cudaMallocAsync(&M, sizeof(double) * n * n, c.stream));
   CK(cudaMallocAsync(&W, sizeof(double) * trinv_w_count(n), c.stream));
   CK(cudaMallocAsync(&t, sizeof(double) * n, c.stream));
   CK(cudaMallocAsync(&part, sizeof(double) * cg_tri_chunks((int)n) * n, c.stream));
   CK(cudaMallocAsync(&st, sizeof(CgState), c.stream));
   CK(trinv_f64((int)n, R, ldr, M, n, W, c.num_sms, c.stream));
-  const int rc = direct_solve((int)m, (int)n, Q, ldq, M, n, b, x, t, part, st);
+  const int rc = direct_solve((int)m, (int)n, Q, ldq, M, n, b, x, t, part, tpart, st);
+  cudaFreeAsync(tpart, c.stream);
   cudaFreeAsync(M, c.stream);
   cudaFreeAsync(W, c.stream);
   cudaFreeAsync(t, c.stream);
@@ -1553,7 +1884,10 @@ int tcqr_gemv(int trans, int64_t m, int64_t n, const float* A, int64_t lda, cons
     CK(gemv_f32_n((int)m, (int)n, A, lda, v, y, part, cap, c.stream));
     cudaFreeAsync(part, c.stream);
   } else {
-    CK(gemv_f32_t((int)m, (int)n, A, lda, v, y, c.stream));
+    double* part = nullptr;
+    CK(cudaMallocAsync(&part, sizeof(double) * cg_gemv_t_part_count((int)m, (int)n), c.stream));
+    CK(gemv_f32_t((int)m, (int)n, A, lda, v, y, part, c.stream));
+    cudaFreeAsync(part, c.stream);
   }
   CK(cudaStreamSynchronize(c.stream));
   return 0;

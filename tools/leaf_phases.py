@@ -13,7 +13,7 @@ L.tcqr_debug_leaf_timestamps.argtypes = [ctypes.c_void_p]
 names = ["load"]
 for op in ["P0", "J01", "P1", "J0123", "P2", "J23", "P3"]:
     if op[0] == "P":
-        names += [op + s for s in (":mgs", ":gram+bar", ":sum", ":bar", ":chol+S", ":apply")]
+        names += [op + s for s in (":mgs", ":gram+bar", ":sum", ":bar", ":chol+S", ":apply+st")]
     else:
         names += [op + s for s in (":partial", ":bar", ":sum", ":bar", ":update")]
 names += ["write"]
@@ -26,7 +26,7 @@ for m in [int(v) for v in (sys.argv[1:] or ["32768"])]:  # m <= 148 * 256 (leaf 
     for _ in range(3):
         tq.factor(A, Q, R)
     L.tcqr_debug_leaf_timestamps(ctypes.c_void_p(dbg.data_ptr()))
-    runs, extra = [], []
+    runs, extra, probes = [], [], []
     for _ in range(5):
         dbg.zero_()
         tq.factor(A, Q, R)
@@ -34,9 +34,13 @@ for m in [int(v) for v in (sys.argv[1:] or ["32768"])]:  # m <= 148 * 256 (leaf 
         d = dbg.cpu().numpy().astype(np.int64)
         runs.append(np.diff(d[:len(names) + 1]) / 1000.0)
         extra.append(((d[102] - d[100]) / 1000.0, (d[104] - d[102]) / 1000.0, (d[101] - d[100]) / 1000.0))
+        probes.append(d[110:116].copy())
     L.tcqr_debug_leaf_timestamps(None)
     med = np.median(np.array(runs), axis=0)
-    print(f"m={m}: total {med.sum():.1f} us; last panel: chol+S {np.median([e[0] for e in extra]):.2f} us, "
-          f"apply before stores {np.median([e[1] for e in extra]):.2f} us, chol input loads {np.median([e[2] for e in extra]):.2f} us")
+    print(f"m={m}: total {med.sum():.1f} us; last panel: chol {np.median([e[0] for e in extra]):.2f} us, "
+          f"S + apply before stores {np.median([e[1] for e in extra]):.2f} us")
+    pr = np.median(np.array(probes), axis=0)
+    print("  MGS step 5 of panel 2, warp 0 (cycles): colbuf+dot %d, shfl %d, sqrt/rcp/rkj %d, "
+          "R+q publish %d, update %d, column publish %d" % tuple(pr))
     for nm, v in zip(names, med):
         print(f"  {nm:16s} {v:7.2f}")
