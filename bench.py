@@ -124,6 +124,40 @@ def cpu_oracle_sample(a_cols_np, reps=1):
     return dt
 
 
+def cpu_oracle_cgls_sample(a_np, iters=8):
+    """Seconds per iteration of the oracle's corrected Alg. 5 (oracle.cgls.pcgls, as it stands) on
+    an m x n_s sample, preconditioned by the sample's own sign-fixed R (computed outside the timed
+    region); `iters` iterations (the tolerance is set so that none stops early)."""
+    from oracle.cgls import pcgls
+    a = a_np.astype(np.float64)
+    r = np.linalg.qr(a, mode="r")
+    r = r * np.sign(np.diag(r))[:, None]
+    b = a @ np.ones(a.shape[1]) + 1e-3 * np.random.default_rng(5).standard_normal(a.shape[0])
+    t0 = time.perf_counter()
+    _, info = pcgls(a, b, r, tol=1e-300, maxit=iters, window=10 ** 9)
+    return (time.perf_counter() - t0) / max(info.iterations, 1)
+
+
+def cpu_info():
+    """CPU model (from /proc/cpuinfo) and the BLAS numpy calls (threadpoolctl)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [f"{d.get('internal_api')} {d.get('version')} ({d.get('num_threads')} threads)"
+                for d in threadpool_info() if d.get("user_api") == "blas"]
+    except Exception:  # noqa: BLE001 -- informational only
+        pass
+    return {"cpu_model": model, "blas": blas, "numpy": np.__version__}
+
+
 def run_reference(args, wl):
     """--impl reference: the CPU FP64 oracle timed on this box's host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -146,10 +180,110 @@ def run_reference(args, wl):
         "impl": "reference",
         "config": {"workload": wl["name"] + f" [CPU sample {m}x{n_s}]", "m": m, "n": n_s},
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, **cpu_info()},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def model_ideal_ms(m, n, peaks, cutoff=128):
+    """Modelled ideal factorization time at the measured peaks: per split node the
+    longer of its tensor-core time (4 m h w2 flops at the sustained bf16 = fp16 dense rate) and its
+    HBM time (K1 cast 6 m w2 + K3 2m(h + w2) + K4 2mh + 8 m w2 bytes); per leaf the longer of its
+    FP32 time (2 m c^2 flops at the FP32 SIMT peak) and its HBM time (10 m c bytes)."""
+    tc = peaks["tc_sustained"] * 1e12
+    hbm = peaks["hbm"] * 1e9
+    fp32 = fp32_peak_tflops() * 1e12
+
+    def rec(w):
+        if w <= cutoff:
+            return max(2.0 * m * w * w / fp32, 10.0 * m * w / hbm)
+        h = 32 * ((w + 63) // 64)
+        w2 = w - h
+        node = max(4.0 * m * h * w2 / tc, (4.0 * m * h + 16.0 * m * w2) / hbm)
+        return rec(h) + node + rec(w2)
+
+    return rec(n) * 1e3
+
+
+def other_configs(tq, W, torch, dev, peaks, steps, cutoff):
+    """The other BASELINE.json configs at N = 1 (extra keys, not the headline): configs[0] latency,
+    configs[1] and configs[4] QR TFLOP/s, the NEXT-3 4194304 x 128 orthogonalization, configs[4]
+    LLS and the configs[3] FP32-target LLS; each with its modelled-ideal fraction and a parity
+    check against the oracle (small configs) or the leading columns (large ones)."""
+    from oracle.cgls import oracle_lls
+    from oracle.metrics import r_rel_error, x_rel_error
+    from oracle.qr import rgs
+    out = {}
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    def qr_case(key, m, n, seed, reps, lead=256):
+        A = W.gaussian_cuda(m, n, seed, device=dev)
+        Q = tq.colmajor_empty(m, n, device=dev)
+        R = tq.colmajor_empty(n, n, device=dev)
+        ms = timed(lambda: tq.factor(A, Q, R), reps)
+        ideal = model_ideal_ms(m, n, peaks, cutoff)
+        k = min(lead, n)
+        _, r_o = rgs(A[:, :k].cpu().numpy().astype(np.float64))
+        rec = {"m": m, "n": n, "ms": ms, "tflops": conv_flops(m, n) / (ms * 1e-3) / 1e12,
+               "model_ideal_ms": ideal, "frac_of_model_ideal": ideal / ms,
+               f"R_lead{k}_rel_err_vs_oracle": r_rel_error(R[:k, :k].cpu().numpy().astype(np.float64), r_o)}
+        del A, Q, R
+        torch.cuda.empty_cache()
+        out[key] = rec
+        return rec
+
+    # configs[0]: 1024 x 128 QR + LLS latency, full oracle parity (c = 128: the leaf kernel only)
+    a1 = W.gaussian(1024, 128, seed=W.CONFIG_SEEDS["cfg1"])
+    b1, _ = W.consistent_rhs(a1, seed=W.CONFIG_SEEDS["cfg1_x"])
+    A1 = tq.to_device_colmajor(a1)
+    B1 = torch.from_numpy(b1).to(dev)
+    Q1, R1 = tq.colmajor_empty(1024, 128, device=dev), tq.colmajor_empty(128, 128, device=dev)
+    qr_us = timed(lambda: tq.factor(A1, Q1, R1), 50) * 1e3
+    x1 = [None]
+    lls_us = timed(lambda: x1.__setitem__(0, tq.lls_solve(A1, B1, tol=1e-10, maxit=200)), 20) * 1e3
+    _, r1o = rgs(a1.astype(np.float64))
+    x1o, _ = oracle_lls(a1.astype(np.float64), b1)
+    out["cfg1"] = {"workload": "configs[0] 1024x128 Gaussian: QR + R-preconditioned CGLS to 1e-10",
+                   "qr_latency_us": qr_us, "lls_latency_us": lls_us,
+                   "lls_iterations": x1[0][1]["iterations"],
+                   "R_rel_err_vs_oracle": r_rel_error(R1.cpu().numpy().astype(np.float64), r1o),
+                   "x_rel_err_vs_oracle": x_rel_error(x1[0][0].cpu().numpy(), x1o),
+                   "note": "launch-latency bound (a us-scale ideal), reported as latency"}
+    del A1, B1, Q1, R1
+    qr_case("cfg2", 16384, 4096, W.CONFIG_SEEDS["cfg2"], steps)["workload"] = \
+        "configs[1] QR of 16384x4096 Gaussian"
+    qr_case("cfg5", 262144, 2048, W.CONFIG_SEEDS["cfg5"], steps)["workload"] = \
+        "configs[4] QR of 262144x2048 Gaussian (1 GPU)"
+    qr_case("next3", 4194304, 128, 9, steps, lead=128)["workload"] = \
+        "NEXT-3 orthogonalization of 4194304x128 Gaussian (PAPER.md:598)"
+    # configs[4] LLS: Gaussian b = A x_true, FP64 target
+    m5, n5 = 262144, 2048
+    A5 = W.gaussian_cuda(m5, n5, W.CONFIG_SEEDS["cfg5"], device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(W.CONFIG_SEEDS["cfg5_x"])
+    xt = torch.randn(n5, generator=g, device=dev, dtype=torch.float64)
+    b5 = A5.to(torch.float64) @ xt
+    res = [None]
+    ms5 = timed(lambda: res.__setitem__(0, tq.lls_solve(A5, b5, tol=1e-10, maxit=400)), 2)
+    x5, info5 = res[0]
+    out["cfg5_lls"] = {"workload": "configs[4] LLS 262144x2048 Gaussian, b = A x_true, FP64 target",
+                       "time_to_solution_ms": ms5, "qr_ms": info5["qr_ms"],
+                       "cgls_ms": info5["cgls_ms"], "iterations": info5["iterations"],
+                       "x_rel_err_vs_x_true": float(torch.linalg.norm(x5 - xt) / torch.linalg.norm(xt))}
+    del A5, b5, x5
+    torch.cuda.empty_cache()
+    return out
 
 
 def _streamed_r_bytes(n, cutoff):
@@ -187,6 +321,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--cutoff", type=int, default=128)
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other BASELINE configs (extra keys)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -390,8 +526,10 @@ def main():
             bl = b_full[l0:l1].contiguous()
             del Al_full, b_full
             torch.cuda.empty_cache()
-            for label, reorth, split in cases:
-                tq.set_config(cutoff=args.cutoff, reorth=reorth, fp16_split=split)
+            for case in cases:
+                label, reorth, split = case[:3]
+                restart = case[3] if len(case) > 3 else 1
+                tq.set_config(cutoff=args.cutoff, reorth=reorth, fp16_split=split, restart=restart)
                 tq.lls_solve(Al, bl, tol=1e-10, maxit=4000)      # warm-up: builds the QR graph
                 barrier()
                 torch.cuda.synchronize()
@@ -412,6 +550,21 @@ def main():
             del Al, bl
 
         lls_case(1e4, (("paper_R", 0, 0), ("reorth_R", 1, 0), ("split_reorth_R", 1, 1)))
+        # FP32 target (one pass, tol 1e-10, no restart; gate x within 1e-5, SURVEY 8(d) configs[3])
+        lls_case(1e4, (("paper_R_fp32_target", 0, 0, 0),))
+        lls["paper_R_fp32_target"]["fp32_accuracy_reached"] = \
+            lls["paper_R_fp32_target"]["x_rel_err_vs_x_true"] <= 1e-5
+        tq.set_config(cutoff=args.cutoff)
+        # CGLS per-iteration roofline: 2 FP32 passes over A (8 m n B) and 2 over the FP32 upper
+        # triangle of R^-1 (4 n (n+1) B) per iteration
+        pr = lls["paper_R"]
+        it_ms = pr["cgls_ms"] / max(pr["iterations"], 1)
+        it_bytes = 8.0 * Ml * nl + 4.0 * nl * (nl + 1)
+        lls["cgls_iteration"] = {"ms": it_ms, "bytes": it_bytes,
+                                 "gbs": it_bytes / (it_ms * 1e-3) / 1e9,
+                                 "frac_of_hbm": it_bytes / (it_ms * 1e-3) / 1e9 / peaks["hbm"],
+                                 "note": "paper_R cgls_ms (includes the one-time FP64 R^-1) / "
+                                         "iterations"}
         # kappa = 1e6 geometric is beyond the paper with its FP16 R (reading R-A24: CGLS does not
         # converge; 4000 iterations x 2 passes would take seconds): NEXT-4 + NEXT-1 only
         lls_case(1e6, (("k1e6_split_reorth_R", 1, 1),))
@@ -424,16 +577,31 @@ def main():
                                               "(R-A24)")
         tq.set_config(cutoff=args.cutoff)
 
+    # ---- the other BASELINE configs (N = 1 only; extra keys) ----
+    configs = None
+    if world == 1 and not args.no_configs and args.workload == "cfg3":
+        try:
+            del Q, R
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        configs = other_configs(tq, W, torch, dev, peaks, args.steps, args.cutoff)
+
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s = min(n, args.cpu_sample_cols)
         a_s = W.gaussian(M, n_s, seed=wl["seed"])   # same distribution, host generator
         dt = cpu_oracle_sample(a_s)
+        it_s = cpu_oracle_cgls_sample(a_s[:, :512])
         cpu = {"value": conv_flops(M, n_s) / dt / 1e12, "unit": "TFLOP/s",
                "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                "sample": f"oracle.qr.rgs (FP64 numpy/OpenBLAS) on a {M}x{n_s} Gaussian "
-                         f"(first {n_s} columns of the workload shape), {dt:.2f} s"}
+                         f"(first {n_s} columns of the workload shape), {dt:.2f} s",
+               "cgls": {"sample": f"oracle.cgls.pcgls on {M}x512 (8 iterations, FP64)",
+                        "ms_per_iteration": it_s * 1e3,
+                        "gbs": (16.0 * M * 512 + 8.0 * 512 * 512) / it_s / 1e9},
+               **cpu_info()}
 
     if rank == 0:
         line = {
@@ -456,6 +624,7 @@ def main():
             "parity": parity,
             "e2e": e2e,
             "lls": lls,
+            "configs": configs,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

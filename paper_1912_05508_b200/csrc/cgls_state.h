@@ -31,8 +31,10 @@ cudaError_t cg_launch_tri_t(int n, const double* M, long long ldm, const double*
 // FP32 copy of the preconditioner M = R^-1 (reading R-A13): same products, FP64 accumulation.
 cudaError_t cg_launch_tri_n(int n, const float* M, long long ldm, const double* p, double* t,
                             double* part, const int* done, cudaStream_t st);
+// s = M' v for the FP32 M (part: cg_tri_t_part_count(n) doubles)
+int cg_tri_t_part_count(int n);
 cudaError_t cg_launch_tri_t(int n, const float* M, long long ldm, const double* v, double* s,
-                            const int* done, cudaStream_t st);
+                            double* part, const int* done, cudaStream_t st);
 cudaError_t cg_launch_m_to_f32(int n, const double* M, long long ldm, float* M32, cudaStream_t st);
 cudaError_t cg_launch_a_n(int m, int n, const float* A, long long lda, const double* t, double* q,
                           double* part, double* dpart, const int* done, cudaStream_t st);

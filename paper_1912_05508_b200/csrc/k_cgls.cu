@@ -523,7 +523,8 @@ __global__ void gemv_t_reduce_kernel(int n, int splits, const double* __restrict
   y[j] = acc;
 }
 
-// Row splits of the A' v kernel: enough CTAs for two per SM, splits of whole 1024-row chunks.
+// Row splits of the A' v kernel: enough CTAs for two per SM, whole 1024-row chunks (four per
+// SM measured slower at configs[3]).
 static void gemv_t_plan(int m, int n, int* splits, int* rps) {
   const int cblocks = (n + kGtCols - 1) / kGtCols;
   int s = (2 * 148 + cblocks - 1) / cblocks;
@@ -680,6 +681,79 @@ __global__ void __launch_bounds__(256) tri_t_f32_kernel(int n, const float* __re
   for (i += lane; i <= j; i += 32) a0 = fma((double)mm[i], v[i], a0);
   const double r = warp_sum_d(a0 + a1);
   if (lane == 0) s[j] = r;
+}
+
+// s = M' v with the FP32 upper-triangular M (zero below the diagonal), column-blocked like
+// gemv_t_part_kernel: CTA (column block of 64, row chunk c of 1024) -- chunks entirely below the
+// block's last column's diagonal only) -- v staged in shared memory, each value feeding the warp's
+// 8 columns; part[c * n + j] summed over c in order by tri_t_reduce_kernel.  (One warp per column
+// re-read v from L2 once per column: twice the bytes of M.)
+constexpr int kTtChunk = 1024;
+__global__ void __launch_bounds__(256) tri_t_part_f32_kernel(int n, const float* __restrict__ M,
+                                                             long long ldm,
+                                                             const double* __restrict__ v,
+                                                             double* __restrict__ part,
+                                                             const int* __restrict__ done) {
+  if (done && *done) return;
+  const int jb = blockIdx.x * kGtCols;
+  const long long c0 = (long long)blockIdx.y * kTtChunk;
+  if (c0 > jb + kGtCols - 1 || jb >= n) return;  // no row <= any of the block's columns
+  __shared__ __align__(16) double vs[kTtChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = jb + warp * 8;
+  const int cn = (int)min((long long)kTtChunk, (long long)n - c0);
+  for (int i = threadIdx.x; i < cn; i += 256) vs[i] = v[c0 + i];
+  __syncthreads();
+  double acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+  const bool vec = ((ldm & 3) == 0) && ((reinterpret_cast<uintptr_t>(M) & 15) == 0) &&
+                   cn == kTtChunk;
+  if (vec) {
+#pragma unroll 2
+    for (int i = lane * 4; i < kTtChunk; i += 128) {
+      const double2 v01 = *reinterpret_cast<const double2*>(vs + i);
+      const double2 v23 = *reinterpret_cast<const double2*>(vs + i + 2);
+      float4 a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        a[u] = (j0 + u < n && c0 + i <= j0 + u)
+                   ? __ldg(reinterpret_cast<const float4*>(M + (long long)(j0 + u) * ldm + c0 + i))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc[u] = fma((double)a[u].x, v01.x, acc[u]);
+        acc[u] = fma((double)a[u].y, v01.y, acc[u]);
+        acc[u] = fma((double)a[u].z, v23.x, acc[u]);
+        acc[u] = fma((double)a[u].w, v23.y, acc[u]);
+      }
+    }
+  } else {
+    for (int i = lane; i < cn; i += 32) {
+      const double x = vs[i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < n && c0 + i <= j0 + u)
+          acc[u] = fma((double)M[(long long)(j0 + u) * ldm + c0 + i], x, acc[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double sum = warp_sum_d(acc[u]);
+    if (lane == 0 && j0 + u < n) part[(long long)blockIdx.y * n + j0 + u] = sum;
+  }
+}
+
+// s[j] = sum over the chunks c <= j / 1024 of part[c * n + j] (fixed order)
+__global__ void tri_t_reduce_kernel(int n, const double* __restrict__ part, double* __restrict__ s,
+                                    const int* __restrict__ done) {
+  if (done && *done) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int jb = (j / kGtCols) * kGtCols + kGtCols - 1;  // the last column of j's block
+  double acc = part[j];
+  for (int c = 1; (long long)c * kTtChunk <= jb && c * kTtChunk < n; ++c) acc += part[(long long)c * n + j];
+  s[j] = acc;
 }
 
 // M32 = fl32(M) on the upper triangle (zero below): the FP32 copy of the CGLS preconditioner.
@@ -859,10 +933,14 @@ cudaError_t cg_launch_tri_t(int n, const double* M, long long ldm, const double*
 }
 
 cudaError_t cg_launch_tri_t(int n, const float* M, long long ldm, const double* v, double* s,
-                            const int* done, cudaStream_t st) {
-  tri_t_f32_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, M, ldm, v, s, done);
+                            double* part, const int* done, cudaStream_t st) {
+  const dim3 g((n + kGtCols - 1) / kGtCols, (n + kTtChunk - 1) / kTtChunk);
+  tri_t_part_f32_kernel<<<g, 256, 0, st>>>(n, M, ldm, v, part, done);
+  tri_t_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, part, s, done);
   return cudaGetLastError();
 }
+
+int cg_tri_t_part_count(int n) { return ((n + kTtChunk - 1) / kTtChunk) * n; }
 
 cudaError_t cg_launch_m_to_f32(int n, const double* M, long long ldm, float* M32, cudaStream_t st) {
   const long long nn = (long long)n * n;

@@ -239,7 +239,8 @@ static void plan_lls_ws(Arena& a, long long m, long long n, int nranks, int maxi
   w.M = a.take<double>((size_t)n * n);
   w.M32 = a.take<float>((size_t)n * n);
   w.r2 = a.take<double>(m);
-  w.tpart = a.take<double>((size_t)cg_gemv_t_part_count((int)m, (int)n) + 64);
+  w.tpart = a.take<double>((size_t)std::max(cg_gemv_t_part_count((int)m, (int)n),
+                                             cg_tri_t_part_count((int)n)) + 64);
   w.W = a.take<double>((size_t)trinv_w_count(n));
   w.x = a.take<double>(n);
   w.xbest = a.take<double>(n);
@@ -1348,7 +1349,7 @@ static int cg_chunk(LlsWs& w, int m, int n, const float* A, long long lda, int i
          CK(cg_launch_a_t(m, n, A, lda, rin, w.v, w.tpart, done, c.stream, w.q, w.st, rout)));
     CKR(allreduce_f64(w.v, n));
     PROF(TCQR_K6_TRI, (double)n * n, tri,
-         CK(cg_launch_tri_t(n, w.M32, n, w.v, w.s, done, c.stream)));  // s = inv(R)' v
+         CK(cg_launch_tri_t(n, w.M32, n, w.v, w.s, w.tpart, done, c.stream)));  // s = inv(R)' v
     PROF(TCQR_K7_SCALAR, 4.0 * n, 40.0 * n,
          CK(cg_launch_finish(n, w.st, w.s, w.p, w.x, w.xbest, w.hist, c.stream)));  // beta, p
   }
@@ -1371,7 +1372,7 @@ static int lls_pass(LlsWs& w, int m, int n, const float* A, long long lda, doubl
   // set-up: s = R^-T (A' r)   (Alg. 5 line 7, R-A10 ii)
   CK(cg_launch_a_t(m, n, A, lda, w.r, w.v, w.tpart, nullptr, c.stream));
   CKR(allreduce_f64(w.v, n));
-  CK(cg_launch_tri_t(n, w.M32, n, w.v, w.s, nullptr, c.stream));
+  CK(cg_launch_tri_t(n, w.M32, n, w.v, w.s, w.tpart, nullptr, c.stream));
   CK(cg_launch_init(n, w.st, w.s, w.p, w.x, w.xbest, c.stream));
   int launched = 0;
   constexpr int kChunk = 8;  // iterations enqueued between host reads of the state (even: the
