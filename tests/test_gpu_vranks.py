@@ -197,6 +197,19 @@ def test_vranks_planted_hadamard_zero_padded_bitwise(tq, P, leaf_kernel, cutoff)
         assert not np.any(q)
 
 
+def test_vranks_planted_hadamard_all_ranks_bitwise(tq):
+    # P2 at 16384 = 4 x 4096 rows, every rank holding Hadamard rows (no padding): each rank's
+    # 256-row K2L blocks, 64-row MGS blocks and its 64-block local stack, and the 4-rank stack, are
+    # all powers of 4 -> R == R0 and Q == H / sqrt(m) bitwise on every rank
+    m, n, P = 16384, 256, 4
+    a, qt, r0 = W.planted_hadamard(m, n, seed=204)
+    qs, rs, res, bounds = _vfactor(tq, a, P)
+    assert all(rc == 0 for rc, _ in res), res
+    for r in rs:
+        assert np.array_equal(r, r0)
+    assert np.array_equal(np.vstack(qs), qt)
+
+
 def _vlls(tq, a, b, P, tol=1e-10, maxit=200, **cfg):
     m, n = a.shape
     A = tq.to_device_colmajor(a)
