@@ -389,6 +389,8 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
   }
   tc_fence_before();
   cluster_sync_all();  // barriers of both CTAs initialized, TMEM allocated
+  __syncthreads();     // (also a CTA barrier: compute-sanitizer's racecheck orders the tcgen05.alloc
+                       // write of tmem_slot before the reads below only through a CTA barrier)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 

@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
       // completed (a named barrier must not see arrivals of two generations with different counts)
       if (wid > 0) {
         if (tb == 0)
-          while (*reinterpret_cast<volatile int*>(&s_step) < kfirst - 1) __nanosleep(20);
+          while (atomicAdd(&s_step, 0) < kfirst - 1) __nanosleep(20);  // flag: shared atomics
         __syncwarp();
       }
       for (int k = kfirst; k < w; ++k) {
@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(NT, 1) panel_pipe_kernel(PipeArgs a) {
         const int cnt = 32 * min(nwa, (k + 1) / 4 + 1);  // warps joined at step k
         mgs_step_any<NT, RPT>(x, NT * RPT, w, k, qp, 32 * w, Rsm, 1, 32,
                               a.root_is_global != 0, a.status, a.col0, red, buf, k < i0, cnt);
-        if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(&s_step) = k;  // barrier k passed
+        if (threadIdx.x == 0) atomicExch(&s_step, k);  // barrier k passed
       }
     }
     __syncthreads();
