@@ -311,8 +311,17 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   // (1) Alg. 4 on the CTA's four 64-row blocks, one warp each (rows >= nrows are zero), and each
-  // block's Gram R_b' R_b
-  if (warp < kMW) mgs_warp(s, warp, c0, pw);
+  // block's Gram R_b' R_b; blocks entirely past the CTA's rows (CTAs of 64 or 128 rows) only clear
+  // their R_b and Gram (an all-zero block would take the divide's special-value path every step)
+  if (warp < kMW) {
+    if (warp * kBR < nrows) {
+      mgs_warp(s, warp, c0, pw);
+    } else {
+#pragma unroll 4
+      for (int k = 0; k < 32; ++k) s.Rbd[warp][k * kLdR + lane] = 0.0;
+      for (int e = lane; e < 528; e += 32) s.u.Gp[warp][e] = 0.0;
+    }
+  }
   __syncthreads();
   leaf_ts(a, slot);
   // (2) the CTA's part of the stack's Gram: G = (G_0 + G_1) + (G_2 + G_3) (FP64, fixed order;
@@ -525,6 +534,51 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
   leaf_ts(a, slot);
   for (int e = t; e < H * W2P; e += kNT) s.u.T[e] = __ldcg(a.r12 + e);
   __syncthreads();
+  if (nrows <= 128) {
+    // A2 -= Q1 R12 for CTAs of <= 128 rows: thread = row t % 128, columns [jq * W2P/4, ...)
+    constexpr int JQ = W2P / 4;
+    const int r = t % 128, jq = t / 128 * 2;  // two column quarters per thread: jq, jq + 1
+    if (r < nrows) {
+      float u[2 * JQ];
+#pragma unroll
+      for (int j = 0; j < 2 * JQ; ++j) u[j] = 0.f;
+      const float* qa = s.L + r * kLd + c0;
+#pragma unroll 2
+      for (int i4 = 0; i4 < H; i4 += 4) {
+        const float4 va = *reinterpret_cast<const float4*>(qa + i4);
+        const float qx[4] = {va.x, va.y, va.z, va.w};
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          const float4* tr = reinterpret_cast<const float4*>(s.u.T + (i4 + ii) * W2P + jq * JQ);
+          const float2 qi = make_float2(qx[ii], qx[ii]);
+#pragma unroll
+          for (int j4 = 0; j4 < JQ / 2; ++j4) {
+            const float4 v = tr[j4];
+            const float2 c01 = ffma2(qi, make_float2(v.x, v.y), make_float2(u[4 * j4], u[4 * j4 + 1]));
+            const float2 c23 = ffma2(qi, make_float2(v.z, v.w),
+                                     make_float2(u[4 * j4 + 2], u[4 * j4 + 3]));
+            u[4 * j4] = c01.x;
+            u[4 * j4 + 1] = c01.y;
+            u[4 * j4 + 2] = c23.x;
+            u[4 * j4 + 3] = c23.y;
+          }
+        }
+      }
+      float* dst = s.L + r * kLd + c0 + H + jq * JQ;
+#pragma unroll
+      for (int j4 = 0; j4 < JQ / 2; ++j4) {
+        float4 v = *reinterpret_cast<float4*>(dst + 4 * j4);
+        v.x -= u[4 * j4];
+        v.y -= u[4 * j4 + 1];
+        v.z -= u[4 * j4 + 2];
+        v.w -= u[4 * j4 + 3];
+        *reinterpret_cast<float4*>(dst + 4 * j4) = v;
+      }
+    }
+    __syncthreads();
+    leaf_ts(a, slot);
+    return;
+  }
   // A2 -= Q1 R12: thread = rows (t % 128, t % 128 + 128), columns [jh * W2P/2, (jh+1) * W2P/2)
   constexpr int JC = W2P / 2;
   const int r0 = t % 128, jh = t / 128;
@@ -752,7 +806,11 @@ cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long 
                        long long ldr, int col0, int* status, void* scratch, size_t scratch_bytes,
                        unsigned* bar, unsigned* bar_seq, int num_sms, cudaStream_t st) {
   if (wl < 1 || wl > kCols || m < wl) return cudaErrorNotSupported;
-  const int nb = (m + kRows - 1) / kRows;
+  // rows per CTA: the fewest 64-row MGS blocks per CTA that still fit the rows in one CTA per SM
+  // (the MGS and Cholesky chains take the same time for 1 to 4 blocks, the projections and the
+  // Q_b S_b apply scale with the CTA's rows): 64 up to 148 x 64 rows, 128 up to 148 x 128, else 256
+  const int rows_cta = m <= num_sms * 64 ? 64 : (m <= num_sms * 128 ? 128 : kRows);
+  const int nb = (m + rows_cta - 1) / rows_cta;
   static int per_sm = -1;
   const int smem = (int)sizeof(Smem);
   if (per_sm < 0) {
