@@ -29,10 +29,10 @@ __global__ void __launch_bounds__(256) f32_tn_kernel(int m, int h, int w2,
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
-  for (long long c0 = r0; c0 < r1; c0 += kTnRows) {
-    __syncthreads();
-    // all 32 loads of this thread in flight before any shared store (latency-bound otherwise)
-    float qv_[16], av_[16];
+  // software-pipelined: the next chunk's 32 loads per thread are in flight while the current
+  // chunk (staged in shared memory) is multiplied
+  float qv_[16], av_[16];
+  auto fetch = [&](long long c0) {
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int e = tid + u * 256;
@@ -42,6 +42,10 @@ __global__ void __launch_bounds__(256) f32_tn_kernel(int m, int h, int w2,
       qv_[u] = (rok && cc < h) ? __ldg(Q1 + row + cc * ldq) : 0.f;
       av_[u] = (rok && cc < w2) ? __ldg(A2 + row + cc * lda) : 0.f;
     }
+  };
+  if (r0 < r1) fetch(r0);
+  for (long long c0 = r0; c0 < r1; c0 += kTnRows) {
+    __syncthreads();
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int e = tid + u * 256;
@@ -50,6 +54,7 @@ __global__ void __launch_bounds__(256) f32_tn_kernel(int m, int h, int w2,
       As[rr][cc] = av_[u];
     }
     __syncthreads();
+    if (c0 + kTnRows < r1) fetch(c0 + kTnRows);
 #pragma unroll 4
     for (int rr = grp; rr < kTnRows; rr += 4) {
       const float4 q0 = *reinterpret_cast<const float4*>(&Qs[rr][ti * 8]);
@@ -57,11 +62,18 @@ __global__ void __launch_bounds__(256) f32_tn_kernel(int m, int h, int w2,
       const float4 a0 = *reinterpret_cast<const float4*>(&As[rr][tj * 8]);
       const float4 a1 = *reinterpret_cast<const float4*>(&As[rr][tj * 8 + 4]);
       const float qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float2 av2[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w),
+                             make_float2(a1.x, a1.y), make_float2(a1.z, a1.w)};
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < 8; ++a) {  // FFMA2: the same fmaf sequence per entry
+        const float2 qa = make_float2(qv[a], qv[a]);
 #pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(qv[a], av[b], acc[a][b]);
+        for (int b2 = 0; b2 < 4; ++b2) {
+          const float2 c = ffma2(qa, av2[b2], make_float2(acc[a][2 * b2], acc[a][2 * b2 + 1]));
+          acc[a][2 * b2] = c.x;
+          acc[a][2 * b2 + 1] = c.y;
+        }
+      }
     }
   }
   // combine the 4 row groups in a fixed order (deterministic)
@@ -139,13 +151,16 @@ __global__ void __launch_bounds__(128) f32_nn_kernel(int m, int h, int w2,
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       if (i0 + u < h) {
+        const float2 qu = make_float2(qb[u], qb[u]);
 #pragma unroll
-        for (int j = 0; j < W2; j += 4) {
+        for (int j = 0; j < W2; j += 4) {  // FFMA2: the same fmaf sequence per entry
           const float4 tv = *reinterpret_cast<const float4*>(&Ts[i0 + u][j]);
-          acc[j] = fmaf(qb[u], tv.x, acc[j]);
-          acc[j + 1] = fmaf(qb[u], tv.y, acc[j + 1]);
-          acc[j + 2] = fmaf(qb[u], tv.z, acc[j + 2]);
-          acc[j + 3] = fmaf(qb[u], tv.w, acc[j + 3]);
+          const float2 c01 = ffma2(qu, make_float2(tv.x, tv.y), make_float2(acc[j], acc[j + 1]));
+          const float2 c23 = ffma2(qu, make_float2(tv.z, tv.w), make_float2(acc[j + 2], acc[j + 3]));
+          acc[j] = c01.x;
+          acc[j + 1] = c01.y;
+          acc[j + 2] = c23.x;
+          acc[j + 3] = c23.y;
         }
       }
     }
@@ -158,14 +173,61 @@ __global__ void __launch_bounds__(128) f32_nn_kernel(int m, int h, int w2,
     if (j < w2) A2[row + (long long)j * lda] = cold[j] - acc[j];
 }
 
+// The same for 32 < w2 <= 64 with two threads per row (64 rows per CTA, thread g = threadIdx.x / 64
+// takes columns [32 g, 32 g + 32)): the one-thread-per-row version held 64 accumulators and 64
+// old values (255 registers with spills, one CTA per SM).  The two threads of a row read the same
+// Q1 values (the second read hits L1).
+__global__ void __launch_bounds__(128) f32_nn2_kernel(int m, int h, int w2,
+                                                      const float* __restrict__ Q1, long long ldq,
+                                                      const float* __restrict__ T,
+                                                      float* __restrict__ A2, long long lda) {
+  __shared__ __align__(16) float Ts[64][64];
+  for (int e = threadIdx.x; e < h * 64; e += blockDim.x) {
+    const int i = e / 64, j = e % 64;
+    Ts[i][j] = (j < w2) ? T[i + (long long)j * h] : 0.f;
+  }
+  __syncthreads();
+  const int g = threadIdx.x >> 6;
+  const long long row = (long long)blockIdx.x * 64 + (threadIdx.x & 63);
+  if (row >= m) return;
+  float acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+  for (int i0 = 0; i0 < h; i0 += 8) {
+    float qb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) qb[u] = (i0 + u < h) ? __ldg(Q1 + row + (long long)(i0 + u) * ldq) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (i0 + u < h) {
+        const float2 qu = make_float2(qb[u], qb[u]);
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 tv = *reinterpret_cast<const float4*>(&Ts[i0 + u][32 * g + j]);
+          const float2 c01 = ffma2(qu, make_float2(tv.x, tv.y), make_float2(acc[j], acc[j + 1]));
+          const float2 c23 = ffma2(qu, make_float2(tv.z, tv.w), make_float2(acc[j + 2], acc[j + 3]));
+          acc[j] = c01.x;
+          acc[j + 1] = c01.y;
+          acc[j + 2] = c23.x;
+          acc[j + 3] = c23.y;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int jj = 32 * g + j;
+    if (jj < w2) A2[row + (long long)jj * lda] -= acc[j];
+  }
+}
+
 cudaError_t f32_nn_update(int m, int h, int w2, const float* Q1, long long ldq, const float* T,
                           float* A2, long long lda, cudaStream_t st) {
   if (h > 64 || w2 > 64) return cudaErrorInvalidValue;
-  const int grid = (m + 127) / 128;
   if (w2 <= 32)
-    f32_nn_kernel<32><<<grid, 128, 0, st>>>(m, h, w2, Q1, ldq, T, A2, lda);
+    f32_nn_kernel<32><<<(m + 127) / 128, 128, 0, st>>>(m, h, w2, Q1, ldq, T, A2, lda);
   else
-    f32_nn_kernel<64><<<grid, 128, 0, st>>>(m, h, w2, Q1, ldq, T, A2, lda);
+    f32_nn2_kernel<<<(m + 63) / 64, 128, 0, st>>>(m, h, w2, Q1, ldq, T, A2, lda);
   return cudaGetLastError();
 }
 
@@ -293,9 +355,16 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
           av[v4] = a4.x; av[v4 + 1] = a4.y; av[v4 + 2] = a4.z; av[v4 + 3] = a4.w;
         }
 #pragma unroll
-        for (int a = 0; a < MT; ++a)
+        for (int a = 0; a < MT; ++a) {  // FFMA2: the same fmaf sequence per entry
+          const float2 qa = make_float2(qv[a], qv[a]);
 #pragma unroll
-          for (int c = 0; c < MT; ++c) acc[a][c] = fmaf(qv[a], av[c], acc[a][c]);
+          for (int c = 0; c < MT; c += 2) {
+            const float2 r = ffma2(qa, make_float2(av[c], av[c + 1]),
+                                   make_float2(acc[a][c], acc[a][c + 1]));
+            acc[a][c] = r.x;
+            acc[a][c + 1] = r.y;
+          }
+        }
       }
     }
     __syncthreads();
@@ -363,13 +432,17 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
 #pragma unroll
         for (int i = 0; i < TD; ++i) {
           if (i < h) {
+            const float2 qi = make_float2(qrow[i], qrow[i]);
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
+            for (int j = 0; j < 32; j += 4) {  // FFMA2: the same fmaf sequence per entry
               const float4 tv = *reinterpret_cast<const float4*>(&Ts[i * TD + jh + j]);
-              acc[j] = fmaf(qrow[i], tv.x, acc[j]);
-              acc[j + 1] = fmaf(qrow[i], tv.y, acc[j + 1]);
-              acc[j + 2] = fmaf(qrow[i], tv.z, acc[j + 2]);
-              acc[j + 3] = fmaf(qrow[i], tv.w, acc[j + 3]);
+              const float2 c01 = ffma2(qi, make_float2(tv.x, tv.y), make_float2(acc[j], acc[j + 1]));
+              const float2 c23 = ffma2(qi, make_float2(tv.z, tv.w),
+                                       make_float2(acc[j + 2], acc[j + 3]));
+              acc[j] = c01.x;
+              acc[j + 1] = c01.y;
+              acc[j + 2] = c23.x;
+              acc[j + 3] = c23.y;
             }
           }
         }

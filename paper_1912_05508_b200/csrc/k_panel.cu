@@ -29,31 +29,36 @@ int panel_num_blocks(int rows, int br, int w) {
 
 // (panel_mgs_kernel is defined below, after the rotating MGS step it shares.)
 
-// X_b <- X_b * T_b with T_b = S[b*w:(b+1)*w, 0:w] (lds).  grid.x = row chunks of 256 rows.
-__global__ void __launch_bounds__(256) panel_apply_kernel(int rows, int w, float* __restrict__ X,
-                                                          long long ldx, int br, int nb,
-                                                          const float* __restrict__ S,
-                                                          long long lds) {
-  __shared__ __align__(16) float T[32][36];  // 16-byte rows: one LDS.128 per four FMAs
-  const int i = blockIdx.x * 256 + threadIdx.x;
-  // block index of the first row of this CTA (CTAs never straddle: chunks are 256 rows and br is
-  // a multiple of 32 but not necessarily of 256 -> compute per row below, T loaded per block).
-  const int row_first = blockIdx.x * 256;
+// X_b <- X_b * T_b with T_b = S[b*w:(b+1)*w, 0:w] (lds): Eq. (6) step 4.  A CTA takes 128 rows
+// with two threads per row, each forming 16 of the (up to 32) output columns by FFMA2 (the same
+// fmaf sequence per entry: l in increasing order); the row's 32 inputs are read by both threads
+// (the second read hits L1).  Register-lean (three CTAs per SM) so that enough loads are in
+// flight to stream the panel at HBM rate -- the one-thread-per-row version held 64 values per
+// thread (167 registers, one CTA per SM) and ran at 1.1 TB/s.  T_b staged in shared memory per
+// block the CTA's rows touch (br is a multiple of 32, CTAs may straddle two blocks).
+__global__ void __launch_bounds__(256, 3) panel_apply_kernel(int rows, int w, float* __restrict__ X,
+                                                             long long ldx, int br, int nb,
+                                                             const float* __restrict__ S,
+                                                             long long lds) {
+  __shared__ __align__(16) float T[32][36];
+  const int half = threadIdx.x >> 7;
+  const int i = blockIdx.x * 128 + (threadIdx.x & 127);
+  const int row_first = blockIdx.x * 128;
   int b_first = row_first / br;
   if (b_first > nb - 1) b_first = nb - 1;
-  int row_last = row_first + 255;
+  int row_last = row_first + 127;
   if (row_last > rows - 1) row_last = rows - 1;
   int b_last = row_last / br;
   if (b_last > nb - 1) b_last = nb - 1;
-  float x[32];
   const bool ok = i < rows;
   int bi = ok ? i / br : 0;
   if (bi > nb - 1) bi = nb - 1;
+  float x[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) x[j] = (ok && j < w) ? X[(long long)i + (long long)j * ldx] : 0.f;
-  float y[32];
+  float2 y[8];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) y[j] = 0.f;
+  for (int j = 0; j < 8; ++j) y[j] = make_float2(0.f, 0.f);
   for (int b = b_first; b <= b_last; ++b) {
     __syncthreads();
     for (int e = threadIdx.x; e < 32 * 32; e += 256) {
@@ -64,31 +69,30 @@ __global__ void __launch_bounds__(256) panel_apply_kernel(int rows, int w, float
     if (ok && bi == b) {
 #pragma unroll
       for (int l = 0; l < 32; ++l) {
-        if (l < w) {
-          const float xl = x[l];
-          const float4* t4 = reinterpret_cast<const float4*>(&T[l][0]);
+        const float2 xl = make_float2(x[l], x[l]);
+        const float4* t4 = reinterpret_cast<const float4*>(&T[l][16 * half]);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 t = t4[q];
-            y[4 * q] = fmaf(xl, t.x, y[4 * q]);
-            y[4 * q + 1] = fmaf(xl, t.y, y[4 * q + 1]);
-            y[4 * q + 2] = fmaf(xl, t.z, y[4 * q + 2]);
-            y[4 * q + 3] = fmaf(xl, t.w, y[4 * q + 3]);
-          }
+        for (int q = 0; q < 4; ++q) {
+          const float4 t = t4[q];
+          y[2 * q] = ffma2(xl, make_float2(t.x, t.y), y[2 * q]);
+          y[2 * q + 1] = ffma2(xl, make_float2(t.z, t.w), y[2 * q + 1]);
         }
       }
     }
   }
   if (ok) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < w) X[(long long)i + (long long)j * ldx] = y[j];
+    for (int j2 = 0; j2 < 8; ++j2) {
+      const int j = 16 * half + 2 * j2;
+      if (j < w) X[(long long)i + (long long)j * ldx] = y[j2].x;
+      if (j + 1 < w) X[(long long)i + (long long)(j + 1) * ldx] = y[j2].y;
+    }
   }
 }
 
 cudaError_t panel_apply(int rows, int w, float* X, long long ldx, int br, int nb, const float* S,
                         long long lds, cudaStream_t st) {
-  const int grid = (rows + 255) / 256;
+  const int grid = (rows + 127) / 128;
   panel_apply_kernel<<<grid, 256, 0, st>>>(rows, w, X, ldx, br, nb, S, lds);
   return cudaGetLastError();
 }
