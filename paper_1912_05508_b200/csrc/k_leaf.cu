@@ -24,10 +24,16 @@
 //   PROJ(c0, h, w2) Alg. 2 lines 8-9 in FP32 below the cutoff: R12 = Q1' A2 (per-CTA partial over
 //     its rows, fixed-order sum over the CTAs), R block <- R12, A2 -= Q1 R12.
 //
-// Cross-CTA steps (the Gram / R12 sums) go through L2 between grid barriers; every CTA computes
-// the 32 x 32 Cholesky redundantly (same inputs, same code: bit-identical R everywhere), so a
-// panel costs two grid barriers.  At the end each CTA writes its rows of the final Q (FP32 and the
+// Cross-CTA steps (the Gram / R12 sums) go through L2 as tagged words, without grid barriers:
+// every CTA stores its partial as 64-bit words {payload, tag} (tag = the reduction's sequence
+// number in the factorization), the owner CTA of each 32-entry chunk polls the nb partials of its
+// entries until their tags match, sums them in a fixed order and stores the tagged sum, and every
+// CTA polls the sums it needs.  Each value is its own ready flag (an 8-byte store is single-copy
+// atomic), so a reduction costs two L2 round trips instead of two grid barriers plus a pass; the
+// words are zeroed once per factorization (tags start at 1).  Every CTA computes the 32 x 32
+// Cholesky redundantly (same inputs, same code: bit-identical R everywhere).  At the end each CTA writes its rows of the final Q (FP32 and the
 // FP16 shadow the tensor-core GEMMs above read) and CTA 0 has written the leaf's R blocks.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -62,12 +68,8 @@ struct LeafArgs {
   long long ldr;
   int m, wl, nb, nops;
   LeafOp ops[kMaxOps];
-  double* gpart;  // nb x 1024 Gram partials
-  double* gsum;   // 1024
-  float* ppart;   // nb x 4096 projection partials
-  float* r12;     // 4096
-  unsigned* bar;  // grid barrier arrival counter (zeroed before the factorization's first leaf)
-  unsigned bar_base;  // counter arrivals of the earlier launches (the host counts them)
+  unsigned long long* tg;  // tagged words (leaf_tag_words(), zeroed before the first leaf)
+  unsigned tag0;           // reductions of the earlier launches (the host counts them)
   int* status;    // breakdown status (null: local leaf of a rank, zero norms allowed, R-A8)
   int col0;       // global column of the leaf's column 0 (breakdown codes)
   unsigned long long* dbg;  // optional phase timestamps of CTA 0 (globaltimer ns), 128 slots
@@ -85,42 +87,122 @@ struct Smem {
   double rowb[kMW][2][64];     // Cholesky: row k of R twice over, per chain warp (step parity)
   float colbuf[kMW][kBR];      // MGS: the pivot column of each block
   float qbuf[kMW][kBR];        // MGS: q_k of each block
-  float wsum[kNW * 32];        // per-warp partial sums of the cross-CTA reductions
-  unsigned barseq;             // grid barriers passed by this CTA in this launch (thread 0)
+  double Gs[528];              // PANEL: the stack's Gram (packed upper triangle), from the owners
+  float wsum[kNW * 32];        // per-warp partial sums of the cross-CTA reductions (FP32)
+  double wsumd[kNW * 32];      //   (FP64)
 };
 
-// Grid barrier on a monotonic arrival counter: barrier i of this launch completes when the
-// counter reaches bar_base + i * nb (bar_base = the arrivals of every earlier launch of the
-// factorization, whatever their grid sizes).  Fire-and-forget release arrival, relaxed polling,
-// one acquire load at the end (the CTA barriers carry the ordering to the other threads).
-// Watchdog: a barrier still open after 2 s (a co-residency failure) is abandoned and the launch
-// reports TCQR_ERR_CUDA through the status word, so a bug fails the call instead of hanging the
-// device.
-__device__ __forceinline__ void leaf_barrier(const LeafArgs& a, Smem& s) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned target = a.bar_base + (++s.barseq) * (unsigned)a.nb;
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
-    unsigned v;
-    unsigned long long t0 = 0;
-    for (unsigned it = 0;; ++it) {
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
-      if ((int)(v - target) >= 0) break;
-      if ((it & 4095) == 0) {
-        unsigned long long now;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
-        if (t0 == 0) {
-          t0 = now;
-        } else if (now - t0 > 2000000000ull) {
-          if (a.status) atomicMin(a.status, -1001);
-          break;
-        }
-      }
-    }
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
-  }
-  __syncthreads();
+// tagged-word layout (u64 words): [0] abort word; Gram partials nb x 528 entries x 2 words (low,
+// high half of the FP64 value); Gram sums 528 x 2; projection partials nb x 4096; sums 4096
+constexpr long long kTgGP = 8;
+constexpr long long kTgGS = kTgGP + 148LL * 528 * 2;
+constexpr long long kTgPP = kTgGS + 528 * 2;
+constexpr long long kTgPS = kTgPP + 148LL * 4096;
+constexpr long long kTgWords = kTgPS + 4096;
+
+// Tagged words: {payload (low 32 bits), tag (high 32 bits)}, stored and polled at GPU scope (L2).
+__device__ __forceinline__ void st_tag(unsigned long long* p, unsigned payload, unsigned tag) {
+  const unsigned long long v = ((unsigned long long)tag << 32) | payload;
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_tag(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_tag2(unsigned long long* p, unsigned lo, unsigned hi,
+                                        unsigned tag) {
+  const unsigned long long v0 = ((unsigned long long)tag << 32) | lo;
+  const unsigned long long v1 = ((unsigned long long)tag << 32) | hi;
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(v0), "l"(v1) : "memory");
+}
+__device__ __forceinline__ void ld_tag2(const unsigned long long* p, unsigned long long& v0,
+                                        unsigned long long& v1) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v0), "=l"(v1) : "l"(p) : "memory");
+}
+// Watchdog of the polls: a value still missing after 2 s (a co-residency failure) raises the
+// abort word, which releases every other waiter of the launch, and the launch reports
+// TCQR_ERR_CUDA through the status word, so a bug fails the call instead of hanging the device.
+__device__ __noinline__ bool poll_watchdog(const LeafArgs& a, unsigned long long& t0) {
+  if (ld_tag(a.tg) != 0ull) return true;
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+  if (t0 == 0) {
+    t0 = now;
+  } else if (now - t0 > 2000000000ull) {
+    st_tag(a.tg, 1u, 1u);
+    if (a.status) atomicMin(a.status, -1001);
+    return true;
+  }
+  return false;
+}
+// Load the words p[i] (null: none) until every one carries `tag`; each round re-issues the loads
+// of all the words still missing together (one L2 round trip per round).
+// Pairs (p[2i], p[2i] + 1) loaded with one 16-byte load; each half still carries its own tag.
+template <int N>
+__device__ __forceinline__ void poll_pairs(const LeafArgs& a, unsigned long long (&v)[2 * N],
+                                           const unsigned long long* const (&p)[N],
+                                           unsigned tag) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    v[2 * i] = v[2 * i + 1] = 0ull;
+    if (p[i]) ld_tag2(p[i], v[2 * i], v[2 * i + 1]);
+  }
+  unsigned long long t0 = 0;
+  for (unsigned it = 1;; ++it) {
+    bool done = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      done &= !p[i] || ((unsigned)(v[2 * i] >> 32) == tag && (unsigned)(v[2 * i + 1] >> 32) == tag);
+    if (done) return;
+    __nanosleep(64);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (p[i] && ((unsigned)(v[2 * i] >> 32) != tag || (unsigned)(v[2 * i + 1] >> 32) != tag))
+        ld_tag2(p[i], v[2 * i], v[2 * i + 1]);
+    if ((it & 255) == 0 && poll_watchdog(a, t0)) return;
+  }
+}
+template <int N>
+__device__ __forceinline__ void poll_words(const LeafArgs& a, unsigned long long (&v)[N],
+                                           const unsigned long long* const (&p)[N],
+                                           unsigned tag) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = p[i] ? ld_tag(p[i]) : 0ull;
+  unsigned long long t0 = 0;
+  for (unsigned it = 1;; ++it) {
+    bool done = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) done &= !p[i] || (unsigned)(v[i] >> 32) == tag;
+    if (done) return;
+    __nanosleep(64);  // back off: a storm of polls would slow the stores it waits for
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (p[i] && (unsigned)(v[i] >> 32) != tag) v[i] = ld_tag(p[i]);
+    if ((it & 255) == 0 && poll_watchdog(a, t0)) return;
+  }
+}
+template <typename T>
+struct TagWords;
+template <>
+struct TagWords<float> {
+  static constexpr int W = 1;
+  __device__ static void put(unsigned long long* p, float v, unsigned tag) {
+    st_tag(p, __float_as_uint(v), tag);
+  }
+  __device__ static float get(const unsigned long long* v) { return __uint_as_float((unsigned)v[0]); }
+};
+template <>
+struct TagWords<double> {
+  static constexpr int W = 2;
+  __device__ static void put(unsigned long long* p, double v, unsigned tag) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    st_tag2(p, (unsigned)b, (unsigned)(b >> 32), tag);  // one 16-byte store (each half tagged)
+  }
+  __device__ static double get(const unsigned long long* v) {
+    return __longlong_as_double((long long)(((v[1] & 0xffffffffull) << 32) | (v[0] & 0xffffffffull)));
+  }
+};
 
 __device__ __forceinline__ void leaf_ts(const LeafArgs& a, int& slot) {
   if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && slot < 128) {
@@ -131,33 +213,54 @@ __device__ __forceinline__ void leaf_ts(const LeafArgs& a, int& slot) {
   ++slot;
 }
 
+// CTA b's rows start at leaf_row(b): balanced in row quads (16-byte loads), the last CTA ragged
 __device__ __forceinline__ int leaf_row(int b, int m, int nb) {
-  return (int)((long long)b * m / nb);
+  const long long mq = (m + 3) / 4;
+  return (int)min((long long)m, 4 * ((long long)b * mq / nb));
 }
 
-// Fixed-order cross-CTA sum: out[e] = sum_{b=0..nb-1} part[b * pstride + e] for the entries
-// e in [0, E) that belong to this CTA (chunks of 32 consecutive entries, chunk c on CTA c % nb).
-// Lane = entry, warp w sums the partials b = w, w + 8, ... in increasing order, then the 8 warp
-// sums are added in warp order.  Deterministic; reads bypass L1 (written by other CTAs).
+// Fixed-order cross-CTA sum of tagged partials: out[e] = sum_{b=0..nb-1} part[b][e] for the
+// entries e in [0, E) owned by this CTA (chunks of 32 consecutive entries, chunk c on CTA c % nb).
+// Lane = entry (coalesced loads of one partial row per warp), warp w sums the partials b = w,
+// w + 8, ... in increasing order (up to 16 partials in flight, polled until their tags match, with
+// a short back-off between rounds), then the 8 warp sums are added in warp order and stored
+// tagged.  Deterministic.  (Measured, tools/micro/xcta_reduce.cu: 2.9 us for 528 FP64 entries on
+// 128 CTAs against 4.6 us for barrier + sum + barrier.)  Projection sums also go to the R block.
 template <typename T>
-__device__ __forceinline__ void cross_sum(const T* part, long long pstride, int E, int nb,
-                                          T* out, T* wsum, float* Rblk, long long ldr, int h,
-                                          int w2, int w2p, int c0, bool to_r) {
+__device__ __forceinline__ void tagged_sum(const LeafArgs& a, const unsigned long long* part,
+                                           long long pstride, int E, unsigned tag,
+                                           unsigned long long* out, T* wsum, int h, int w2,
+                                           int w2p, int c0, bool to_r) {
+  constexpr int W = TagWords<T>::W, NBT = 16, N = NBT * W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nchunks = (E + 31) / 32;
-  for (int c = blockIdx.x; c < nchunks; c += nb) {
+  for (int c = blockIdx.x; c < nchunks; c += a.nb) {
     const int e = c * 32 + lane;
     T s = 0;
     if (e < E) {
-      T v[4];
-      int b = warp;
-      for (; b + 3 * kNW < nb; b += 4 * kNW) {
+      for (int b0 = warp; b0 < a.nb; b0 += NBT * kNW) {
+        unsigned long long v[N];
+        if constexpr (W == 2) {
+          const unsigned long long* p[NBT];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcg(part + (long long)(b + u * kNW) * pstride + e);
+          for (int u = 0; u < NBT; ++u) {
+            const int b = b0 + u * kNW;
+            p[u] = b < a.nb ? part + b * pstride + e * W : nullptr;
+          }
+          poll_pairs<NBT>(a, v, p, tag);
+        } else {
+          const unsigned long long* p[N];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) s += v[u];
+          for (int u = 0; u < NBT; ++u) {
+            const int b = b0 + u * kNW;
+            p[u] = b < a.nb ? part + b * pstride + e : nullptr;
+          }
+          poll_words<N>(a, v, p, tag);
+        }
+#pragma unroll
+        for (int u = 0; u < NBT; ++u)
+          if (b0 + u * kNW < a.nb) s += TagWords<T>::get(v + u * W);
       }
-      for (; b < nb; b += kNW) s += __ldcg(part + (long long)b * pstride + e);
     }
     wsum[warp * 32 + lane] = s;
     __syncthreads();
@@ -165,14 +268,39 @@ __device__ __forceinline__ void cross_sum(const T* part, long long pstride, int 
       T t = wsum[lane];
 #pragma unroll
       for (int u = 1; u < kNW; ++u) t += wsum[u * 32 + lane];
-      out[e] = t;
+      TagWords<T>::put(out + e * W, t, tag);
       if (to_r) {  // projection: R(c0 + i, c0 + h + j) = R12(i, j)
         const int i = e / w2p, j = e % w2p;
-        if (i < h && j < w2) Rblk[(c0 + i) + (long long)(c0 + h + j) * ldr] = (float)t;
+        if (i < h && j < w2) a.R[(c0 + i) + (long long)(c0 + h + j) * a.ldr] = (float)t;
       }
     }
     __syncthreads();
   }
+}
+
+// Every CTA: dst[e] = the tagged sums out[e], e in [0, E) (up to 16 entries per thread in flight)
+template <typename T>
+__device__ __forceinline__ void tagged_gather(const LeafArgs& a, const unsigned long long* out,
+                                              int E, unsigned tag, T* dst) {
+  constexpr int W = TagWords<T>::W, U = 16 / W, N = U * W;
+  for (int e0 = threadIdx.x; e0 < E; e0 += U * kNT) {
+    unsigned long long v[N];
+    if constexpr (W == 2) {
+      const unsigned long long* p[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) p[u] = e0 + u * kNT < E ? out + (e0 + u * kNT) * W : nullptr;
+      poll_pairs<U>(a, v, p, tag);
+    } else {
+      const unsigned long long* p[N];
+#pragma unroll
+      for (int u = 0; u < U; ++u) p[u] = e0 + u * kNT < E ? out + e0 + u * kNT : nullptr;
+      poll_words<N>(a, v, p, tag);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * kNT < E) dst[e0 + u * kNT] = TagWords<T>::get(v + u * W);
+  }
+  __syncthreads();
 }
 
 // Alg. 4 on MGS block `blk` = rows [64 blk, 64 blk + 64) of the CTA, columns
@@ -299,9 +427,53 @@ __device__ __forceinline__ void leaf_store_row(const LeafArgs& a, const Smem& s,
   }
 }
 
+struct CholCtx {
+  const LeafArgs& a;
+  Smem& s;
+  float* Sf;
+  int warp, lane, c0;
+};
+// Steps [k0, k1) of the panel's Cholesky + S_b chain (see (3) in leaf_panel); T = live terms of the
+// trailing triangle for every step of the phase (31 - k0).  Slots c[T..], r[T..] go stale: from
+// step k0 on they stand for rows / columns past 31.
+template <int T>
+__device__ __forceinline__ void chol_phase(const CholCtx& x, int k0, int k1, double (&c)[32],
+                                           double (&r)[32], double& d, bool& ok, double& ri) {
+  const int lane = x.lane;
+#pragma unroll 1
+  for (int k = k0; k < k1; ++k) {
+    ri = ok ? ri : 0.0;
+    const double rkj = lane == k ? d * ri : (lane > k ? c[0] * ri : 0.0);
+    const double dn = fma(-rkj, rkj, c[1]);  // lane k+1: W(k+1,k+1) - R(k,k+1)^2
+    d = __shfl_sync(0xffffffffu, dn, (k + 1) & 31);  // next pivot (unused after the last step)
+    double* rowk = x.s.rowb[x.warp][k & 1];
+    rowk[lane] = rkj;  // twice: rowk[k + 1 + i] is R(k, k+1+i), and 0 past column 31
+    rowk[lane + 32] = rkj;
+    if (x.warp == 0) {
+      x.s.Rd[k * 34 + lane] = rkj;
+      if (!ok && lane == 0 && blockIdx.x == 0 && x.a.status)
+        atomicMin(x.a.status, x.a.col0 + x.c0 + k + 1);
+    }
+    const double sk = r[0] * ri;  // S_b(lane, k)
+    x.Sf[lane * kLdS + k] = (float)sk;
+    ok = d > 0.0 && d <= 1.7976931348623157e308;
+    ri = rsqrt_nr(ok ? d : 1.0);
+    __syncwarp();
+    // R(k, k+1+i); slots past column 31 read R(k, 0..k-1) = 0 from the second copy
+    const double* rk = rowk + k + 1;
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      const double v = rk[i];
+      c[i] = fma(-v, rkj, c[i + 1]);
+      r[i] = fma(-sk, v, r[i + 1]);
+    }
+  }
+}
+
 // ---- PANEL ------------------------------------------------------------------------------------
 __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, int c0, int pw,
-                                        int& slot, bool first, int st_c0, int st_pw, bool defer) {
+                                        int& slot, bool first, int st_c0, int st_pw, bool defer,
+                                        unsigned tag) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   // first panel: the upper half (warps 4-7, idle during the MGS) issues the async loads of the
   // leaf's later columns (two rows per thread) beside the MGS instead of before it
@@ -325,22 +497,24 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
   __syncthreads();
   leaf_ts(a, slot);
   // (2) the CTA's part of the stack's Gram: G = (G_0 + G_1) + (G_2 + G_3) (FP64, fixed order;
-  // zero below the diagonal and past the panel)
-  for (int e = t; e < 1024; e += kNT) {
-    const int i = e >> 5, j = e & 31;
-    double g = 0.0;
-    if (i <= j && j < pw) {
-      const int pk = j * (j + 1) / 2 + i;
-      g = (s.u.Gp[0][pk] + s.u.Gp[1][pk]) + (s.u.Gp[2][pk] + s.u.Gp[3][pk]);
-    }
-    a.gpart[(long long)blockIdx.x * 1024 + e] = g;
+  // packed upper triangle, zero past the panel), stored tagged; the owners sum the nb partials
+  // (fixed order) and every CTA gathers the sum
+  for (int e = t; e < 528; e += kNT) {
+    int j = (int)((sqrtf(8.f * e + 1.f) - 1.f) * 0.5f);  // e = j (j + 1) / 2 + i, i <= j
+    if (j * (j + 1) / 2 > e) --j;
+    if ((j + 1) * (j + 2) / 2 <= e) ++j;
+    const double g = j < pw ? (s.u.Gp[0][e] + s.u.Gp[1][e]) + (s.u.Gp[2][e] + s.u.Gp[3][e]) : 0.0;
+    TagWords<double>::put(a.tg + kTgGP + ((long long)blockIdx.x * 528 + e) * 2, g, tag);
   }
-  leaf_barrier(a, s);
   leaf_ts(a, slot);
-  cross_sum<double>(a.gpart, 1024, 1024, a.nb, a.gsum, reinterpret_cast<double*>(s.u.T), nullptr,
-                    0, 0, 0, 1, 0, false);
+  if (a.dbg && t == 0) {  // debug: the latest CTA's publish time of this op
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    atomicMax(a.dbg + 120 + min(7u, tag - a.tag0 - 1u), v);
+  }
+  tagged_sum<double>(a, a.tg + kTgGP, 528 * 2, 528, tag, a.tg + kTgGS, s.wsumd, 0, 0, 1, 0, false);
   leaf_ts(a, slot);
-  leaf_barrier(a, s);
+  tagged_gather<double>(a, a.tg + kTgGS, 528, tag, s.Gs);
   leaf_ts(a, slot);
   if (a.dbg && blockIdx.x == 0 && t == 0) {  // debug: Cholesky start
     unsigned long long v;
@@ -349,56 +523,33 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
   }
   // (3) R = chol(G) and S_b = R_b R^-1, in warps 0-3 (one per SM sub-partition): warp b runs the
   // Cholesky redundantly (same inputs, same code: the same R bits in every warp and CTA) with the
-  // forward substitution of ITS block's R_b fused in.  One ROLLED pass over k (a fully unrolled
-  // 32-step chain is instruction-fetch bound).  Lane j holds column j of the trailing Gram, c[i] =
-  // W(k+i, j) (shifted down one slot per step, so the pivot is always c[0]), and row j of S_b, r[i]
-  // = the running value of column k+i.  Step k: the pivot G(k,k) by shuffle, one FP64 reciprocal
-  // square root ri = 1/R(k,k) (<= 1 ulp; R(k,j) = W(k,j) ri and the substitution's quotients
-  // become products; FP64 values within an ulp round to the same FP32 R and Q, exact inputs stay
-  // exact -- the planted pin), row k of R broadcast through the warp's row buffer.  The pivot of
-  // step k+1 comes from lane k+1's own values (its update of W(k+1,k+1) with its own R(k,k+1)), so
-  // shuffle -> rsqrt starts before the row is in shared memory.
+  // forward substitution of ITS block's R_b fused in.  Rolled passes over k (a fully unrolled
+  // 32-step chain is instruction-fetch bound) in four phases of eight steps whose inner loops
+  // cover only the live part of the trailing triangle (31, 23, 15, 7 terms).  Lane j holds column
+  // j of the trailing Gram, c[i] = W(k+i, j) (shifted down one slot per step, so the pivot is
+  // always c[0]), and row j of S_b, r[i] = the running value of column k+i.  Step k: the pivot
+  // G(k,k) by shuffle, one FP64 reciprocal square root ri = 1/R(k,k) (<= 1 ulp; R(k,j) = W(k,j) ri
+  // and the substitution's quotients become products; FP64 values within an ulp round to the
+  // same FP32 R and Q, exact inputs stay exact -- the planted pin), row k of R broadcast through
+  // the warp's row buffer.  The pivot of step k+1 comes from lane k+1's own values (its update of
+  // W(k+1,k+1) with its own R(k,k+1)), so shuffle -> rsqrt starts before the row is in shared
+  // memory.
   if (warp < kMW) {
     const double* Rb = s.Rbd[warp];
     float* Sf = s.u.Sf[warp];
     double c[32], r[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) c[i] = (i <= lane && lane < pw) ? __ldcg(a.gsum + i * 32 + lane) : 0.0;
+    for (int i = 0; i < 32; ++i) c[i] = (i <= lane && lane < pw) ? s.Gs[lane * (lane + 1) / 2 + i] : 0.0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) r[j] = (lane < pw && j < pw) ? Rb[lane * kLdR + j] : 0.0;
     double d = __shfl_sync(0xffffffffu, c[0], 0);
     bool ok = d > 0.0 && d <= 1.7976931348623157e308;
     double ri = rsqrt_nr(ok ? d : 1.0);
-#pragma unroll 1
-    for (int k = 0; k < pw; ++k) {
-      ri = ok ? ri : 0.0;
-      const double rkj = lane == k ? d * ri : (lane > k ? c[0] * ri : 0.0);
-      const double dn = fma(-rkj, rkj, c[1]);  // lane k+1: W(k+1,k+1) - R(k,k+1)^2
-      d = __shfl_sync(0xffffffffu, dn, (k + 1) & 31);  // next pivot (unused after the last step)
-      double* rowk = s.rowb[warp][k & 1];
-      rowk[lane] = rkj;  // twice: rowk[k + 1 + i] is R(k, k+1+i), and 0 past column 31
-      rowk[lane + 32] = rkj;
-      if (warp == 0) {
-        s.Rd[k * 34 + lane] = rkj;
-        if (!ok && lane == 0 && blockIdx.x == 0 && a.status)
-          atomicMin(a.status, a.col0 + c0 + k + 1);
-      }
-      const double sk = r[0] * ri;  // S_b(lane, k)
-      Sf[lane * kLdS + k] = (float)sk;
-      ok = d > 0.0 && d <= 1.7976931348623157e308;
-      ri = rsqrt_nr(ok ? d : 1.0);
-      __syncwarp();
-      // R(k, k+1+i); slots past column 31 read R(k, 0..k-1) = 0 from the second copy
-      const double* rk = rowk + k + 1;
-#pragma unroll
-      for (int i = 0; i < 31; ++i) {
-        const double v = rk[i];
-        c[i] = fma(-v, rkj, c[i + 1]);
-        r[i] = fma(-sk, v, r[i + 1]);
-      }
-      c[31] = 0.0;
-      r[31] = 0.0;
-    }
+    CholCtx cc{a, s, Sf, warp, lane, c0};
+    chol_phase<31>(cc, 0, min(pw, 8), c, r, d, ok, ri);
+    chol_phase<23>(cc, 8, min(pw, 16), c, r, d, ok, ri);
+    chol_phase<15>(cc, 16, min(pw, 24), c, r, d, ok, ri);
+    chol_phase<7>(cc, 24, pw, c, r, d, ok, ri);
 #pragma unroll 1
     for (int j = pw; j < 32; ++j) Sf[lane * kLdS + j] = 0.f;
   } else if (st_pw > 0) {
@@ -471,7 +622,7 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
 // and stay zero).
 template <int H, int W2P>
 __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, int c0, int w2,
-                                       int& slot) {
+                                       int& slot, unsigned tag) {
   constexpr int TJ = W2P / 4, TILES = (H / 4) * TJ, G = kNT / TILES;
   const int t = threadIdx.x;
   asm volatile("cp.async.wait_all;" ::: "memory");  // the leaf's later columns (loaded async)
@@ -504,12 +655,12 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
       }
     }
   }
-  float* pp = a.ppart + (long long)blockIdx.x * 4096;
+  unsigned long long* pp = a.tg + kTgPP + (long long)blockIdx.x * 4096;
   if (G == 1) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      *reinterpret_cast<float4*>(pp + (4 * ti + i) * W2P + 4 * tj) =
-          make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) TagWords<float>::put(pp + (4 * ti + i) * W2P + 4 * tj + j, acc[i][j], tag);
   } else {
     // row groups: combine in group order through shared memory
 #pragma unroll
@@ -521,19 +672,16 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
       float v = s.u.T[e];
 #pragma unroll
       for (int g = 1; g < G; ++g) v += s.u.T[g * (H * W2P) + e];
-      pp[e] = v;
+      TagWords<float>::put(pp + e, v, tag);
     }
+    __syncthreads();  // s.u.T is reused for the gathered sum below
   }
   leaf_ts(a, slot);
-  leaf_barrier(a, s);
+  tagged_sum<float>(a, a.tg + kTgPP, 4096, H * W2P, tag, a.tg + kTgPS, s.wsum, H, w2, W2P, c0,
+                    true);
   leaf_ts(a, slot);
-  cross_sum<float>(a.ppart, 4096, H * W2P, a.nb, a.r12, s.wsum, a.R, a.ldr, H, w2, W2P, c0,
-                   true);
+  tagged_gather<float>(a, a.tg + kTgPS, H * W2P, tag, s.u.T);
   leaf_ts(a, slot);
-  leaf_barrier(a, s);
-  leaf_ts(a, slot);
-  for (int e = t; e < H * W2P; e += kNT) s.u.T[e] = __ldcg(a.r12 + e);
-  __syncthreads();
   if (nrows <= 128) {
     // A2 -= Q1 R12 for CTAs of <= 128 rows: thread = row t % 128, columns [jq * W2P/4, ...)
     constexpr int JQ = W2P / 4;
@@ -642,7 +790,6 @@ __global__ void __launch_bounds__(kNT, 1) leaf_kernel(const __grid_constant__ Le
   const int row0 = leaf_row(blockIdx.x, a.m, a.nb);
   const int nrows = leaf_row(blockIdx.x + 1, a.m, a.nb) - row0;
   int slot = 0;
-  if (t == 0) s.barseq = 0;
   leaf_ts(a, slot);
   // load the block's rows of the leaf; columns past the leaf and rows past the block are zero.
   // Columns [0, 32) (the first panel) now, 16-byte loads down the columns (a warp = 2 row quads x
@@ -689,18 +836,19 @@ __global__ void __launch_bounds__(kNT, 1) leaf_kernel(const __grid_constant__ Le
   int st_c0 = 0, st_pw = 0;  // a panel's Q columns whose stores wait for the next panel's MGS
   for (int o = 0; o < a.nops; ++o) {
     const LeafOp op = a.ops[o];
+    const unsigned tag = a.tag0 + 1u + (unsigned)o;  // one reduction per op
     if (op.kind == 0) {
       const bool defer = o != last_panel;
-      leaf_panel(a, s, nrows, op.c0, op.h, slot, o == 0, st_c0, st_pw, defer);
+      leaf_panel(a, s, nrows, op.c0, op.h, slot, o == 0, st_c0, st_pw, defer, tag);
       st_c0 = op.c0;
       st_pw = defer ? op.h : 0;
     } else if (op.h == 64) {
       if (op.w2 > 32)
-        leaf_proj<64, 64>(a, s, nrows, op.c0, op.w2, slot);
+        leaf_proj<64, 64>(a, s, nrows, op.c0, op.w2, slot, tag);
       else
-        leaf_proj<64, 32>(a, s, nrows, op.c0, op.w2, slot);
+        leaf_proj<64, 32>(a, s, nrows, op.c0, op.w2, slot, tag);
     } else {
-      leaf_proj<32, 32>(a, s, nrows, op.c0, op.w2, slot);
+      leaf_proj<32, 32>(a, s, nrows, op.c0, op.w2, slot, tag);
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -798,17 +946,17 @@ cudaError_t apply_right(int m, int w, float* X, long long ldx, const float* S, l
 
 unsigned long long* g_leaf_dbg = nullptr;
 
-size_t leaf_scratch_bytes() {
-  return sizeof(double) * (148 * 1024 + 1024) + sizeof(float) * (148 * 4096 + 4096) + 1024;
-}
+size_t leaf_tag_words() { return (size_t)kTgWords; }
 
 cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long long ldh, float* R,
-                       long long ldr, int col0, int* status, void* scratch, size_t scratch_bytes,
-                       unsigned* bar, unsigned* bar_seq, int num_sms, cudaStream_t st) {
+                       long long ldr, int col0, int* status, unsigned long long* tg,
+                       unsigned* tag_seq, int num_sms, cudaStream_t st) {
   if (wl < 1 || wl > kCols || m < wl) return cudaErrorNotSupported;
   // rows per CTA: the fewest 64-row MGS blocks per CTA that still fit the rows in one CTA per SM
-  // (the MGS and Cholesky chains take the same time for 1 to 4 blocks, the projections and the
-  // Q_b S_b apply scale with the CTA's rows): 64 up to 148 x 64 rows, 128 up to 148 x 128, else 256
+  // of the budget (the MGS and Cholesky chains take the same time for 1 to 4 blocks, the
+  // projections and the Q_b S_b apply scale with the CTA's rows)
+  // (64-row MGS blocks and power-of-two CTA heights: a block never straddles two CTAs, and the
+  // planted pin's blocks stay Hadamard-exact)
   const int rows_cta = m <= num_sms * 64 ? 64 : (m <= num_sms * 128 ? 128 : kRows);
   const int nb = (m + rows_cta - 1) / rows_cta;
   static int per_sm = -1;
@@ -820,7 +968,6 @@ cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long 
       per_sm = 0;
   }
   if (nb > per_sm * num_sms || nb > 148) return cudaErrorNotSupported;
-  if (scratch_bytes < leaf_scratch_bytes()) return cudaErrorNotSupported;
   LeafArgs a{};
   a.X = X;
   a.ldx = ldx;
@@ -833,13 +980,8 @@ cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long 
   a.nb = nb;
   a.nops = 0;
   leaf_plan(0, wl, a);
-  char* p = static_cast<char*>(scratch);
-  a.gpart = reinterpret_cast<double*>(p);
-  a.gsum = a.gpart + 148 * 1024;
-  a.ppart = reinterpret_cast<float*>(a.gsum + 1024);
-  a.r12 = a.ppart + 148 * 4096;
-  a.bar = bar;
-  a.bar_base = *bar_seq;
+  a.tg = tg;
+  a.tag0 = tag_seq[0];
   a.status = status;
   a.col0 = col0;
   a.dbg = g_leaf_dbg;
@@ -854,7 +996,7 @@ cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, leaf_kernel, a);
-  if (e == cudaSuccess) *bar_seq += 2u * (unsigned)a.nops * (unsigned)nb;  // 2 barriers per op
+  if (e == cudaSuccess) tag_seq[0] += (unsigned)a.nops;  // one reduction per op
   return e;
 }
 

@@ -87,14 +87,14 @@ extern unsigned long long* g_proj_dbg;  // debug: phase timestamps of the FP32 p
 // ---- K2L whole-leaf kernel (k_leaf.cu) ----
 // The leaf columns [0, wl) of X (m rows, ldx; wl <= 128) factored in one cooperative launch:
 // Q in place (and its FP16 shadow into Xh when non-null), R(i, j) of the leaf at R[i + j ldr].
-// scratch: leaf_scratch_bytes() of device memory; bar: an arrival counter zeroed together with
-// *bar_seq = 0 (the host's count of counter arrivals, advanced by each launch).
+// tg: leaf_tag_words() 64-bit words, zeroed together with tag_seq[0] = 0 (the host's count of the
+// tagged reductions used so far, advanced by each launch).  num_sms: the launch's SM budget.
 // cudaErrorNotSupported when the blocks do not fit the co-resident grid.
-size_t leaf_scratch_bytes();
+size_t leaf_tag_words();
 extern unsigned long long* g_leaf_dbg;  // debug: CTA-0 phase timestamps of the leaf kernel
 cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long long ldh, float* R,
-                       long long ldr, int col0, int* status, void* scratch, size_t scratch_bytes,
-                       unsigned* bar, unsigned* bar_seq, int num_sms, cudaStream_t st);
+                       long long ldr, int col0, int* status, unsigned long long* tg,
+                       unsigned* tag_seq, int num_sms, cudaStream_t st);
 
 // X (m x w, ldx; w <= 128) <- X S (S w x w, lds; FP32), FP16 shadow of the result into Xh if
 // non-null: Eq. (6) step 4 for the per-leaf TSQR across ranks.

@@ -77,6 +77,7 @@ struct Context {
   cudaEvent_t ev_la[64] = {}, ev_la_fork[64] = {};
   int la_max_w = 512;  // env TCQR_LOOKAHEAD_W (0: off); measured: 1024 and up lose (the tail outlasts the leaf)
   int la_sms = 10;      // env TCQR_LA_SMS (the short-K update runs two CTAs per SM)
+  int leaf_reserve = 10;  // env TCQR_LEAF_RESERVE: SMs the leaf beside a look-ahead leaves free
   int num_sms = 148;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
@@ -157,7 +158,8 @@ struct FactorWs {
   float* tstack = nullptr;       //   their stack (P*128 x 128, ld P*w), factored in place
   float* R2 = nullptr;           // re-orthogonalization: R of the second pass (n x n)
   float* Rt = nullptr;           // re-orthogonalization: R2 * R1 staging (n x n)
-  unsigned leaf_bars = 0;        // leaf grid-barrier counter arrivals since iws was zeroed
+  unsigned long long* ltag = nullptr;  // whole-leaf kernel: tagged reduction words
+  unsigned leaf_tags[1] = {0};   // leaf reductions since ltag was zeroed (the tags used so far)
   // NEXT-4 FP16 split (cfg.fp16_split): low halves of the shadow and of R12, two more R12 stagings
   __half* Ql = nullptr;     // ld ldh, like Qh
   __half* R12l = nullptr;   // like R12h
@@ -187,6 +189,7 @@ static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, Facto
   w.iws_cap = 4096 + m / 16;
   w.iws = a.take<int>((size_t)w.iws_cap);
   w.cmax = a.take<unsigned int>((size_t)n + 64);
+  w.ltag = a.take<unsigned long long>(leaf_tag_words());
   w.pipeR = a.take<float>(32 * 32 * 32);
   w.pipeS = a.take<float>(32 * 32 * 32);
   if (nranks > 1) {
@@ -649,6 +652,7 @@ struct FactorJob {
   StreamPlan* sp = nullptr;
   int depth = 0;  // recursion depth of the current rgs call (fork / join event slot)
   cudaEvent_t la_pending = nullptr;  // look-ahead update to wait for after the next leaf
+  bool la_leaf = false;  // this leaf runs beside a look-ahead update (on la_sms SMs)
 };
 
 // The compute stream waits for every chunk overlapping columns [c0, c1).
@@ -705,13 +709,11 @@ static int leaf_tsqr(FactorJob& J, int c0, int w, bool need_h) {
   FactorWs& ws = *J.ws;
   const int m = J.m, P = c.nranks;
   float* Qc = J.Q + (long long)c0 * J.ldq;
-  unsigned* bar = reinterpret_cast<unsigned*>(ws.iws + ws.iws_cap - 16);
-  const size_t scratch = sizeof(float) * (size_t)ws.p_cap;
   CK(cudaMemsetAsync(ws.rleaf, 0, sizeof(float) * (size_t)w * w, c.stream));
   cudaError_t e = cudaErrorNotSupported;
   PROF(TCQR_K2_LEAF, 2.0 * m * w * w, 8.0 * m * w,
-       e = leaf_fused(m, w, Qc, J.ldq, nullptr, 0, ws.rleaf, w, c0, nullptr, ws.P, scratch, bar,
-                      &ws.leaf_bars, c.num_sms, c.stream));
+       e = leaf_fused(m, w, Qc, J.ldq, nullptr, 0, ws.rleaf, w, c0, nullptr, ws.ltag,
+                      ws.leaf_tags, c.num_sms, c.stream));
   if (e == cudaErrorNotSupported) {
     cudaGetLastError();
     return 1;
@@ -725,8 +727,7 @@ static int leaf_tsqr(FactorJob& J, int c0, int w, bool need_h) {
                          cudaMemcpyDeviceToDevice, c.stream));
   PROF(TCQR_K2_LEAF, 2.0 * lds * w * w, 8.0 * lds * w,
        e = leaf_fused((int)lds, w, ws.tstack, lds, nullptr, 0, J.R + c0 + (long long)c0 * J.ldr,
-                      J.ldr, c0, c.d_status, ws.P, scratch, bar, &ws.leaf_bars, c.num_sms,
-                      c.stream));
+                      J.ldr, c0, c.d_status, ws.ltag, ws.leaf_tags, c.num_sms, c.stream));
   CK(e);
   PROF(TCQR_K2_APPLY, 2.0 * m * w * w, 8.0 * m * w + (need_h ? 2.0 * m * w : 0.0),
        CK(apply_right(m, w, Qc, J.ldq, ws.tstack + (long long)c.rank * w, lds,
@@ -744,7 +745,9 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     // stream; everything after it waits for the rest of that update
     cudaEvent_t e = J.la_pending;
     J.la_pending = nullptr;
+    J.la_leaf = true;
     const int rc = rgs(J, c0, w, need_h);
+    J.la_leaf = false;
     CK(cudaStreamWaitEvent(c.stream, e, 0));
     return rc;
   }
@@ -760,9 +763,8 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     cudaError_t e = cudaErrorNotSupported;
     PROF(TCQR_K2_LEAF, 2.0 * m * w * w, 8.0 * m * w + (need_h ? 2.0 * m * w : 0.0),
          e = leaf_fused(m, w, Qc, J.ldq, need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, ws.ldh,
-                        J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0, c.d_status, ws.P,
-                        sizeof(float) * (size_t)ws.p_cap, reinterpret_cast<unsigned*>(ws.iws + ws.iws_cap - 16),
-                        &ws.leaf_bars, c.num_sms, c.stream));
+                        J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0, c.d_status, ws.ltag,
+                        ws.leaf_tags, c.num_sms - (J.la_leaf ? c.leaf_reserve : 0), c.stream));
     if (e == cudaSuccess) {
       if (need_h) CKR(emit_q_lo(J, c0, w));
       return chunk_done(J, c0, w);
@@ -955,7 +957,8 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));  // INT_MAX-ish = OK
   CK(cudaMemsetAsync(R, 0, sizeof(float) * (size_t)n * n, c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
-  ws.leaf_bars = 0;
+  ws.leaf_tags[0] = 0;
+  CK(cudaMemsetAsync(ws.ltag, 0, sizeof(unsigned long long) * leaf_tag_words(), c.stream));
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   PROF(TCQR_COPY, 0, 8.0 * m * n, CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream)));
   FactorJob J{m, n, Q, (long long)m, R, (long long)n, &ws};
@@ -1209,6 +1212,8 @@ static int init_ctx(int device, void* cuda_stream, const void* nccl_unique_id, i
     c.la_max_w = w ? atoi(w) : 512;
     const char* n = getenv("TCQR_LA_SMS");
     c.la_sms = n ? std::max(1, atoi(n)) : 10;
+    const char* r = getenv("TCQR_LEAF_RESERVE");
+    c.leaf_reserve = r ? std::max(0, atoi(r)) : c.la_sms;
   }
   c.num_sms = prop.multiProcessorCount;
   // virtual ranks share one device: each gets an even 1/P share of the SMs as its grid budget,
@@ -1588,7 +1593,8 @@ static int factor_host_streamed(int m, int n, const float* A, long long lda, flo
   // compute stream
   CK(cudaMemsetAsync(dR, 0, sizeof(float) * (size_t)n * n, c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
-  ws.leaf_bars = 0;
+  ws.leaf_tags[0] = 0;
+  CK(cudaMemsetAsync(ws.ltag, 0, sizeof(unsigned long long) * leaf_tag_words(), c.stream));
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   FactorJob J{m, n, dQ, (long long)m, dR, (long long)n, &ws, &sp};
   rc = rgs(J, 0, n, n > c.cfg.cutoff);
@@ -1760,7 +1766,8 @@ int tcqr_panel_qr(int64_t m, int64_t w, float* X, int64_t ldx, float* R, int64_t
   plan_factor_ws(a, m, 32, 1, ws);
   CK(cudaMemsetAsync(c.d_status, 0x7f, sizeof(int), c.stream));
   CK(cudaMemsetAsync(ws.iws, 0, sizeof(int) * (size_t)ws.iws_cap, c.stream));
-  ws.leaf_bars = 0;
+  ws.leaf_tags[0] = 0;
+  CK(cudaMemsetAsync(ws.ltag, 0, sizeof(unsigned long long) * leaf_tag_words(), c.stream));
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
   bool wrote_h = false;
   int rc = panel(ws, (int)m, (int)w, X, ldx, R, ldr, 0, nullptr, &wrote_h);
