@@ -73,7 +73,11 @@ typedef struct tcqr_config {
                         cooperative launch with 256-row blocks resident in shared memory and the
                         Eq. (6) stack factored through its FP64 Gram matrix (reading R-B1);
                         0: one pipelined MGS-root panel launch per 32 columns plus FP32
-                        projection launches (default 1)                                         */
+                        projection launches (default 1).  Across ranks (P > 1): 1 = replicated
+                        leaves when P * (rows per rank, padded) fit one such grid (the leaf's rows
+                        allgathered, every rank factors the whole leaf, keeps its rows of Q),
+                        else the per-leaf TSQR (local leaf, allgather of the P local R's, the
+                        stack's leaf, Q_r <- Q_r S_r); 2 = always the per-leaf TSQR             */
   int fp16_split;    /* 1: error-compensated FP16 split for the tensor-core split nodes (NEXT-4,
                         SURVEY.md 8(f); beyond the paper, whose related work on tensor-core
                         precision is PAPER.md:758): X diag(s) = Xh + Xl with Xh = fl16(X diag(s)),

@@ -623,58 +623,68 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
 template <int H, int W2P>
 __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, int c0, int w2,
                                        int& slot, unsigned tag) {
-  constexpr int TJ = W2P / 4, TILES = (H / 4) * TJ, G = kNT / TILES;
+  // partial R12 = Q1' A2 over the CTA's rows: 8 x 8 output tiles, G = 256 / tiles threads per tile
+  // (adjacent lanes), thread g of a tile takes the rows g, g + G, ... (two 16-byte loads of Q1 and
+  // two of A2 per row feed 32 FFMA2: FMA-bound, where 4 x 4 tiles were shared-memory bound); the
+  // G partial tiles are added by a transposing xor-shuffle reduction (each level halves the values a
+  // lane keeps, fixed order), after which lane g holds entries [g 64/G, (g+1) 64/G) of the tile
+  constexpr int TJ = W2P / 8, TILES = (H / 8) * TJ, G = kNT / TILES, KEEP = 64 / G;
+  static_assert(G >= 2 && G <= 32 && (G & (G - 1)) == 0, "tile groups");
   const int t = threadIdx.x;
   asm volatile("cp.async.wait_all;" ::: "memory");  // the leaf's later columns (loaded async)
   __syncthreads();
-  const int tile = t % TILES, grp = t / TILES;
+  const int tile = t / G, grp = t % G;
   const int ti = tile / TJ, tj = tile % TJ;
-  float acc[4][4];
+  float2 acc[8][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
   {
-    const float* q1 = s.L + c0 + 4 * ti;
-    const float* a2 = s.L + c0 + H + 4 * tj;
-#pragma unroll 4
+    const float* q1 = s.L + c0 + 8 * ti;
+    const float* a2 = s.L + c0 + H + 8 * tj;
+#pragma unroll 2
     for (int r = grp; r < nrows; r += G) {
-      const float4 qv = *reinterpret_cast<const float4*>(q1 + r * kLd);
-      const float4 av = *reinterpret_cast<const float4*>(a2 + r * kLd);
-      const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
-      const float2 a01 = make_float2(av.x, av.y), a23 = make_float2(av.z, av.w);
+      const float4 q0 = *reinterpret_cast<const float4*>(q1 + r * kLd);
+      const float4 q4 = *reinterpret_cast<const float4*>(q1 + r * kLd + 4);
+      const float4 a0 = *reinterpret_cast<const float4*>(a2 + r * kLd);
+      const float4 a4 = *reinterpret_cast<const float4*>(a2 + r * kLd + 4);
+      const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q4.x, q4.y, q4.z, q4.w};
+      const float2 av[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w),
+                            make_float2(a4.x, a4.y), make_float2(a4.z, a4.w)};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {  // FFMA2: the same fmaf sequence per entry, two per instruction
+      for (int i = 0; i < 8; ++i) {
         const float2 qi = make_float2(qq[i], qq[i]);
-        float2 c01 = ffma2(qi, a01, make_float2(acc[i][0], acc[i][1]));
-        float2 c23 = ffma2(qi, a23, make_float2(acc[i][2], acc[i][3]));
-        acc[i][0] = c01.x;
-        acc[i][1] = c01.y;
-        acc[i][2] = c23.x;
-        acc[i][3] = c23.y;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = ffma2(qi, av[j], acc[i][j]);
+      }
+    }
+  }
+  float v[64];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[8 * i + 2 * j] = acc[i][j].x;
+      v[8 * i + 2 * j + 1] = acc[i][j].y;
+    }
+#pragma unroll
+  for (int o = G / 2, hs = 32; o >= 1; o /= 2, hs /= 2) {
+    const bool up = (grp & o) != 0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k < hs) {
+        const float send = up ? v[k] : v[k + hs];
+        const float keep = up ? v[k + hs] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
       }
     }
   }
   unsigned long long* pp = a.tg + kTgPP + (long long)blockIdx.x * 4096;
-  if (G == 1) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) TagWords<float>::put(pp + (4 * ti + i) * W2P + 4 * tj + j, acc[i][j], tag);
-  } else {
-    // row groups: combine in group order through shared memory
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      *reinterpret_cast<float4*>(s.u.T + grp * (H * W2P) + (4 * ti + i) * W2P + 4 * tj) =
-          make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-    __syncthreads();
-    for (int e = t; e < H * W2P; e += kNT) {
-      float v = s.u.T[e];
-#pragma unroll
-      for (int g = 1; g < G; ++g) v += s.u.T[g * (H * W2P) + e];
-      TagWords<float>::put(pp + e, v, tag);
-    }
-    __syncthreads();  // s.u.T is reused for the gathered sum below
+  for (int k = 0; k < KEEP; ++k) {
+    const int idx = grp * KEEP + k;
+    TagWords<float>::put(pp + (8 * ti + idx / 8) * W2P + 8 * tj + idx % 8, v[k], tag);
   }
   leaf_ts(a, slot);
   tagged_sum<float>(a, a.tg + kTgPP, 4096, H * W2P, tag, a.tg + kTgPS, s.wsum, H, w2, W2P, c0,
@@ -727,54 +737,55 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
     leaf_ts(a, slot);
     return;
   }
-  // A2 -= Q1 R12: thread = rows (t % 128, t % 128 + 128), columns [jh * W2P/2, (jh+1) * W2P/2)
-  constexpr int JC = W2P / 2;
-  const int r0 = t % 128, jh = t / 128;
-  float u[2][JC];
+  // A2 -= Q1 R12: thread = rows rq + 64 rr (rr = 0..3; a warp's lanes take consecutive rows, so
+  // the 16-byte loads of Q1 are conflict-free), columns [jq W2P/4, (jq+1) W2P/4): four rows share
+  // every (broadcast) load of R12, so the FFMA2 issue dominates; terms summed in increasing i
+  constexpr int JC = W2P / 4;
+  const int rq = t % 64, jq = t / 64;
+  float2 u[4][JC / 2];
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr)
+  for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
-    for (int j = 0; j < JC; ++j) u[rr][j] = 0.f;
-  const float* qa = s.L + r0 * kLd + c0;
-  const float* qb = s.L + (r0 + 128) * kLd + c0;
-#pragma unroll 2
+    for (int j = 0; j < JC / 2; ++j) u[rr][j] = make_float2(0.f, 0.f);
+#pragma unroll 1
   for (int i4 = 0; i4 < H; i4 += 4) {
-    const float4 va = *reinterpret_cast<const float4*>(qa + i4);
-    const float4 vb = *reinterpret_cast<const float4*>(qb + i4);
-    const float qx[2][4] = {{va.x, va.y, va.z, va.w}, {vb.x, vb.y, vb.z, vb.w}};
+    float qx[4][4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const float4 q = *reinterpret_cast<const float4*>(s.L + (rq + 64 * rr) * kLd + c0 + i4);
+      qx[rr][0] = q.x;
+      qx[rr][1] = q.y;
+      qx[rr][2] = q.z;
+      qx[rr][3] = q.w;
+    }
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii) {
-      const float4* tr = reinterpret_cast<const float4*>(s.u.T + (i4 + ii) * W2P + jh * JC);
+      const float4* tr = reinterpret_cast<const float4*>(s.u.T + (i4 + ii) * W2P + jq * JC);
 #pragma unroll
       for (int j4 = 0; j4 < JC / 4; ++j4) {
         const float4 v = tr[j4];
+        const float2 v01 = make_float2(v.x, v.y), v23 = make_float2(v.z, v.w);
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
+        for (int rr = 0; rr < 4; ++rr) {
           const float2 qi = make_float2(qx[rr][ii], qx[rr][ii]);
-          const float2 c01 = ffma2(qi, make_float2(v.x, v.y),
-                                   make_float2(u[rr][4 * j4], u[rr][4 * j4 + 1]));
-          const float2 c23 = ffma2(qi, make_float2(v.z, v.w),
-                                   make_float2(u[rr][4 * j4 + 2], u[rr][4 * j4 + 3]));
-          u[rr][4 * j4] = c01.x;
-          u[rr][4 * j4 + 1] = c01.y;
-          u[rr][4 * j4 + 2] = c23.x;
-          u[rr][4 * j4 + 3] = c23.y;
+          u[rr][2 * j4] = ffma2(qi, v01, u[rr][2 * j4]);
+          u[rr][2 * j4 + 1] = ffma2(qi, v23, u[rr][2 * j4 + 1]);
         }
       }
     }
   }
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const int r = r0 + rr * 128;
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = rq + 64 * rr;
     if (r < nrows) {
-      float* dst = s.L + r * kLd + c0 + H + jh * JC;
+      float* dst = s.L + r * kLd + c0 + H + jq * JC;
 #pragma unroll
       for (int j4 = 0; j4 < JC / 4; ++j4) {
         float4 v = *reinterpret_cast<float4*>(dst + 4 * j4);
-        v.x -= u[rr][4 * j4];
-        v.y -= u[rr][4 * j4 + 1];
-        v.z -= u[rr][4 * j4 + 2];
-        v.w -= u[rr][4 * j4 + 3];
+        v.x -= u[rr][2 * j4].x;
+        v.y -= u[rr][2 * j4].y;
+        v.z -= u[rr][2 * j4 + 1].x;
+        v.w -= u[rr][2 * j4 + 1].y;
         *reinterpret_cast<float4*>(dst + 4 * j4) = v;
       }
     }
@@ -941,6 +952,50 @@ cudaError_t apply_right(int m, int w, float* X, long long ldx, const float* S, l
   }
   apply_right_kernel<<<(m + kApRows - 1) / kApRows, 256, smem, st>>>(m, w, X, ldx, S, lds, Xh,
                                                                       ldh);
+  return cudaGetLastError();
+}
+
+namespace {
+
+// Replicated leaf across ranks (tcqr.cu leaf_replicated): the rank's m x w rows packed into an
+// mpad x w column-major block (zero rows past m) for the allgather, and its rows of the factored
+// full panel unpacked back into X with the FP16 shadow (Xh nullable).
+__global__ void pack_rows_kernel(int m, int w, const float* __restrict__ X, long long ldx, int mpad,
+                                 float* __restrict__ dst) {
+  const long long total = (long long)mpad * w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % mpad), j = (int)(e / mpad);
+    dst[e] = i < m ? X[i + (long long)j * ldx] : 0.f;
+  }
+}
+__global__ void unpack_rows_kernel(int m, int w, const float* __restrict__ src, long long lds,
+                                   float* __restrict__ X, long long ldx, __half* __restrict__ Xh,
+                                   long long ldh) {
+  const long long total = (long long)m * w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    const float v = src[i + (long long)j * lds];
+    X[i + (long long)j * ldx] = v;
+    if (Xh) Xh[i + (long long)j * ldh] = __float2half_rn(v);
+  }
+}
+
+}  // namespace
+
+cudaError_t pack_rows(int m, int w, const float* X, long long ldx, int mpad, float* dst,
+                      cudaStream_t st) {
+  const long long total = (long long)mpad * w;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  pack_rows_kernel<<<std::max(grid, 1), 256, 0, st>>>(m, w, X, ldx, mpad, dst);
+  return cudaGetLastError();
+}
+cudaError_t unpack_rows(int m, int w, const float* src, long long lds, float* X, long long ldx,
+                        __half* Xh, long long ldh, cudaStream_t st) {
+  const long long total = (long long)m * w;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  unpack_rows_kernel<<<std::max(grid, 1), 256, 0, st>>>(m, w, src, lds, X, ldx, Xh, ldh);
   return cudaGetLastError();
 }
 

@@ -96,6 +96,13 @@ cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long 
                        long long ldr, int col0, int* status, unsigned long long* tg,
                        unsigned* tag_seq, int num_sms, cudaStream_t st);
 
+// Replicated leaf across ranks: pack the rank's m x w rows into an mpad x w block (ld mpad, zero
+// rows past m); unpack rows of a factored panel (ld lds) into X and its FP16 shadow Xh (nullable).
+cudaError_t pack_rows(int m, int w, const float* X, long long ldx, int mpad, float* dst,
+                      cudaStream_t st);
+cudaError_t unpack_rows(int m, int w, const float* src, long long lds, float* X, long long ldx,
+                        __half* Xh, long long ldh, cudaStream_t st);
+
 // X (m x w, ldx; w <= 128) <- X S (S w x w, lds; FP32), FP16 shadow of the result into Xh if
 // non-null: Eq. (6) step 4 for the per-leaf TSQR across ranks.
 cudaError_t apply_right(int m, int w, float* X, long long ldx, const float* S, long long lds,

@@ -94,6 +94,11 @@ struct Context {
   void* hstage = nullptr;   // device staging of the host-pointer entry points (grow-only, so
   size_t hstage_bytes = 0;  // pointers stay stable and the factorization graph is reused)
   int* d_status = nullptr;  // [0] factor status, [1] scratch
+  // replicated leaves across ranks (leaf_replicated): the agreed padded rows per rank of this call
+  // (0: off) and the pack / gather / full-panel buffer
+  int rep_mmax = 0;
+  float* rep_buf = nullptr;
+  size_t rep_bytes = 0;
   int* h_status = nullptr;  // pinned
   std::map<std::string, GraphEntry> graphs;
 };
@@ -736,6 +741,67 @@ static int leaf_tsqr(FactorJob& J, int c0, int w, bool need_h) {
   return chunk_done(J, c0, w);
 }
 
+// Replicated leaf across ranks (cfg.leaf_kernel == 1, P * mmax rows fit one co-resident K2L grid):
+// the P ranks' rows of the leaf are allgathered (one collective, zero rows padding every rank to
+// mmax), every rank factors the whole leaf with the one-GPU whole-leaf kernel (identical inputs
+// and code: R and every Q row bit-identical on all ranks; global breakdowns flagged there) and
+// keeps its own rows of Q with the FP16 shadow.  The leaf's dependent chain is the one-GPU chain
+// (the per-leaf TSQR runs two of them back to back: the local leaf, then the stack's).
+static int leaf_replicated(FactorJob& J, int c0, int w, bool need_h) {
+  Context& c = g_ctx;
+  FactorWs& ws = *J.ws;
+  const int P = c.nranks, mm = c.rep_mmax, m = J.m;
+  const long long M = (long long)P * mm;
+  float* Qc = J.Q + (long long)c0 * J.ldq;
+  float* send = c.rep_buf;
+  float* gath = send + (size_t)mm * 128;
+  float* full = gath + (size_t)P * mm * 128;
+  CK(pack_rows(m, w, Qc, J.ldq, mm, send, c.stream));
+  CKR(allgather_f32(send, gath, (size_t)mm * w));
+  for (int r = 0; r < P; ++r)
+    CK(cudaMemcpy2DAsync(full + (long long)r * mm, sizeof(float) * M, gath + (long long)r * mm * w,
+                         sizeof(float) * mm, sizeof(float) * mm, w, cudaMemcpyDeviceToDevice,
+                         c.stream));
+  cudaError_t e = cudaErrorNotSupported;
+  PROF(TCQR_K2_LEAF, 2.0 * M * w * w, 8.0 * M * w,
+       e = leaf_fused((int)M, w, full, M, nullptr, 0, J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0,
+                      c.d_status, ws.ltag, ws.leaf_tags, c.num_sms, c.stream));
+  CK(e);
+  CK(unpack_rows(m, w, full + (long long)c.rank * mm, M, Qc, J.ldq,
+                 need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, ws.ldh, c.stream));
+  if (need_h) CKR(emit_q_lo(J, c0, w));
+  return chunk_done(J, c0, w);
+}
+
+// Agree on the padded rows per rank for the replicated leaves of this call (one min-allreduce of
+// -m, read back on the host before the factorization is enqueued or its graph replayed) and size
+// the buffer; c.rep_mmax = 0 when the leaves use the per-leaf TSQR instead.
+static int plan_leaf_replication(int m) {
+  Context& c = g_ctx;
+  c.rep_mmax = 0;
+  if (c.nranks <= 1 || c.cfg.leaf_kernel != 1) return 0;
+  const int neg = -m;
+  CK(cudaMemcpyAsync(c.d_status + 1, &neg, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  CKR(allreduce_min_i32(c.d_status + 1));
+  int mx = 0;
+  CK(cudaMemcpyAsync(&mx, c.d_status + 1, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  const int mm = (int)round_up(-mx, 4);
+  const long long M = (long long)c.nranks * mm;
+  if (M > 256LL * c.num_sms) return 0;
+  if (c.vg && (size_t)mm * 128 * sizeof(float) > c.vg->slot_bytes) return 0;
+  const size_t need = sizeof(float) * (size_t)mm * 128 * (1 + 2 * (size_t)c.nranks);
+  if (c.rep_bytes < need) {
+    if (c.rep_buf) cudaFree(c.rep_buf);
+    c.rep_buf = nullptr;
+    c.rep_bytes = 0;
+    if (cudaMalloc(&c.rep_buf, need) != cudaSuccess) return TCQR_ERR_OOM;
+    c.rep_bytes = need;
+  }
+  c.rep_mmax = mm;
+  return 0;
+}
+
 static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   Context& c = g_ctx;
   FactorWs& ws = *J.ws;
@@ -752,6 +818,10 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     return rc;
   }
   float* Qc = J.Q + (long long)c0 * J.ldq;
+  if (c.rep_mmax > 0 && c.nranks > 1 && w <= 128 && w <= c.cfg.cutoff && !J.sp) {
+    need_cols(J, c0, c0 + w);
+    return leaf_replicated(J, c0, w, need_h);
+  }
   if (c.cfg.leaf_kernel && c.nranks > 1 && w <= 128 && w <= c.cfg.cutoff && !J.sp) {
     need_cols(J, c0, c0 + w);
     const int rc = leaf_tsqr(J, c0, w, need_h);
@@ -1009,7 +1079,8 @@ static int run_factor(int m, int n, const float* A, long long lda, float* Q, flo
   // virtual ranks: no capture (their collectives order P streams with events and host barriers)
   if (!c.cfg.use_graphs || g_prof || c.vg) return enqueue_factor(m, n, A, lda, Q, R, ws);
   const std::string key =
-      graph_key("f", {m, n, lda, (long long)A, (long long)Q, (long long)R, (long long)ws_base});
+      graph_key("f", {m, n, lda, (long long)A, (long long)Q, (long long)R, (long long)ws_base,
+                      (long long)c.rep_mmax});
   auto it = c.graphs.find(key);
   if (it == c.graphs.end()) {
     cudaGraph_t g = nullptr;
@@ -1089,7 +1160,7 @@ int tcqr_set_config(const tcqr_config_t* cfg) {
   if (cfg->tol2 <= 0 || cfg->stag_window < 1 || cfg->stag_floor < 0) return -1;
   if (cfg->reorth != 0 && cfg->reorth != 1) return -1;
   if (cfg->warm_start != 0 && cfg->warm_start != 1) return -1;
-  if (cfg->leaf_kernel != 0 && cfg->leaf_kernel != 1) return -1;
+  if (cfg->leaf_kernel < 0 || cfg->leaf_kernel > 2) return -1;
   if (cfg->fp16_split != 0 && cfg->fp16_split != 1) return -1;
   g_ctx.cfg = *cfg;
   return 0;
@@ -1131,6 +1202,10 @@ static int finalize_ctx() {
   c.hstage = nullptr;
   c.hstage_bytes = 0;
   if (c.d_status) cudaFree(c.d_status);
+  if (c.rep_buf) cudaFree(c.rep_buf);
+  c.rep_buf = nullptr;
+  c.rep_bytes = 0;
+  c.rep_mmax = 0;
   if (c.h_status) cudaFreeHost(c.h_status);
   c.d_status = nullptr;
   c.h_status = nullptr;
@@ -1324,6 +1399,11 @@ int tcqr_factor(int64_t m, int64_t n, const float* A, int64_t lda, float* Q, flo
   Arena a{base, 0};
   FactorWs ws;
   plan_factor_ws(a, m, n, c.nranks, ws, c.cfg.reorth != 0);
+  rc = plan_leaf_replication((int)m);
+  if (rc) {
+    vabort(c.vg);
+    return rc;
+  }
   c.ncoll = 0;
   rc = run_factor((int)m, (int)n, A, lda, Q, R, ws, base);
   if (rc == 0) rc = read_status();
@@ -1467,6 +1547,11 @@ static int lls_solve_impl(int64_t m, int64_t n, const float* A, int64_t lda, con
   Arena a{base, 0};
   LlsWs w;
   plan_lls_ws(a, m, n, c.nranks, maxit, w);
+  rc = plan_leaf_replication((int)m);
+  if (rc) {
+    vabort(c.vg);
+    return rc;
+  }
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

@@ -132,10 +132,13 @@ def _leaves_and_splits(n, c=128):
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_vranks_factor_matches_oracle(tq, P):
+@pytest.mark.parametrize("leaf_kernel", [1, 2])
+def test_vranks_factor_matches_oracle(tq, P, leaf_kernel):
+    # leaf_kernel=1: replicated leaves (P x 4096/P rows fit one whole-leaf grid of the rank's SM
+    # share); leaf_kernel=2: per-leaf TSQR
     m, n = 4096, 512
     a = W.gaussian(m, n, seed=900 + P)
-    qs, rs, res, bounds = _vfactor(tq, a, P)
+    qs, rs, res, bounds = _vfactor(tq, a, P, leaf_kernel=leaf_kernel)
     assert all(rc == 0 for rc, _ in res), res
     for r in rs[1:]:
         assert np.array_equal(r, rs[0])                 # R replicated bitwise on all ranks
@@ -152,7 +155,8 @@ def test_vranks_factor_matches_oracle(tq, P):
     assert r_rel_error(r, od[0][1]) <= 1e-2
     q_od = np.vstack([o[0] for o in od])
     assert np.linalg.norm(q - q_od) / np.linalg.norm(q_od) <= 1e-2
-    # per-leaf TSQR: one allgather per leaf, one R12 allreduce per split node, one status
+    # one allgather per leaf (the leaf's rows, or the local R's), one R12 allreduce per split
+    # node, one status
     leaves, splits = _leaves_and_splits(n)
     assert all(cnt == leaves + splits + 1 for _, cnt in res), (res, leaves, splits)
 
@@ -195,6 +199,19 @@ def test_vranks_planted_hadamard_zero_padded_bitwise(tq, P, leaf_kernel, cutoff)
     assert np.array_equal(qs[0], qt)
     for q in qs[1:]:
         assert not np.any(q)
+
+
+def test_vranks_planted_hadamard_replicated_leaves_bitwise(tq):
+    # P2 through the replicated leaves: 4 x 1024 Hadamard rows gathered into one 4096-row leaf
+    # (128-row K2L blocks, 64-row MGS blocks: powers of 4) -> R == R0 and Q == H / sqrt(m)
+    # bitwise on every rank, and Q identical to the one-GPU factorization
+    m, n, P = 4096, 256, 4
+    a, qt, r0 = W.planted_hadamard(m, n, seed=205)
+    qs, rs, res, bounds = _vfactor(tq, a, P, leaf_kernel=1)
+    assert all(rc == 0 for rc, _ in res), res
+    for r in rs:
+        assert np.array_equal(r, r0)
+    assert np.array_equal(np.vstack(qs), qt)
 
 
 def test_vranks_planted_hadamard_all_ranks_bitwise(tq):
