@@ -78,6 +78,13 @@ struct Context {
   int la_max_w = 512;  // env TCQR_LOOKAHEAD_W (0: off); measured: 1024 and up lose (the tail outlasts the leaf)
   int la_sms = 10;      // env TCQR_LA_SMS (the short-K update runs two CTAs per SM)
   int leaf_reserve = 10;  // env TCQR_LEAF_RESERVE: SMs the leaf beside a look-ahead leaves free
+  // Across ranks: a split node's R12 allreduce in column chunks of ar_chunk on s_comm, each
+  // chunk's allreduce overlapping the next chunks' TN products and the previous chunks' finalize
+  // and NN updates (nodes with at least 2 * ar_chunk columns; env TCQR_AR_CHUNK, 0: off)
+  cudaStream_t s_comm = nullptr;
+  static constexpr int kArEv = 64;
+  cudaEvent_t ev_tn[kArEv] = {}, ev_ar[kArEv] = {};
+  int ar_chunk = 1024;
   int num_sms = 148;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
@@ -400,7 +407,8 @@ __global__ void vcomm_kernel(int op, int n, VSlots in, void* out, long long coun
   }
 }
 
-static int vcollective(int op, const void* send, void* recv, size_t count, size_t elem) {
+static int vcollective(int op, const void* send, void* recv, size_t count, size_t elem,
+                       cudaStream_t st) {
   Context& c = g_ctx;
   VGroup& g = *c.vg;
   const size_t bytes = count * elem;
@@ -414,35 +422,36 @@ static int vcollective(int op, const void* send, void* recv, size_t count, size_
   const int par = (int)(k & 1), e = (int)(k & 3), r = c.rank;
   // the slot of this parity is free once every rank has read collective k - 2
   if (k >= 2)
-    for (int q = 0; q < g.n; ++q) cudaStreamWaitEvent(c.stream, g.ev_read[(k - 2) & 3][q], 0);
-  if (cudaMemcpyAsync(g.slot[par][r], send, bytes, cudaMemcpyDeviceToDevice, c.stream) !=
+    for (int q = 0; q < g.n; ++q) cudaStreamWaitEvent(st, g.ev_read[(k - 2) & 3][q], 0);
+  if (cudaMemcpyAsync(g.slot[par][r], send, bytes, cudaMemcpyDeviceToDevice, st) !=
           cudaSuccess ||
-      cudaEventRecord(g.ev_written[e][r], c.stream) != cudaSuccess) {
+      cudaEventRecord(g.ev_written[e][r], st) != cudaSuccess) {
     vabort(&g);
     return TCQR_ERR_CUDA;
   }
   if (!vbarrier(g)) return TCQR_ERR_NCCL;
   VSlots in{};
   for (int q = 0; q < g.n; ++q) {
-    cudaStreamWaitEvent(c.stream, g.ev_written[e][q], 0);
+    cudaStreamWaitEvent(st, g.ev_written[e][q], 0);
     in.p[q] = g.slot[par][q];
   }
   const int grid = (int)std::min<size_t>((count + 255) / 256, 1184);
-  vcomm_kernel<<<std::max(grid, 1), 256, 0, c.stream>>>(op, g.n, in, recv, (long long)count);
+  vcomm_kernel<<<std::max(grid, 1), 256, 0, st>>>(op, g.n, in, recv, (long long)count);
   if (cudaGetLastError() != cudaSuccess ||
-      cudaEventRecord(g.ev_read[e][r], c.stream) != cudaSuccess) {
+      cudaEventRecord(g.ev_read[e][r], st) != cudaSuccess) {
     vabort(&g);
     return TCQR_ERR_CUDA;
   }
   return 0;
 }
 
-static int allreduce_f32(float* buf, size_t count) {
+static int allreduce_f32(float* buf, size_t count, cudaStream_t st = nullptr) {
   Context& c = g_ctx;
   if (c.nranks <= 1) return 0;
+  if (!st) st = c.stream;
   ++c.ncoll;
-  if (c.vg) return vcollective(kVSumF32, buf, buf, count, sizeof(float));
-  return g_nccl.AllReduce(buf, buf, count, ncclFloat32, ncclSum, c.comm, c.stream) == ncclSuccess
+  if (c.vg) return vcollective(kVSumF32, buf, buf, count, sizeof(float), st);
+  return g_nccl.AllReduce(buf, buf, count, ncclFloat32, ncclSum, c.comm, st) == ncclSuccess
              ? 0
              : TCQR_ERR_NCCL;
 }
@@ -450,7 +459,7 @@ static int allreduce_f64(double* buf, size_t count) {
   Context& c = g_ctx;
   if (c.nranks <= 1) return 0;
   ++c.ncoll;
-  if (c.vg) return vcollective(kVSumF64, buf, buf, count, sizeof(double));
+  if (c.vg) return vcollective(kVSumF64, buf, buf, count, sizeof(double), c.stream);
   return g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, c.comm, c.stream) == ncclSuccess
              ? 0
              : TCQR_ERR_NCCL;
@@ -460,7 +469,7 @@ static int allreduce_min_i32(int* buf) {
   Context& c = g_ctx;
   if (c.nranks <= 1) return 0;
   ++c.ncoll;
-  if (c.vg) return vcollective(kVMinI32, buf, buf, 1, sizeof(int));
+  if (c.vg) return vcollective(kVMinI32, buf, buf, 1, sizeof(int), c.stream);
   return g_nccl.AllReduce(buf, buf, 1, ncclInt32, ncclMin, c.comm, c.stream) == ncclSuccess
              ? 0
              : TCQR_ERR_NCCL;
@@ -469,7 +478,7 @@ static int allreduce_min_i32(int* buf) {
 static int allgather_f32(const float* send, float* recv, size_t count) {
   Context& c = g_ctx;
   ++c.ncoll;
-  if (c.vg) return vcollective(kVGatherF32, send, recv, count, sizeof(float));
+  if (c.vg) return vcollective(kVGatherF32, send, recv, count, sizeof(float), c.stream);
   return g_nccl.AllGather(send, recv, count, ncclFloat32, c.comm, c.stream) == ncclSuccess
              ? 0
              : TCQR_ERR_NCCL;
@@ -945,6 +954,36 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
           PROF(TCQR_K3_TN, 2.0 * m * h * wp, 2.0 * m * (h + wp) + 14.0 * h * wp,
                CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, Tp, h, ws.inv_s + p0, ws.P,
                              ws.p_cap, c.num_sms, c.stream, &fin)));
+        } else if (c.ar_chunk > 0 && wp >= 2 * c.ar_chunk && !g_prof) {
+          // across ranks, wide node: the R12 allreduce in column chunks on s_comm, overlapping
+          // the next chunks' TN products and the earlier chunks' finalize + NN (every column of
+          // R12 and of the update depends only on its own A2 column)
+          const int cw = c.ar_chunk, nk = (wp + cw - 1) / cw;
+          for (int k0 = 0; k0 < nk; k0 += Context::kArEv) {
+            const int k1 = std::min(nk, k0 + Context::kArEv);
+            for (int k = k0; k < k1; ++k) {
+              const int j0 = k * cw, wk = std::min(cw, wp - j0);
+              float* Tk = Tp + (long long)j0 * h;
+              CK(tc_gemm_tn(m, h, wk, A1h, ws.ldh, A2h + (long long)j0 * ws.ldh, ws.ldh, Tk, h,
+                            ws.inv_s + p0 + j0, ws.P, ws.p_cap, c.num_sms, c.stream));
+              CK(cudaEventRecord(c.ev_tn[k - k0], c.stream));
+              CK(cudaStreamWaitEvent(c.s_comm, c.ev_tn[k - k0], 0));
+              CKR(allreduce_f32(Tk, (size_t)h * wk, c.s_comm));
+              CK(cudaEventRecord(c.ev_ar[k - k0], c.s_comm));
+            }
+            for (int k = k0; k < k1; ++k) {
+              const int j0 = k * cw, wk = std::min(cw, wp - j0);
+              CK(cudaStreamWaitEvent(c.stream, c.ev_ar[k - k0], 0));
+              CK(r12_finalize(h, wk, Tp + (long long)j0 * h, h,
+                              Rblk + (long long)(off + j0) * J.ldr, J.ldr,
+                              R12hp + (long long)j0 * ldh2, ldh2, ws.inv_s2 + p0 + j0,
+                              c.cfg.col_scaling, c.stream));
+              CK(tc_gemm_nn_update(m, h, wk, A1h, ws.ldh, R12hp + (long long)j0 * ldh2, ldh2,
+                                   A2p + (long long)j0 * J.ldq, J.ldq, ws.inv_s2 + p0 + j0,
+                                   c.num_sms, c.stream));
+            }
+          }
+          continue;
         } else {
           PROF(TCQR_K3_TN, 2.0 * m * h * wp, 2.0 * m * (h + wp) + 4.0 * h * wp,
                CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, Tp, h, ws.inv_s + p0, ws.P,
@@ -1218,6 +1257,13 @@ static int finalize_ctx() {
   c.s_side = nullptr;
   if (c.s_la) cudaStreamDestroy(c.s_la);
   c.s_la = nullptr;
+  if (c.s_comm) cudaStreamDestroy(c.s_comm);
+  c.s_comm = nullptr;
+  for (int i = 0; i < Context::kArEv; ++i) {
+    if (c.ev_tn[i]) cudaEventDestroy(c.ev_tn[i]);
+    if (c.ev_ar[i]) cudaEventDestroy(c.ev_ar[i]);
+    c.ev_tn[i] = c.ev_ar[i] = nullptr;
+  }
   for (int i = 0; i < 64; ++i) {
     if (c.ev_fork[i]) cudaEventDestroy(c.ev_fork[i]);
     if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
@@ -1273,7 +1319,13 @@ static int init_ctx(int device, void* cuda_stream, const void* nccl_unique_id, i
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo: the least urgent
     if (cudaStreamCreateWithPriority(&c.s_la, cudaStreamNonBlocking, lo) != cudaSuccess)
       return TCQR_ERR_CUDA;
+    if (cudaStreamCreateWithPriority(&c.s_comm, cudaStreamNonBlocking, hi) != cudaSuccess)
+      return TCQR_ERR_CUDA;
   }
+  for (int i = 0; i < Context::kArEv; ++i)
+    if (cudaEventCreateWithFlags(&c.ev_tn[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.ev_ar[i], cudaEventDisableTiming) != cudaSuccess)
+      return TCQR_ERR_CUDA;
   for (int i = 0; i < 64; ++i)
     if (cudaEventCreateWithFlags(&c.ev_fork[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming) != cudaSuccess ||
@@ -1289,6 +1341,8 @@ static int init_ctx(int device, void* cuda_stream, const void* nccl_unique_id, i
     c.la_sms = n ? std::max(1, atoi(n)) : 10;
     const char* r = getenv("TCQR_LEAF_RESERVE");
     c.leaf_reserve = r ? std::max(0, atoi(r)) : c.la_sms;
+    const char* ac = getenv("TCQR_AR_CHUNK");
+    c.ar_chunk = ac ? std::max(0, atoi(ac)) : 1024;
   }
   c.num_sms = prop.multiProcessorCount;
   // virtual ranks share one device: each gets an even 1/P share of the SMs as its grid budget,

@@ -161,6 +161,39 @@ def test_vranks_factor_matches_oracle(tq, P, leaf_kernel):
     assert all(cnt == leaves + splits + 1 for _, cnt in res), (res, leaves, splits)
 
 
+def _chunked_collectives(n, chunk, c=128):
+    """Collectives of one factor with the R12 allreduce in column chunks of `chunk` (nodes whose
+    right part has >= 2 chunks): leaves + per split node max(1, ceil(w2 / chunk)) + 1 status."""
+    def rec(w):
+        if w <= c:
+            return 1
+        h = 32 * (-(-w // 64))
+        w2 = w - h
+        k = -(-w2 // chunk) if w2 >= 2 * chunk else 1
+        return rec(h) + rec(w2) + k
+    return rec(n) + 1
+
+
+def test_vranks_chunked_r12_allreduce(tq, monkeypatch):
+    # the R12 allreduce in 64-column chunks on the communication stream, overlapping the TN and NN
+    # products (TCQR_AR_CHUNK, read when the virtual contexts are created)
+    monkeypatch.setenv("TCQR_AR_CHUNK", "64")
+    m, n, P = 4096, 512, 4
+    a = W.gaussian(m, n, seed=990)
+    qs, rs, res, bounds = _vfactor(tq, a, P)
+    assert all(rc == 0 for rc, _ in res), res
+    for r in rs[1:]:
+        assert np.array_equal(r, rs[0])
+    q, r = np.vstack(qs), rs[0]
+    a64 = a.astype(np.float64)
+    _, r_o = rgs(a64)
+    assert backward_error_f(a64, q, r) <= 5e-3
+    assert orthogonality_f(q) <= 5e-2
+    assert r_rel_error(r, r_o) <= 1e-2
+    want = _chunked_collectives(n, 64)
+    assert all(cnt == want for _, cnt in res), (res, want)
+
+
 @pytest.mark.parametrize("P,leaf_kernel,cutoff", [(2, 0, 128), (4, 0, 64), (8, 1, 32)])
 def test_vranks_factor_panel_paths(tq, P, leaf_kernel, cutoff):
     # leaf_kernel=0: per-panel TSQR (allgather per 32-column panel) + FP32 intra-leaf allreduces;
