@@ -365,6 +365,7 @@ def main():
         tq.factor(A, Q, R)
     torch.cuda.synchronize()
     launches_per_step = tq.last_launch_count()
+    collectives_per_step = tq.last_collective_count()
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -618,6 +619,7 @@ def main():
                                  "(graph replay), max over ranks"},
             "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_per_step": launches_per_step,
+            "collectives_per_step": collectives_per_step,
             "clocks": clk.summary(),
             "roofline": roofline,
             "kernel_classes": classes,
