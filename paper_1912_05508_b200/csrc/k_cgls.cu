@@ -523,11 +523,12 @@ __global__ void gemv_t_reduce_kernel(int n, int splits, const double* __restrict
   y[j] = acc;
 }
 
-// Row splits of the A' v kernel: enough CTAs for two per SM, whole 1024-row chunks (four per
-// SM measured slower at configs[3]).
+// Row splits of the A' v kernel: whole 1024-row chunks, enough CTAs for about 14 per SM (many
+// short CTAs balance across the SMs: at configs[3] 16 splits of 2048 rows take 205 us per pass,
+// 4 splits 223 us -- the 3-CTA-per-SM residency left a tail wave; tools/micro/gemv_bench.cu).
 static void gemv_t_plan(int m, int n, int* splits, int* rps) {
   const int cblocks = (n + kGtCols - 1) / kGtCols;
-  int s = (2 * 148 + cblocks - 1) / cblocks;
+  int s = (14 * 148 + cblocks - 1) / cblocks;
   const int chunks = (m + kGtChunk - 1) / kGtChunk;
   s = std::max(1, std::min(s, chunks));
   const int cps = (chunks + s - 1) / s;
