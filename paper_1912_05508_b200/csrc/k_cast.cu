@@ -610,11 +610,11 @@ __global__ void __launch_bounds__(256, 1) trmm_upper_big(int n, const float* __r
       rb[u] = (j0 + mm < n && k < kend) ? __ldg(B + k + (long long)(j0 + mm) * ldb) : 0.f;
     }
   };
-  float acc[8][8];
+  float2 acc[8][4];  // acc[x][y2] = columns (2 y2, 2 y2 + 1) of row x: FFMA2, the same fmaf per entry
 #pragma unroll
   for (int x = 0; x < 8; ++x)
 #pragma unroll
-    for (int y = 0; y < 8; ++y) acc[x][y] = 0.f;
+    for (int y = 0; y < 4; ++y) acc[x][y] = make_float2(0.f, 0.f);
   float ra[NLD], rb[NLD];
   int buf = 0;
   load(kbeg, ra, rb);
@@ -634,11 +634,14 @@ __global__ void __launch_bounds__(256, 1) trmm_upper_big(int n, const float* __r
       const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][ty * 8]);
       const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][ty * 8 + 4]);
       const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const float2 bb[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
+                            make_float2(b1.x, b1.y), make_float2(b1.z, b1.w)};
 #pragma unroll
-      for (int x = 0; x < 8; ++x)
+      for (int x = 0; x < 8; ++x) {
+        const float2 ax = make_float2(a[x], a[x]);
 #pragma unroll
-        for (int y = 0; y < 8; ++y) acc[x][y] = fmaf(a[x], bb[y], acc[x][y]);
+        for (int y = 0; y < 4; ++y) acc[x][y] = ffma2(ax, bb[y], acc[x][y]);
+      }
     }
     buf ^= 1;
   }
@@ -647,7 +650,7 @@ __global__ void __launch_bounds__(256, 1) trmm_upper_big(int n, const float* __r
 #pragma unroll
     for (int y = 0; y < 8; ++y) {
       const int r = i0 + tx * 8 + x, c = j0 + ty * 8 + y;
-      if (r < n && c < n) C[r + (long long)c * ldc] = acc[x][y];
+      if (r < n && c < n) C[r + (long long)c * ldc] = (y & 1) ? acc[x][y >> 1].y : acc[x][y >> 1].x;
     }
 }
 

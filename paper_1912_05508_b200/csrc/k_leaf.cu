@@ -52,7 +52,7 @@ constexpr int kNW = kNT / 32;
 constexpr int kBR = 64;       // rows per MGS block (4^3: powers of 4 keep the planted pin exact)
 constexpr int kMW = kRows / kBR;  // MGS blocks (= warps) per CTA: one per SM sub-partition
 constexpr int kLdR = 33;      // ld of the blocks' R_b (FP64) in shared memory
-constexpr int kLdS = 34;      // ld of the blocks' S_b (FP32; even: 8-byte pairs for FFMA2)
+constexpr int kLdS = 36;      // ld of the blocks' S_b (FP32; 16-byte rows: four columns per load)
 
 struct LeafOp {
   int kind;  // 0 panel (c0, h = width), 1 projection (c0, h, w2)
@@ -574,8 +574,8 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
   }
   // (4) Q_b <- Q_b S_b: thread t = row t (block t / 64).  S_b is upper triangular, so column j
   // takes the terms l <= j only, summed in increasing l from zero (the same value as the full
-  // product: the skipped terms are exact zeros); FFMA2 on column pairs (the pair's extra term
-  // S(l, l-1) of an odd l is an exact zero too).  Rows l >= pw of S_b are zero.
+  // product: the skipped terms are exact zeros); one 16-byte load feeds two FFMA2 on column pairs
+  // (the quad's extra terms S(l, j < l) are exact zeros too).  Rows l >= pw of S_b are zero.
   if (t < nrows) {
     float* row = s.L + t * kLd + c0;
     const float* Sf = s.u.Sf[t / kBR];
@@ -595,8 +595,11 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     for (int l = 0; l < 32; ++l) {
       const float2 ql = make_float2(q[l], q[l]);
 #pragma unroll
-      for (int j2 = l / 2; j2 < 16; ++j2)
-        y[j2] = ffma2(ql, *reinterpret_cast<const float2*>(Sf + l * kLdS + 2 * j2), y[j2]);
+      for (int j4 = l / 4; j4 < 8; ++j4) {  // from the quad holding column l (S_b(l, j < l) = 0)
+        const float4 s4 = *reinterpret_cast<const float4*>(Sf + l * kLdS + 4 * j4);
+        y[2 * j4] = ffma2(ql, make_float2(s4.x, s4.y), y[2 * j4]);
+        y[2 * j4 + 1] = ffma2(ql, make_float2(s4.z, s4.w), y[2 * j4 + 1]);
+      }
     }
 #pragma unroll
     for (int j2 = 0; j2 < 16; ++j2) {
