@@ -75,7 +75,14 @@ struct Context {
   // other SMs).  The critical stream waits for it right after the leaf.
   cudaStream_t s_la = nullptr;
   cudaEvent_t ev_la[64] = {}, ev_la_fork[64] = {};
-  int la_max_w = 512;  // env TCQR_LOOKAHEAD_W (0: off); measured: 1024 and up lose (the tail outlasts the leaf)
+  static constexpr int kLaPool = 1024;
+  cudaEvent_t ev_blk[kLaPool] = {};  // look-ahead column blocks (reset per factorization)
+  int la_ev_next = 0;
+  // env TCQR_LOOKAHEAD_W (0: off).  Measured at config 3 (ms per factor, la_sms 10 / 20): 512:
+  // 43.9 / 45.6, 1024: 46.9 / 46.6, 2048: 54.6 / 49.7, 4096: 69.8 / 56.9 -- deferred blocks of
+  // wider nodes run at 10-20 SMs' throughput and the critical path soon waits for them (and
+  // their CTAs delay the critical persistent GEMMs), where the full-width update takes 0.1-0.3 ms
+  int la_max_w = 512;
   int la_sms = 10;      // env TCQR_LA_SMS (the short-K update runs two CTAs per SM)
   int leaf_reserve = 10;  // env TCQR_LEAF_RESERVE: SMs the leaf beside a look-ahead leaves free
   // Across ranks: a split node's R12 allreduce in column chunks of ar_chunk on s_comm, each
@@ -171,6 +178,11 @@ struct FactorWs {
   float* R2 = nullptr;           // re-orthogonalization: R of the second pass (n x n)
   float* Rt = nullptr;           // re-orthogonalization: R2 * R1 staging (n x n)
   unsigned long long* ltag = nullptr;  // whole-leaf kernel: tagged reduction words
+  // look-ahead nodes: R12 (scaled FP16, ld round_up(h, 8)) and its column scales, one slot per
+  // recursion depth (a node's deferred column blocks are all consumed before the next node of the
+  // same depth starts: they lie inside the node's own columns)
+  __half* la_r12h[64] = {};
+  float* la_s2[64] = {};
   unsigned leaf_tags[1] = {0};   // leaf reductions since ltag was zeroed (the tags used so far)
   // NEXT-4 FP16 split (cfg.fp16_split): low halves of the shadow and of R12, two more R12 stagings
   __half* Ql = nullptr;     // ld ldh, like Qh
@@ -202,6 +214,30 @@ static void plan_factor_ws(Arena& a, long long m, long long n, int nranks, Facto
   w.iws = a.take<int>((size_t)w.iws_cap);
   w.cmax = a.take<unsigned int>((size_t)n + 64);
   w.ltag = a.take<unsigned long long>(leaf_tag_words());
+  {
+    // per-depth maxima of (h, w2) over the look-ahead candidates (cutoff < w <= la_max_w)
+    long long hm[64] = {}, wm[64] = {};
+    const int cut = g_ctx.cfg.cutoff, lam = g_ctx.la_max_w;
+    std::vector<std::pair<int, int>> st{{(int)n, 0}};
+    while (!st.empty()) {
+      const int wd = st.back().first, d = st.back().second;
+      st.pop_back();
+      if (wd <= cut || d >= 64) continue;
+      const int h = split_point(wd);
+      if (wd <= lam) {
+        hm[d] = std::max<long long>(hm[d], round_up(h, 8));
+        wm[d] = std::max<long long>(wm[d], wd - h);
+      }
+      st.push_back({h, d + 1});
+      st.push_back({wd - h, d + 1});
+    }
+    if (nranks == 1)
+      for (int d = 0; d < 64; ++d)
+        if (hm[d] > 0) {
+          w.la_r12h[d] = a.take<__half>((size_t)(hm[d] * wm[d]) + 64);
+          w.la_s2[d] = a.take<float>((size_t)wm[d] + 64);
+        }
+  }
   w.pipeR = a.take<float>(32 * 32 * 32);
   w.pipeS = a.take<float>(32 * 32 * 32);
   if (nranks > 1) {
@@ -665,8 +701,12 @@ struct FactorJob {
   FactorWs* ws;
   StreamPlan* sp = nullptr;
   int depth = 0;  // recursion depth of the current rgs call (fork / join event slot)
-  cudaEvent_t la_pending = nullptr;  // look-ahead update to wait for after the next leaf
-  bool la_leaf = false;  // this leaf runs beside a look-ahead update (on la_sms SMs)
+  // look-ahead: column blocks [a, b) whose deferred K4 update runs on s_la, done at ev
+  struct LaBlk {
+    int a, b;
+    cudaEvent_t ev;
+  };
+  std::vector<LaBlk> la;
 };
 
 // The compute stream waits for every chunk overlapping columns [c0, c1).
@@ -750,6 +790,22 @@ static int leaf_tsqr(FactorJob& J, int c0, int w, bool need_h) {
   return chunk_done(J, c0, w);
 }
 
+// Order `st` after the deferred look-ahead updates of columns [a, b); on the critical stream the
+// blocks are then consumed (every later operation on it is ordered after them).
+static int la_wait(FactorJob& J, int a, int b, cudaStream_t st) {
+  Context& c = g_ctx;
+  const bool crit = st == c.stream;
+  size_t k = 0;
+  for (size_t i = 0; i < J.la.size(); ++i) {
+    const FactorJob::LaBlk& x = J.la[i];
+    const bool hit = x.a < b && a < x.b;
+    if (hit) CK(cudaStreamWaitEvent(st, x.ev, 0));
+    if (!(hit && crit)) J.la[k++] = x;
+  }
+  J.la.resize(k);
+  return 0;
+}
+
 // Replicated leaf across ranks (cfg.leaf_kernel == 1, P * mmax rows fit one co-resident K2L grid):
 // the P ranks' rows of the leaf are allgathered (one collective, zero rows padding every rank to
 // mmax), every rank factors the whole leaf with the one-GPU whole-leaf kernel (identical inputs
@@ -815,18 +871,10 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   Context& c = g_ctx;
   FactorWs& ws = *J.ws;
   const int m = J.m;
-  if (J.la_pending && w <= c.cfg.cutoff) {
-    // the first leaf after a look-ahead split touches only the columns updated on the critical
-    // stream; everything after it waits for the rest of that update
-    cudaEvent_t e = J.la_pending;
-    J.la_pending = nullptr;
-    J.la_leaf = true;
-    const int rc = rgs(J, c0, w, need_h);
-    J.la_leaf = false;
-    CK(cudaStreamWaitEvent(c.stream, e, 0));
-    return rc;
-  }
   float* Qc = J.Q + (long long)c0 * J.ldq;
+  // a leaf (or the FP32 path below) reads and writes all its columns: the deferred look-ahead
+  // updates of those columns come first
+  if (w <= c.cfg.cutoff) CKR(la_wait(J, c0, c0 + w, c.stream));
   if (c.rep_mmax > 0 && c.nranks > 1 && w <= 128 && w <= c.cfg.cutoff && !J.sp) {
     need_cols(J, c0, c0 + w);
     return leaf_replicated(J, c0, w, need_h);
@@ -843,7 +891,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     PROF(TCQR_K2_LEAF, 2.0 * m * w * w, 8.0 * m * w + (need_h ? 2.0 * m * w : 0.0),
          e = leaf_fused(m, w, Qc, J.ldq, need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, ws.ldh,
                         J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0, c.d_status, ws.ltag,
-                        ws.leaf_tags, c.num_sms - (J.la_leaf ? c.leaf_reserve : 0), c.stream));
+                        ws.leaf_tags, c.num_sms - (J.la.empty() ? 0 : c.leaf_reserve), c.stream));
     if (e == cudaSuccess) {
       if (need_h) CKR(emit_q_lo(J, c0, w));
       return chunk_done(J, c0, w);
@@ -872,6 +920,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
       __half* A2h = ws.Qh + (long long)p0 * ws.ldh;
       CK(cudaEventRecord(c.ev_fork[J.depth], c.stream));
       CK(cudaStreamWaitEvent(c.s_side, c.ev_fork[J.depth], 0));
+      CKR(la_wait(J, p0, p0 + w2, c.s_side));  // ancestors' deferred updates of A2
       CK(cast_scale(m, w2, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling, c.d_status,
                     p0, ws.cmax + p0, c.s_side));
       if (c.cfg.fp16_split && ws.Ql)
@@ -908,6 +957,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
         __half* A2h = ws.Qh + (long long)p0 * ws.ldh;
         float* Tp = ws.T + (long long)off * h;
         __half* R12hp = ws.R12h + (long long)off * ldh2;
+        CKR(la_wait(J, p0, p0 + wp, c.stream));
         if (!side)
           PROF(TCQR_K1_CAST, 0, 6.0 * m * wp,
                CK(cast_scale(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling,
@@ -947,9 +997,23 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
           });
           continue;
         }
+        // look-ahead (one rank, device path): only the columns of the right subtree's first
+        // leaf-level subtree (L) are updated on the critical stream; the rest of the K4 update
+        // runs in leaf-wide column blocks on s_la (la_sms SMs, low priority) beside the next
+        // leaves, each block with its own event, waited on where its columns are next touched
+        // (la_wait).  R12 and its scales go to the depth's own slot: the deferred blocks read
+        // them while deeper nodes write theirs.
+        int L = w2;
+        while (L > c.cfg.cutoff) L = split_point(L);
+        const int dd = J.depth, lab = c.cfg.cutoff;
+        const int nblk = (wp - L + lab - 1) / lab;
+        const bool la = side && c.nranks == 1 && w <= c.la_max_w && L < wp && off == 0 &&
+                        dd < 64 && ws.la_r12h[dd] && c.la_ev_next + nblk <= Context::kLaPool;
+        __half* R12x = la ? ws.la_r12h[dd] : R12hp;
+        float* s2x = la ? ws.la_s2[dd] : ws.inv_s2 + p0;
         if (c.nranks == 1) {
           // one rank: the split-K reduction runs fused with the finalize
-          const R12Finalize fin{Rblk + (long long)off * J.ldr, J.ldr, R12hp, ldh2, ws.inv_s2 + p0,
+          const R12Finalize fin{Rblk + (long long)off * J.ldr, J.ldr, R12x, ldh2, s2x,
                                 c.cfg.col_scaling};
           PROF(TCQR_K3_TN, 2.0 * m * h * wp, 2.0 * m * (h + wp) + 14.0 * h * wp,
                CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, Tp, h, ws.inv_s + p0, ws.P,
@@ -993,22 +1057,19 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
                CK(r12_finalize(h, wp, Tp, h, Rblk + (long long)off * J.ldr, J.ldr, R12hp, ldh2,
                                ws.inv_s2 + p0, c.cfg.col_scaling, c.stream)));
         }
-        // look-ahead: L = width of the right subtree's first leaf-level subtree
-        int L = w2;
-        while (L > c.cfg.cutoff) L = split_point(L);
-        if (side && c.nranks == 1 && w <= c.la_max_w && L < wp && J.depth < 64) {
-          const int d = J.depth;
-          CK(cudaEventRecord(c.ev_la_fork[d], c.stream));
-          CK(cudaStreamWaitEvent(c.s_la, c.ev_la_fork[d], 0));
-          CK(tc_gemm_nn_update(m, h, wp - L, A1h, ws.ldh, R12hp + (long long)L * ldh2, ldh2,
-                               A2p + (long long)L * J.ldq, J.ldq, ws.inv_s2 + p0 + L, c.la_sms,
-                               c.s_la));
-          CK(cudaEventRecord(c.ev_la[d], c.s_la));
-          // the casts the right subtree forks read those columns
-          CK(cudaStreamWaitEvent(c.s_side, c.ev_la[d], 0));
-          CK(tc_gemm_nn_update(m, h, L, A1h, ws.ldh, R12hp, ldh2, A2p, J.ldq, ws.inv_s2 + p0,
-                               c.num_sms, c.stream));
-          J.la_pending = c.ev_la[d];
+        if (la) {
+          CK(tc_gemm_nn_update(m, h, L, A1h, ws.ldh, R12x, ldh2, A2p, J.ldq, s2x, c.num_sms,
+                               c.stream));
+          CK(cudaEventRecord(c.ev_la_fork[dd], c.stream));
+          CK(cudaStreamWaitEvent(c.s_la, c.ev_la_fork[dd], 0));
+          for (int j = L; j < wp; j += lab) {
+            const int wb = std::min(lab, wp - j);
+            CK(tc_gemm_nn_update(m, h, wb, A1h, ws.ldh, R12x + (long long)j * ldh2, ldh2,
+                                 A2p + (long long)j * J.ldq, J.ldq, s2x + j, c.la_sms, c.s_la));
+            cudaEvent_t ev = c.ev_blk[c.la_ev_next++];
+            CK(cudaEventRecord(ev, c.s_la));
+            J.la.push_back({p0 + j, p0 + j + wb, ev});
+          }
         } else {
           PROF(TCQR_K4_NN, 2.0 * m * h * wp, 2.0 * m * h + 2.0 * h * wp + 8.0 * m * wp,
                CK(tc_gemm_nn_update(m, h, wp, A1h, ws.ldh, R12hp, ldh2, A2p, J.ldq,
@@ -1072,13 +1133,17 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
   PROF(TCQR_COPY, 0, 8.0 * m * n, CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream)));
   FactorJob J{m, n, Q, (long long)m, R, (long long)n, &ws};
   const bool need_h = n > c.cfg.cutoff;
+  c.la_ev_next = 0;
   CKR(rgs(J, 0, n, need_h));
+  CKR(la_wait(J, 0, n, c.stream));
   CK(zero_lower(n, R, n, c.stream));
   if (c.cfg.reorth && ws.R2) {
     // NEXT-1: a second QR of Q itself; Q <- Q2, R <- R2 R1.
     CK(cudaMemsetAsync(ws.R2, 0, sizeof(float) * (size_t)n * n, c.stream));
     FactorJob J2{m, n, Q, (long long)m, ws.R2, (long long)n, &ws};
+    c.la_ev_next = 0;
     CKR(rgs(J2, 0, n, need_h));
+    CKR(la_wait(J2, 0, n, c.stream));
     CK(zero_lower(n, ws.R2, n, c.stream));
     PROF(TCQR_TRINV, (double)n * n * n / 3.0, 12.0 * n * n,
          CK(trmm_upper(n, ws.R2, n, R, n, ws.Rt, n, c.stream)));
@@ -1271,6 +1336,10 @@ static int finalize_ctx() {
     if (c.ev_la_fork[i]) cudaEventDestroy(c.ev_la_fork[i]);
     c.ev_fork[i] = c.ev_join[i] = c.ev_la[i] = c.ev_la_fork[i] = nullptr;
   }
+  for (int i = 0; i < Context::kLaPool; ++i) {
+    if (c.ev_blk[i]) cudaEventDestroy(c.ev_blk[i]);
+    c.ev_blk[i] = nullptr;
+  }
   if (c.s_h2d) cudaStreamDestroy(c.s_h2d);
   if (c.s_d2h) cudaStreamDestroy(c.s_d2h);
   c.s_h2d = c.s_d2h = nullptr;
@@ -1331,6 +1400,9 @@ static int init_ctx(int device, void* cuda_stream, const void* nccl_unique_id, i
         cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c.ev_la[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c.ev_la_fork[i], cudaEventDisableTiming) != cudaSuccess)
+      return TCQR_ERR_CUDA;
+  for (int i = 0; i < Context::kLaPool; ++i)
+    if (cudaEventCreateWithFlags(&c.ev_blk[i], cudaEventDisableTiming) != cudaSuccess)
       return TCQR_ERR_CUDA;
   {
     const char* e = getenv("TCQR_CAST_OVERLAP");
