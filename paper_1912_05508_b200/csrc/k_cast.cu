@@ -7,6 +7,8 @@
 #include <cooperative_groups.h>
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -652,6 +654,25 @@ __global__ void __launch_bounds__(256, 1) trmm_upper_big(int n, const float* __r
       const int r = i0 + tx * 8 + x, c = j0 + ty * 8 + y;
       if (r < n && c < n) C[r + (long long)c * ldc] = (y & 1) ? acc[x][y >> 1].y : acc[x][y >> 1].x;
     }
+}
+
+// X <- I - X (n x n, column-major): NEXT-1's R2 turned into the small correction I - R2 of
+// R2 R1 = R1 - (I - R2) R1 (the tensor-core form of the product, tcqr.cu reorth_product_tc).
+__global__ void eye_minus_kernel(int n, float* __restrict__ X, long long ldx) {
+  const long long total = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    float* p = X + i + (long long)j * ldx;
+    *p = (i == j ? 1.f : 0.f) - *p;
+  }
+}
+
+cudaError_t eye_minus(int n, float* X, long long ldx, cudaStream_t st) {
+  const long long total = (long long)n * n;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+  eye_minus_kernel<<<std::max(grid, 1), 256, 0, st>>>(n, X, ldx);
+  return cudaGetLastError();
 }
 
 cudaError_t trmm_upper(int n, const float* A, long long lda, const float* B, long long ldb,

@@ -53,6 +53,8 @@ cudaError_t copy_validate(int m, int n, const float* A, long long lda, float* Q,
 cudaError_t copy_block(int h, int w, const float* S, long long lds, float* D, long long ldd,
                        cudaStream_t st);
 // C = A * B for upper-triangular A, B (n x n, FP32, column-major); C upper triangular.
+// X <- I - X (n x n).
+cudaError_t eye_minus(int n, float* X, long long ldx, cudaStream_t st);
 cudaError_t trmm_upper(int n, const float* A, long long lda, const float* B, long long ldb,
                        float* C, long long ldc, cudaStream_t st);
 // Zero the strictly lower triangle of an n x n matrix (ld).

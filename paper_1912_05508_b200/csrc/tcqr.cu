@@ -1145,10 +1145,37 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
     CKR(rgs(J2, 0, n, need_h));
     CKR(la_wait(J2, 0, n, c.stream));
     CK(zero_lower(n, ws.R2, n, c.stream));
-    PROF(TCQR_TRINV, (double)n * n * n / 3.0, 12.0 * n * n,
-         CK(trmm_upper(n, ws.R2, n, R, n, ws.Rt, n, c.stream)));
-    CK(cudaMemcpyAsync(R, ws.Rt, sizeof(float) * (size_t)n * n, cudaMemcpyDeviceToDevice,
-                       c.stream));
+    const long long n8 = round_up(n, 8);
+    if (n % 8 == 0 && ws.ldh >= 2 * n8) {
+      // R2 R1 = R1 - (I - R2) R1 on the tensor cores, in place on R: I - R2 is small (R2 = I +
+      // O(||Q1'Q1 - I||)), so with both operands split into FP16 hi + lo halves (A: no scaling,
+      // |I - R2| < 1; R1: the per-column power-of-two range guard) and three MMAs per tile
+      // (lo x lo dropped) the correction carries ~2^-22 relative error on a term ~1e-3 of R:
+      // below FP32 rounding of R.  Exact inputs stay exact (R2 = I gives R = R1 bitwise).
+      // Buffers: the FP16 shadow Qh (free once both passes are done) holds I - R2's halves,
+      // Rt holds R1's; the dense product's lower triangle is exactly zero.
+      __half* Ah = ws.Qh;
+      __half* Al = ws.Qh + n8 * n;
+      __half* Bh = reinterpret_cast<__half*>(ws.Rt);
+      __half* Bl = Bh + n8 * n;
+      PROF(TCQR_TRINV, 6.0 * n * n * n, 12.0 * n * n, {
+        CK(eye_minus(n, ws.R2, n, c.stream));
+        CK(cast_scale(n, n, ws.R2, n, Ah, n8, ws.inv_s, 0, nullptr, 0, nullptr, c.stream));
+        CK(cast_lo(n, n, ws.R2, n, Ah, n8, ws.inv_s, Al, n8, c.stream));
+        CK(cast_scale(n, n, R, n, Bh, n8, ws.inv_s2, c.cfg.col_scaling, nullptr, 0, ws.cmax,
+                      c.stream));
+        CK(cast_lo(n, n, R, n, Bh, n8, ws.inv_s2, Bl, n8, c.stream));
+        CK(tc_gemm_nn_update(n, n, n, Ah, n8, Bh, n8, R, n, ws.inv_s2, c.num_sms, c.stream));
+        CK(tc_gemm_nn_update(n, n, n, Ah, n8, Bl, n8, R, n, ws.inv_s2, c.num_sms, c.stream));
+        CK(tc_gemm_nn_update(n, n, n, Al, n8, Bh, n8, R, n, ws.inv_s2, c.num_sms, c.stream));
+        CK(zero_lower(n, R, n, c.stream));
+      });
+    } else {
+      PROF(TCQR_TRINV, (double)n * n * n / 3.0, 12.0 * n * n,
+           CK(trmm_upper(n, ws.R2, n, R, n, ws.Rt, n, c.stream)));
+      CK(cudaMemcpyAsync(R, ws.Rt, sizeof(float) * (size_t)n * n, cudaMemcpyDeviceToDevice,
+                         c.stream));
+    }
   }
   CKR(allreduce_min_i32(c.d_status));
   return 0;
