@@ -690,6 +690,13 @@ struct StreamPlan {
   std::vector<cudaEvent_t> ev_fin;   // chunk j final
   float* hQ = nullptr;               // host outputs (ld m and ld n)
   float* hR = nullptr;
+  // deferred split-node updates (K1 + K3 + K4 of one node on one chunk of its A2), run when the
+  // recursion first touches the chunk, in registration order (an ancestor's before a descendant's)
+  struct DeferOp {
+    int nc0, h, p0, p1;
+  };
+  std::vector<DeferOp> defer;
+  bool flushing = false;
 };
 
 struct FactorJob {
@@ -710,7 +717,7 @@ struct FactorJob {
 };
 
 // The compute stream waits for every chunk overlapping columns [c0, c1).
-static void need_cols(FactorJob& J, int c0, int c1) {
+static void need_cols_raw(FactorJob& J, int c0, int c1) {
   StreamPlan* sp = J.sp;
   if (!sp) return;
   for (size_t j = 0; j < sp->a.size(); ++j)
@@ -718,6 +725,26 @@ static void need_cols(FactorJob& J, int c0, int c1) {
       cudaStreamWaitEvent(g_ctx.stream, sp->ev_in[j], 0);
       sp->waited[j] = 1;
     }
+}
+static int exec_deferred(FactorJob& J, const StreamPlan::DeferOp& op);
+// The compute stream waits for the chunks overlapping [c0, c1) and first runs the deferred
+// split-node updates of those columns (streamed host path).
+static int need_cols(FactorJob& J, int c0, int c1) {
+  StreamPlan* sp = J.sp;
+  if (!sp) return 0;
+  if (!sp->flushing && !sp->defer.empty()) {
+    sp->flushing = true;
+    std::vector<StreamPlan::DeferOp> run, keep;
+    for (const auto& op : sp->defer) (op.p0 < c1 && c0 < op.p1 ? run : keep).push_back(op);
+    sp->defer.swap(keep);
+    int rc = 0;
+    for (const auto& op : run)
+      if (!rc) rc = exec_deferred(J, op);
+    sp->flushing = false;
+    if (rc) return rc;
+  }
+  need_cols_raw(J, c0, c1);
+  return 0;
 }
 
 // After the subtree on [c0, c0+w): if it is a chunk, ship its Q columns and R columns (all n rows:
@@ -867,6 +894,33 @@ static int plan_leaf_replication(int m) {
   return 0;
 }
 
+// One deferred split-node update (see StreamPlan::DeferOp): Alg. 2 lines 8-9 of node
+// [nc0, nc0 + 2h) restricted to the A2 chunk [p0, p1): K1 cast, K3 split-K TN with the fused
+// finalize (R block rows [nc0, nc0 + h) of those columns), K4 update.  Staging (T, R12h) at
+// offset 0: the ops run one after another on the compute stream.
+static int exec_deferred(FactorJob& J, const StreamPlan::DeferOp& op) {
+  Context& c = g_ctx;
+  FactorWs& ws = *J.ws;
+  const int m = J.m, h = op.h, p0 = op.p0, wp = op.p1 - op.p0;
+  need_cols_raw(J, p0, op.p1);
+  float* A2p = J.Q + (long long)p0 * J.ldq;
+  __half* A2h = ws.Qh + (long long)p0 * ws.ldh;
+  const __half* A1h = ws.Qh + (long long)op.nc0 * ws.ldh;
+  const long long ldh2 = round_up(h, 8);
+  PROF(TCQR_K1_CAST, 0, 6.0 * m * wp,
+       CK(cast_scale(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling, c.d_status,
+                     p0, ws.cmax + p0, c.stream)));
+  const R12Finalize fin{J.R + op.nc0 + (long long)p0 * J.ldr, J.ldr, ws.R12h, ldh2,
+                        ws.inv_s2 + p0, c.cfg.col_scaling};
+  PROF(TCQR_K3_TN, 2.0 * m * h * wp, 2.0 * m * (h + wp) + 14.0 * h * wp,
+       CK(tc_gemm_tn(m, h, wp, A1h, ws.ldh, A2h, ws.ldh, ws.T, h, ws.inv_s + p0, ws.P, ws.p_cap,
+                     c.num_sms, c.stream, &fin)));
+  PROF(TCQR_K4_NN, 2.0 * m * h * wp, 2.0 * m * h + 2.0 * h * wp + 8.0 * m * wp,
+       CK(tc_gemm_nn_update(m, h, wp, A1h, ws.ldh, ws.R12h, ldh2, A2p, J.ldq, ws.inv_s2 + p0,
+                            c.num_sms, c.stream)));
+  return 0;
+}
+
 static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   Context& c = g_ctx;
   FactorWs& ws = *J.ws;
@@ -876,17 +930,17 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   // updates of those columns come first
   if (w <= c.cfg.cutoff) CKR(la_wait(J, c0, c0 + w, c.stream));
   if (c.rep_mmax > 0 && c.nranks > 1 && w <= 128 && w <= c.cfg.cutoff && !J.sp) {
-    need_cols(J, c0, c0 + w);
+    CKR(need_cols(J, c0, c0 + w));
     return leaf_replicated(J, c0, w, need_h);
   }
   if (c.cfg.leaf_kernel && c.nranks > 1 && w <= 128 && w <= c.cfg.cutoff && !J.sp) {
-    need_cols(J, c0, c0 + w);
+    CKR(need_cols(J, c0, c0 + w));
     const int rc = leaf_tsqr(J, c0, w, need_h);
     if (rc != 1) return rc;
   }
   if (c.cfg.leaf_kernel && c.nranks == 1 && w <= 128 && w <= c.cfg.cutoff) {
     // the whole leaf (every node below the cutoff) in one cooperative launch (k_leaf.cu)
-    need_cols(J, c0, c0 + w);
+    CKR(need_cols(J, c0, c0 + w));
     cudaError_t e = cudaErrorNotSupported;
     PROF(TCQR_K2_LEAF, 2.0 * m * w * w, 8.0 * m * w + (need_h ? 2.0 * m * w : 0.0),
          e = leaf_fused(m, w, Qc, J.ldq, need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, ws.ldh,
@@ -901,7 +955,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   }
   if (w <= 32) {
     bool wrote_h = false;
-    need_cols(J, c0, c0 + w);
+    CKR(need_cols(J, c0, c0 + w));
     CKR(panel(ws, m, w, Qc, J.ldq, J.R + c0 + (long long)c0 * J.ldr, J.ldr, c0,
               need_h ? ws.Qh + (long long)c0 * ws.ldh : nullptr, &wrote_h));
     if (wrote_h) {
@@ -952,7 +1006,14 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
       }
       for (auto& pc : pieces) {
         const int p0 = pc.first, wp = pc.second - pc.first, off = p0 - (c0 + h);
-        need_cols(J, p0, p0 + wp);
+        if (J.sp && c.nranks == 1 && !(c.cfg.fp16_split && ws.Ql)) {
+          // streamed host path: this piece's update waits until the recursion first touches
+          // its chunk, so the right subtree starts on the chunks that have arrived while the
+          // later ones are still crossing PCIe
+          J.sp->defer.push_back({c0, h, p0, p0 + wp});
+          continue;
+        }
+        CKR(need_cols(J, p0, p0 + wp));
         float* A2p = J.Q + (long long)p0 * J.ldq;
         __half* A2h = ws.Qh + (long long)p0 * ws.ldh;
         float* Tp = ws.T + (long long)off * h;
@@ -1077,7 +1138,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
         }
       }
     } else if (c.nranks == 1) {
-      need_cols(J, c0 + h, c0 + w);
+      CKR(need_cols(J, c0 + h, c0 + w));
       // one cooperative launch: R12 = Q1' A2 (deterministic), R block, A2 -= Q1 R12
       cudaError_t e = cudaErrorNotSupported;
       PROF(TCQR_K2B_TN, 4.0 * m * h * w2, 8.0 * m * h + 12.0 * m * w2,
@@ -1095,7 +1156,7 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
              CK(f32_nn_update(m, h, w2, Qc, J.ldq, ws.T, A2, J.ldq, c.stream)));
       }
     } else {
-      need_cols(J, c0 + h, c0 + w);
+      CKR(need_cols(J, c0 + h, c0 + w));
       PROF(TCQR_K2B_TN, 2.0 * m * h * w2, 4.0 * m * (h + w2),
            CK(f32_tn(m, h, w2, Qc, J.ldq, A2, J.ldq, ws.T, ws.P, ws.p_cap, c.num_sms,
                      c.stream)));
@@ -1840,8 +1901,8 @@ static int factor_host_streamed(int m, int n, const float* A, long long lda, flo
   for (size_t j = 0; j < nc; ++j)
     for (int col = sp.a[j]; col < sp.b[j]; ++col)
       memset(R + (long long)col * n + sp.b[j], 0, sizeof(float) * (size_t)(n - sp.b[j]));
+  if (rc == 0) rc = need_cols(J, 0, n);  // every validation has finished before the status is read
   if (rc == 0) {
-    need_cols(J, 0, n);  // every validation has finished before the status is read
     CK(zero_lower(n, dR, n, c.stream));
     rc = read_status();
   }
