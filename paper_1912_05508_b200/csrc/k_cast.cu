@@ -142,10 +142,12 @@ __global__ void __launch_bounds__(256) cast_pass2_kernel(int m, const float* __r
 // memory (max is order-independent: the same s as the two-kernel path, bit for bit); pass 2 casts
 // from the registers.  One launch and one read of X instead of memset + colmax + cast_pass2.
 template <int V>
-__global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* __restrict__ X,
-                                                           long long ldx, __half* __restrict__ Xh,
+__global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* X, long long ldx,
+                                                           __half* __restrict__ Xh,
                                                            long long ldh, float* __restrict__ inv_s,
-                                                           int scaling, int* status, int col_base) {
+                                                           int scaling, int* status, int col_base,
+                                                           const float* __restrict__ src,
+                                                           long long lds) {
   namespace cg = cooperative_groups;
   constexpr int RPC = 256 * 4 * V;  // rows per CTA
   __shared__ float red[32];
@@ -154,7 +156,10 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* _
   const int j = blockIdx.y;
   const int rank = (int)cluster.block_rank();
   const long long r0 = (long long)rank * RPC;
-  const float* x = X + (long long)j * ldx;
+  // copy-cast (src non-null): the column is read from the factorization's input and its FP32
+  // copy written to X on the way (the first touch of these columns: no separate copy pass)
+  const float* x = src ? src + (long long)j * lds : X + (long long)j * ldx;
+  float* xc = src ? const_cast<float*>(X) + (long long)j * ldx : nullptr;
   // every CTA of the cluster must be running before any CTA touches a peer's shared memory: a
   // relaxed arrive now, the matching wait just before the distributed stores (it overlaps the
   // HBM loads below)
@@ -172,6 +177,19 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* _
       v[u].y = q + 1 < m ? x[q + 1] : 0.f;
       v[u].z = q + 2 < m ? x[q + 2] : 0.f;
       v[u].w = q + 3 < m ? x[q + 3] : 0.f;
+    }
+  }
+  if (xc) {
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const long long q = r0 + 4LL * (threadIdx.x + 256 * u);
+      if (q + 3 < m) {
+        *reinterpret_cast<float4*>(xc + q) = v[u];
+      } else {
+        if (q < m) xc[q] = v[u].x;
+        if (q + 1 < m) xc[q + 1] = v[u].y;
+        if (q + 2 < m) xc[q + 2] = v[u].z;
+      }
     }
   }
 #pragma unroll
@@ -217,7 +235,8 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* _
 template <int V>
 static cudaError_t launch_cast_cluster(int m, int w, const float* X, long long ldx, __half* Xh,
                                        long long ldh, float* inv_s, int scaling, int* status,
-                                       int col_base, int nchunks, cudaStream_t st) {
+                                       int col_base, int nchunks, cudaStream_t st,
+                                       const float* src, long long lds) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nchunks, w);
   cfg.blockDim = dim3(256);
@@ -230,13 +249,14 @@ static cudaError_t launch_cast_cluster(int m, int w, const float* X, long long l
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, cast_cluster_kernel<V>, m, X, ldx, Xh, ldh, inv_s, scaling, status,
-                            col_base);
+                            col_base, src, lds);
 }
 
 cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
                        float* inv_s, int scaling, int* status, int col_base, unsigned int* cmax,
-                       cudaStream_t st) {
+                       cudaStream_t st, const float* src, long long lds) {
   if (m <= 0 || w <= 0) return cudaSuccess;
+  if (src == X && lds == ldx) src = nullptr;  // in place: nothing to copy
   // Range guard with m <= 65536 (every config's local height): the cluster kernel at any width
   // (one HBM read; at config 3 it beat the per-column two-pass kernel for w >= 1024 as well:
   // K1 3.81 -> 3.57 ms per factor, profiles/r01_bench_cfg3_v14_*).  Otherwise few columns x many
@@ -248,8 +268,9 @@ cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, 
     use_cluster = ev ? atoi(ev) : 1;
   }
   const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
-                   ((ldh & 3) == 0) && ((reinterpret_cast<uintptr_t>(Xh) & 7) == 0);
-  if (use_cluster && vec && (scaling || status)) {
+                   ((ldh & 3) == 0) && ((reinterpret_cast<uintptr_t>(Xh) & 7) == 0) &&
+                   (!src || (((lds & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)));
+  if (use_cluster && vec && (scaling || status) && m <= 8 * 8192) {
     // 8192-row CTAs (8 float4 loads in flight per thread) by default: at config 3 K1 3.03 ->
     // 2.76 ms against 4096-row CTAs (profiles/r01_bench_cfg3_v19_*); env TCQR_CAST_V8=0 for those
     static int v8 = -1;
@@ -258,9 +279,15 @@ cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, 
       v8 = ev ? atoi(ev) : 1;
     }
     if (m <= 8 * 4096 && !v8) return launch_cast_cluster<4>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
-                                                     col_base, (m + 4095) / 4096, st);
-    if (m <= 8 * 8192) return launch_cast_cluster<8>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status,
-                                                     col_base, (m + 8191) / 8192, st);
+                                                     col_base, (m + 4095) / 4096, st, src, lds);
+    return launch_cast_cluster<8>(m, w, X, ldx, Xh, ldh, inv_s, scaling, status, col_base,
+                                  (m + 8191) / 8192, st, src, lds);
+  }
+  if (src) {  // the other casts read X: copy first
+    const cudaError_t e = cudaMemcpy2DAsync(const_cast<float*>(X), sizeof(float) * ldx, src,
+                                            sizeof(float) * lds, sizeof(float) * m, w,
+                                            cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
   }
   static int col_min = -1;  // per-column kernel from this width on (env TCQR_CAST_COL_MIN)
   if (col_min < 0) {

@@ -36,9 +36,11 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
 // Xh = fl16(X diag(s)); inv_s[j] = 1/s_j; status: atomicMin(1-based first non-finite column).
 // m <= 65536 with aligned pointers: one thread-block cluster per column (cmax unused).  Taller:
 // cmax = w uints of scratch for the split-row column max (may be null -> one CTA per column).
+// src non-null (copy-cast): the columns are read from src (ld lds), the factorization's input,
+// and their FP32 copy written to X in the same pass (first touch of those columns).
 cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, long long ldh,
                        float* inv_s, int scaling, int* status, int col_base, unsigned int* cmax,
-                       cudaStream_t st);
+                       cudaStream_t st, const float* src = nullptr, long long lds = 0);
 // NEXT-4 FP16 split: Xl = fl16(X diag(s) - Xh) (inv_s null: s = 1); dst += a + b.
 cudaError_t cast_lo(int m, int w, const float* X, long long ldx, const __half* Xh, long long ldh,
                     const float* inv_s, __half* Xl, long long ldl, cudaStream_t st);

@@ -714,6 +714,11 @@ struct FactorJob {
     cudaEvent_t ev;
   };
   std::vector<LaBlk> la;
+  // deferred input copy: Q columns [0, untouched) still hold nothing; their first touch reads the
+  // input src (ld lds) -- a node's K1 copy-cast of its A2, or the leftmost leaf's copy_validate
+  const float* src = nullptr;
+  long long lds = 0;
+  int untouched = 0;
 };
 
 // The compute stream waits for every chunk overlapping columns [c0, c1).
@@ -929,6 +934,13 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
   // a leaf (or the FP32 path below) reads and writes all its columns: the deferred look-ahead
   // updates of those columns come first
   if (w <= c.cfg.cutoff) CKR(la_wait(J, c0, c0 + w, c.stream));
+  if (w <= c.cfg.cutoff && J.untouched > c0) {
+    // the leftmost leaf: the last untouched input columns, copied (and validated) now
+    PROF(TCQR_COPY, 0, 8.0 * m * (J.untouched - c0),
+         CK(copy_validate(m, J.untouched - c0, J.src + (long long)c0 * J.lds, J.lds, Qc, J.ldq,
+                          c.d_status, c.stream, c0)));
+    J.untouched = c0;
+  }
   if (c.rep_mmax > 0 && c.nranks > 1 && w <= 128 && w <= c.cfg.cutoff && !J.sp) {
     CKR(need_cols(J, c0, c0 + w));
     return leaf_replicated(J, c0, w, need_h);
@@ -975,8 +987,11 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
       CK(cudaEventRecord(c.ev_fork[J.depth], c.stream));
       CK(cudaStreamWaitEvent(c.s_side, c.ev_fork[J.depth], 0));
       CKR(la_wait(J, p0, p0 + w2, c.s_side));  // ancestors' deferred updates of A2
+      const bool first = J.untouched >= p0 + w2;  // A2 never touched: copy-cast from the input
       CK(cast_scale(m, w2, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling, c.d_status,
-                    p0, ws.cmax + p0, c.s_side));
+                    p0, ws.cmax + p0, c.s_side, first ? J.src + (long long)p0 * J.lds : nullptr,
+                    J.lds));
+      if (first) J.untouched = p0;
       if (c.cfg.fp16_split && ws.Ql)
         CK(cast_lo(m, w2, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, ws.Ql + (long long)p0 * ws.ldh,
                    ws.ldh, c.s_side));
@@ -1019,10 +1034,13 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
         float* Tp = ws.T + (long long)off * h;
         __half* R12hp = ws.R12h + (long long)off * ldh2;
         CKR(la_wait(J, p0, p0 + wp, c.stream));
+        const bool first = !side && J.untouched >= p0 + wp;  // copy-cast from the input
+        if (first) J.untouched = p0;
         if (!side)
           PROF(TCQR_K1_CAST, 0, 6.0 * m * wp,
                CK(cast_scale(m, wp, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling,
-                             c.d_status, p0, ws.cmax + p0, c.stream)));
+                             c.d_status, p0, ws.cmax + p0, c.stream,
+                             first ? J.src + (long long)p0 * J.lds : nullptr, J.lds)));
         if (c.cfg.fp16_split && ws.Ql) {
           // NEXT-4: three MMAs per product on the hi/lo FP16 halves (lo x lo dropped)
           __half* A1l = ws.Ql + (long long)c0 * ws.ldh;
@@ -1191,8 +1209,12 @@ static int enqueue_factor(int m, int n, const float* A, long long lda, float* Q,
   ws.leaf_tags[0] = 0;
   CK(cudaMemsetAsync(ws.ltag, 0, sizeof(unsigned long long) * leaf_tag_words(), c.stream));
   CK(cudaMemsetAsync(ws.pipeR, 0xff, sizeof(float) * 32 * 32 * 32 * 2, c.stream));  // NaN
-  PROF(TCQR_COPY, 0, 8.0 * m * n, CK(copy_validate(m, n, A, lda, Q, m, c.d_status, c.stream)));
+  // the input copy A -> Q is deferred to each column's first touch (copy-casts of the leftmost
+  // path's A2 blocks, copy_validate of the leftmost leaf): no separate pass over A
   FactorJob J{m, n, Q, (long long)m, R, (long long)n, &ws};
+  J.src = A;
+  J.lds = lda;
+  J.untouched = n;
   const bool need_h = n > c.cfg.cutoff;
   c.la_ev_next = 0;
   CKR(rgs(J, 0, n, need_h));

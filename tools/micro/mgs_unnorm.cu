@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(128, 1) bench(const float* A, float* Q, float*
     for (int i = 0; i < BR / 4; ++i)
       *reinterpret_cast<float4*>(colb + 4 * i) = make_float4(x[2 * i].x, x[2 * i].y, x[2 * i + 1].x, x[2 * i + 1].y);
   __syncwarp();
-  if (V == 0) {
+  if (V == 0 || V >= 5) {
 #pragma unroll 1
     for (int k = 0; k < 32; ++k) {
 #pragma unroll
@@ -72,8 +72,10 @@ __global__ void __launch_bounds__(128, 1) bench(const float* A, float* Q, float*
       __syncwarp();
       qb[lane] = q0;
       qb[lane + 32] = q1;
-      L[w][k * LD + lane] = q0;
-      L[w][k * LD + lane + 32] = q1;
+      if (V == 0) {
+        L[w][k * LD + lane] = q0;
+        L[w][k * LD + lane + 32] = q1;
+      }
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < BR / 4; ++i) {
@@ -88,6 +90,10 @@ __global__ void __launch_bounds__(128, 1) bench(const float* A, float* Q, float*
 #pragma unroll
         for (int i = 0; i < BR / 4; ++i)
           *reinterpret_cast<float4*>(colb + 4 * i) = make_float4(x[2 * i].x, x[2 * i].y, x[2 * i + 1].x, x[2 * i + 1].y);
+      if (V == 5) {
+        L[w][k * LD + lane] = q0;
+        L[w][k * LD + lane + 32] = q1;
+      }
       __syncwarp();
     }
   } else {
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(128, 1) bench(const float* A, float* Q, float*
   __syncwarp();
   long long t1 = clock64();
   float* q = Q + ((long long)blockIdx.x * 4 + w) * BR * 32;
-  if (V == 0) {
+  if (V == 0 || V >= 5) {
     for (int j = 0; j < 32; ++j) q[j * BR + lane] = L[w][j * LD + lane], q[j * BR + lane + 32] = L[w][j * LD + lane + 32];
   } else {
     for (int i = 0; i < BR; ++i) q[lane * BR + i] = L[w][lane * LD + i];
@@ -237,6 +243,8 @@ int main() {
     run(bench<2>, "U2 projection form, c = d_j * (1 / d_k)");
     run(bench<3>, "U3 = U2 with R deferred past the loop");
     run(bench<4>, "U4 = U3 with c = d_j * rcp.approx(d_k)");
+    run(bench<5>, "U5 = U0 with the Q column stores after the update");
+    run(bench<6>, "U6 = U0 without the Q column stores (timing only)");
   }
   return 0;
 }
