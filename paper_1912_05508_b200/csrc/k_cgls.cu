@@ -261,7 +261,10 @@ __global__ void __launch_bounds__(256, 1) trinv_pair_dmma(int n, int b, const fl
   const int b1 = b;
   const int b2 = min(b, n - (i0 + b));
   if (b2 <= 0) return;
-  const int tm = blockIdx.x * TB, tn = blockIdx.y * TB;
+  // MODE 0's K range grows with the tile column (X22 is upper triangular): take the long tiles
+  // first so the short ones fill the tail wave (MODE 1's already come first: K shrinks with tm)
+  const int tm = blockIdx.x * TB;
+  const int tn = (MODE == 0 ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y) * TB;
   if (tm >= b1 || tn >= b2) return;
   double* Wp = W + (long long)p * b * b;  // ld = b
   const int K = (MODE == 0) ? b2 : b1;

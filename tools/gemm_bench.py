@@ -30,4 +30,7 @@ for h in shapes:
     fl = 2.0 * m * h * w2
     t1 = e[0].elapsed_time(e[1]) / reps
     t2 = e[1].elapsed_time(e[2]) / reps
-    print(f"h=w2={h:5d}: TN {t1*1e3:8.1f} us {fl/t1/1e9:7.1f} TF/s | NN {t2*1e3:8.1f} us {fl/t2/1e9:7.1f} TF/s")
+    nb = 2.0 * m * h + 2.0 * h * w2 + 8.0 * m * w2
+    tb = 2.0 * m * (h + w2)
+    print(f"h=w2={h:5d}: TN {t1*1e3:8.1f} us {fl/t1/1e9:7.1f} TF/s {tb/t1/1e6:7.0f} GB/s | "
+          f"NN {t2*1e3:8.1f} us {fl/t2/1e9:7.1f} TF/s {nb/t2/1e6:7.0f} GB/s")
