@@ -59,6 +59,8 @@ __device__ __forceinline__ void tile_of(int w, int tiles_m, int tiles_n, int& mb
   nb = l / gm;
 }
 
+__constant__ int nn_pre_all = 1;
+
 template <int BN, int MODE, int NBUF>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -186,9 +188,12 @@ __global__ void __launch_bounds__(192, 1)
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int ncol = min(BN, N - nb * BN), nch = (ncol + 31) / 32;
+      // PRE chunks of C in flight: every buffer is refilled as soon as its chunk's store has read
+      // it (env TCQR_NN_PRE_ALL=0: NBUF - 1 ahead, the buffer of chunk c - 1 refilled for c + 3)
+      const int pre = nn_pre_all ? NBUF : NBUF - 1;
       if (issuer) {
         bulk_wait_read<0>();  // the previous tile's stores have read their buffers
-        for (int c = 0; c < NBUF - 1 && c < nch; ++c) {
+        for (int c = 0; c < pre && c < nch; ++c) {
           mbar_arrive_expect_tx(&cfull[c], 16384);
           tma_load_2d(cbuf + c * 4096, &tmC, &cfull[c], mb * BM, nb * BN + 32 * c);
         }
@@ -217,13 +222,16 @@ __global__ void __launch_bounds__(192, 1)
         if (issuer) {
           tma_store_2d(&tmC, cb, mb * BM, col0);
           bulk_commit();
-          if (c + NBUF - 1 < nch) {
-            // buffer of chunk c+NBUF-1 was last used by chunk c-1, whose store must have read it
-            const int nbuf = (c + NBUF - 1) % NBUF;
-            bulk_wait_read<1>();
+          if (c + pre < nch) {
+            // the buffer of chunk c + pre was last used by chunk c + pre - NBUF (c or c - 1),
+            // whose store must have read it
+            const int nbuf = (c + pre) % NBUF;
+            if (pre == NBUF)
+              bulk_wait_read<0>();
+            else
+              bulk_wait_read<1>();
             mbar_arrive_expect_tx(&cfull[nbuf], 16384);
-            tma_load_2d(cbuf + nbuf * 4096, &tmC, &cfull[nbuf], mb * BM,
-                        nb * BN + 32 * (c + NBUF - 1));
+            tma_load_2d(cbuf + nbuf * 4096, &tmC, &cfull[nbuf], mb * BM, nb * BN + 32 * (c + pre));
           }
         }
       }
@@ -833,6 +841,12 @@ cudaError_t tc_gemm_nn_update(int m, int h, int w2, const __half* Qh, long long 
                               const __half* Bh, long long ldb, float* C, long long ldc,
                               const float* col_mult, int num_sms, cudaStream_t st) {
   if (m <= 0 || h <= 0 || w2 <= 0) return cudaSuccess;
+  static int pre_all = -1;
+  if (pre_all < 0) {
+    const char* e = getenv("TCQR_NN_PRE_ALL");
+    pre_all = e ? atoi(e) : 1;
+    if (pre_all != 1) cudaMemcpyToSymbol(nn_pre_all, &pre_all, sizeof(int));
+  }
   CUtensorMap ma, mb;
   if (!make_map_f16(&ma, Qh, m, h, ldq, 64, 64)) return cudaErrorInvalidValue;
   if (use_tc2() && h >= kTc2NnMinK && w2 >= 256) {
