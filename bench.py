@@ -392,10 +392,18 @@ def main():
         k = min(256, n)
         if M <= 262144:
             a_lead = A[:, :k].cpu().numpy().astype(np.float64)
-            _, r_o = rgs(a_lead)
+            q_o, r_o = rgs(a_lead)
             r_lead = R[:k, :k].cpu().numpy().astype(np.float64)
             q_lead = Q[:, :k].cpu().numpy().astype(np.float64)
+            # R's leading k rows over ALL columns: R = Q'A is unique, so rows 0..k-1 are Q_k' A
+            # with the oracle's Q_k of the leading columns (FP64 on the host, column chunks)
+            rows_o = np.empty((k, n))
+            for c0 in range(0, n, 2048):
+                c1 = min(n, c0 + 2048)
+                rows_o[:, c0:c1] = q_o.T @ A[:, c0:c1].cpu().numpy().astype(np.float64)
             parity = {f"R_lead{k}_rel_err_vs_oracle": r_rel_error(r_lead, r_o),
+                      f"R_rows{k}_all_cols_rel_err_vs_oracle": r_rel_error(
+                          R[:k, :].cpu().numpy().astype(np.float64), np.triu(rows_o)),
                       f"Q_lead{k}_orthogonality_f": float(
                           np.linalg.norm(q_lead.T @ q_lead - np.eye(k)) / np.sqrt(k))}
         else:

@@ -48,6 +48,20 @@ def _lead_block(A, R, k):
     return r_rel_error(R[:k, :k].cpu().numpy().astype(np.float64), r_o)
 
 
+def _lead_rows(A, R, k):
+    """R's leading k rows across ALL columns against the oracle: R = Q'A is unique, so its rows
+    0..k-1 are Q_k' A with Q_k the Q of the leading k columns (oracle RGS in FP64, then the FP64
+    product on the host, in column chunks)."""
+    q_o, _ = rgs(A[:, :k].cpu().numpy().astype(np.float64))
+    m, n = A.shape
+    r_o = np.empty((k, n))
+    for c0 in range(0, n, 2048):
+        c1 = min(n, c0 + 2048)
+        r_o[:, c0:c1] = q_o.T @ A[:, c0:c1].cpu().numpy().astype(np.float64)
+    r_o = np.triu(r_o)  # the strictly-lower part of the leading rows is zero in the exact R
+    return r_rel_error(R[:k, :].cpu().numpy().astype(np.float64), r_o)
+
+
 @pytest.mark.parametrize("kind,cond,seed", [("gaussian", 1, 2), ("geometric", 1e2, 3)])
 def test_config2_gates_vs_oracle(tq, kind, cond, seed):
     # BASELINE configs[1]: 16384 x 4096; the oracle runs at full size (~10-20 s on the host).
@@ -73,6 +87,9 @@ def test_config3_fullsize_properties(tq):
     assert bool(torch.all(torch.diagonal(R) > 0))
     assert float(torch.linalg.norm(torch.tril(R, -1))) == 0.0
     assert _lead_block(A, R, 256) <= 1e-2
+    # the leading 256 rows of R across all 16384 columns (4.2M entries: every split level's R12
+    # blocks contribute) against the oracle
+    assert _lead_rows(A, R, 256) <= 1e-2
 
 
 def test_config3_arithmetic_kappa1e3_r_gate(tq):
@@ -96,6 +113,7 @@ def test_config5_tall_skinny_multilevel_panel(tq):
     be, orth = _device_metrics(A, Q, R)
     assert be <= 5e-3 and orth <= 5e-2, (be, orth)
     assert _lead_block(A, R, 128) <= 1e-2
+    assert _lead_rows(A, R, 128) <= 1e-2
 
 
 @pytest.mark.parametrize("reorth", [0, 1])
