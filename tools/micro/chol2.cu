@@ -109,6 +109,75 @@ __global__ void chol(const double* G, const double* Rb, double* outR, float* out
     }
 }
 
+// E: the Cholesky split over four warps (warp w owns trailing rows [8w, 8w + 8), lane j = column
+// j, absolute row indices: no register shifting), one named barrier per step; the owner warp of
+// row k publishes R(k, :) (double-buffered) and 1/R(k,k); then the S_b substitution post-pass.
+__global__ void chol_coop(const double* G, const double* Rb, double* outR, float* outS, long long* clk) {
+  __shared__ double Rd[32 * 34 + 34];
+  __shared__ double rowbuf[2][32];
+  __shared__ double ris[32];
+  __shared__ float Sf[4][32 * 34];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double cw[8];
+#pragma unroll
+  for (int ii = 0; ii < 8; ++ii) {
+    const int r = 8 * warp + ii;
+    cw[ii] = (r <= lane) ? G[r * 32 + lane] : 0.0;
+  }
+  double r[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) r[j] = Rb[lane * 32 + j];
+  __syncthreads();
+  long long t0 = clock64();
+  bool okall = true;
+#pragma unroll 1
+  for (int k = 0; k < 32; ++k) {
+    const int o = k >> 3;
+    if (warp == o) {
+      double dv = 0.0;
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii) if (ii == (k & 7)) dv = cw[ii];
+      const double d = __shfl_sync(0xffffffffu, dv, k);
+      const bool ok = d > 0.0 && d <= 1.7976931348623157e308;
+      okall &= ok;
+      const double ri = ok ? rsqrt_nr(d) : 0.0;
+      const double rkj = lane == k ? d * ri : (lane > k ? dv * ri : 0.0);
+      rowbuf[k & 1][lane] = rkj;
+      Rd[k * 34 + lane] = rkj;
+      if (lane == 0) ris[k] = ri;
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    const double rk = rowbuf[k & 1][lane];
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) {
+      const int rr = 8 * warp + ii;
+      if (rr > k) cw[ii] = fma(-rowbuf[k & 1][rr], rk, cw[ii]);
+    }
+  }
+  asm volatile("bar.sync 2, 128;" ::: "memory");
+  long long t1 = clock64();
+  // S_b post-pass (as D): S(lane, k) = (R_b(lane, k) - sum_{l<k} S(lane, l) R(l, k)) / R(k, k)
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const double sk = r[k] * ris[k];
+    Sf[warp][lane * 34 + k] = (float)sk;
+#pragma unroll
+    for (int j = k + 1; j < 32; ++j) r[j] = fma(-sk, Rd[k * 34 + j], r[j]);
+  }
+  __syncthreads();
+  long long t2 = clock64();
+  if (threadIdx.x == 0) {
+    clk[6] = t1 - t0;
+    clk[7] = t2 - t1;
+  }
+  if (warp == 0)
+    for (int i = 0; i < 32; ++i) {
+      outR[i * 32 + lane] = Rd[i * 34 + lane];
+      outS[i * 32 + lane] = Sf[0][lane * 34 + i];
+    }
+  (void)okall;
+}
+
 int main() {
   double hG[1024], hRb[1024];
   // G = R_b' R_b + diag for a random upper-triangular R_b
@@ -129,12 +198,13 @@ int main() {
   double refR[1024], R[1024];
   float refS[1024], S[1024];
   const char* names[4] = {"A rolled fused (current)", "B rolled fused, triangular trips",
-                          "C Cholesky only, triangular trips + D post-pass S", "D post-pass S alone"};
-  for (int v = 0; v < 3; ++v) {
+                          "C Cholesky only, triangular trips + D post-pass S", "E four-warp Cholesky + D post-pass S"};
+  for (int v = 0; v < 4; ++v) {
     for (int rep = 0; rep < 3; ++rep) {
       if (v == 0) chol<0><<<1, 128>>>(G, Rb, oR, oS, c);
       if (v == 1) chol<1><<<1, 128>>>(G, Rb, oR, oS, c);
       if (v == 2) chol<2><<<1, 128>>>(G, Rb, oR, oS, c);
+      if (v == 3) chol_coop<<<1, 128>>>(G, Rb, oR, oS, c);
     }
     cudaDeviceSynchronize();
     long long hc[8];

@@ -167,12 +167,68 @@ __global__ void __launch_bounds__(256) t4(int m, int n, const float* __restrict_
   }
 }
 
+// T5: persistent, balanced: grid = CTAs of the resident wave; item = (64-column block, 1024-row
+// chunk) in column-block-major order, each CTA a contiguous item range (<= 2 column blocks), r
+// staged per chunk, per-(CTA, column block) partials
+__global__ void __launch_bounds__(256) t5(int m, int n, const float* __restrict__ A, long long lda,
+                                          const double* __restrict__ v, int nitems, double* __restrict__ part) {
+  __shared__ __align__(16) double vs[1024];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = (m + 1023) / 1024;
+  const int i0 = (int)((long long)blockIdx.x * nitems / gridDim.x);
+  const int i1 = (int)((long long)(blockIdx.x + 1) * nitems / gridDim.x);
+  double acc[8] = {};
+  int cur_cb = i0 < i1 ? i0 / nch : -1, slot = 0;
+  for (int it = i0; it < i1; ++it) {
+    const int cb = it / nch, ch = it % nch;
+    if (cb != cur_cb) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        double s = acc[u];
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) part[((long long)blockIdx.x * 2 + slot) * n + cur_cb * 64 + warp * 8 + u] = s;
+        acc[u] = 0.0;
+      }
+      cur_cb = cb;
+      slot = 1;
+    }
+    const long long c = (long long)ch * 1024;
+    __syncthreads();
+    for (int i = threadIdx.x; i < 1024; i += 256) vs[i] = v[c + i];
+    __syncthreads();
+    const int j0 = cb * 64 + warp * 8;
+#pragma unroll 2
+    for (int i = lane * 4; i < 1024; i += 128) {
+      const double2 v01 = *reinterpret_cast<const double2*>(vs + i);
+      const double2 v23 = *reinterpret_cast<const double2*>(vs + i + 2);
+      float4 a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __ldg(reinterpret_cast<const float4*>(A + (long long)(j0 + u) * lda + c + i));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc[u] = fma((double)a[u].x, v01.x, acc[u]);
+        acc[u] = fma((double)a[u].y, v01.y, acc[u]);
+        acc[u] = fma((double)a[u].z, v23.x, acc[u]);
+        acc[u] = fma((double)a[u].w, v23.y, acc[u]);
+      }
+    }
+  }
+  if (cur_cb >= 0) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      double s = acc[u];
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) part[((long long)blockIdx.x * 2 + slot) * n + cur_cb * 64 + warp * 8 + u] = s;
+    }
+  }
+}
+
 int main() {
   float* A;
   double *v, *part;
   cudaMalloc(&A, (size_t)M * N * 4);
   cudaMalloc(&v, (size_t)M * 8);
-  cudaMalloc(&part, (size_t)64 * M * 8);
+  cudaMalloc(&part, (size_t)1200 * N * 8);
   cudaMemset(A, 0, (size_t)M * N * 4);
   cudaMemset(v, 0, (size_t)M * 8);
   cudaEvent_t e0, e1;
@@ -194,7 +250,13 @@ int main() {
   time("N1 4 rows per thread, 16-byte loads, 512-col chunks", [&] { n1<512><<<dim3(M / 1024, N / 512), 256>>>(M, N, A, M, v, part); });
   time("N1 4 rows per thread, 16-byte loads, 256-col chunks", [&] { n1<256><<<dim3(M / 1024, N / 256), 256>>>(M, N, A, M, v, part); });
   time("N1 4 rows per thread, 16-byte loads, 1024-col chunks", [&] { n1<1024><<<dim3(M / 1024, N / 1024), 256>>>(M, N, A, M, v, part); });
-  for (int s : {2, 4, 8, 16}) {
+  for (int per : {2, 3, 4}) {
+    const int grid = 148 * per, nitems = (N / 64) * (M / 1024);
+    char name[96];
+    snprintf(name, sizeof name, "T5 persistent balanced, %d CTAs per SM", per);
+    time(name, [&] { t5<<<grid, 256>>>(M, N, A, M, v, nitems, part); });
+  }
+  for (int s : {16}) {
     const int rps = M / s;
     char name[96];
     snprintf(name, sizeof name, "T4 8 cols per CTA, warps on row slices, %d splits, unroll 2", s);
