@@ -579,8 +579,15 @@ __global__ void __launch_bounds__(kTriBlk) tri_n_part_kernel(int n, const TM* __
                                                              double* __restrict__ part,
                                                              const int* __restrict__ done) {
   if (done && *done) return;
-  const int rb = blockIdx.x, cb = blockIdx.y;
-  if (cb < rb) return;
+  // compact grid over the upper block triangle only (no CTAs that exit at once): block p ->
+  // (rb, cb), cb >= rb, row-major over the triangle
+  const int nch = (n + kTriBlk - 1) / kTriBlk;
+  int rb = 0, rest = blockIdx.x;
+  while (rest >= nch - rb) {
+    rest -= nch - rb;
+    ++rb;
+  }
+  const int cb = rb + rest;
   __shared__ double ps[kTriBlk];
   const int j0 = cb * kTriBlk;
   const int nc = min(kTriBlk, n - j0);
@@ -916,8 +923,7 @@ int cg_tri_chunks(int n) { return (n + kTriBlk - 1) / kTriBlk; }
 cudaError_t cg_launch_tri_n(int n, const double* M, long long ldm, const double* p, double* t,
                             double* part, const int* done, cudaStream_t st) {
   const int nch = cg_tri_chunks(n);
-  dim3 g(nch, nch);
-  tri_n_part_kernel<double><<<g, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
+  tri_n_part_kernel<double><<<nch * (nch + 1) / 2, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
   tri_n_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, nch, part, t, done);
   return cudaGetLastError();
 }
@@ -925,8 +931,7 @@ cudaError_t cg_launch_tri_n(int n, const double* M, long long ldm, const double*
 cudaError_t cg_launch_tri_n(int n, const float* M, long long ldm, const double* p, double* t,
                             double* part, const int* done, cudaStream_t st) {
   const int nch = cg_tri_chunks(n);
-  dim3 g(nch, nch);
-  tri_n_part_kernel<float><<<g, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
+  tri_n_part_kernel<float><<<nch * (nch + 1) / 2, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
   tri_n_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, nch, part, t, done);
   return cudaGetLastError();
 }
