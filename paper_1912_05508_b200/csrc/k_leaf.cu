@@ -73,6 +73,7 @@ struct LeafArgs {
   int* status;    // breakdown status (null: local leaf of a rank, zero norms allowed, R-A8)
   int col0;       // global column of the leaf's column 0 (breakdown codes)
   unsigned long long* dbg;  // optional phase timestamps of CTA 0 (globaltimer ns), 128 slots
+  unsigned long long* trace;  // optional per-launch trace: [0] count, then CTA 0 (start, end) pairs
 };
 
 struct Smem {
@@ -805,6 +806,8 @@ __global__ void __launch_bounds__(kNT, 1) leaf_kernel(const __grid_constant__ Le
   const int nrows = leaf_row(blockIdx.x + 1, a.m, a.nb) - row0;
   int slot = 0;
   leaf_ts(a, slot);
+  unsigned long long t_start = 0;
+  if (a.trace && blockIdx.x == 0 && t == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_start));
   // load the block's rows of the leaf; columns past the leaf and rows past the block are zero.
   // Columns [0, 32) (the first panel) now, 16-byte loads down the columns (a warp = 2 row quads x
   // 16 columns, so the transposing shared stores hit 32 distinct banks: row stride 132 = 4 mod 32
@@ -868,6 +871,15 @@ __global__ void __launch_bounds__(kNT, 1) leaf_kernel(const __grid_constant__ Le
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   leaf_ts(a, slot);
+  if (a.trace && blockIdx.x == 0 && t == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
+    const unsigned long long i = atomicAdd(a.trace, 1ull);
+    if (i < 4095) {
+      a.trace[1 + 2 * i] = t_start;
+      a.trace[2 + 2 * i] = t_end;
+    }
+  }
 }
 
 int leaf_split(int w) { return 32 * ((w + 63) / 64); }
@@ -1003,6 +1015,7 @@ cudaError_t unpack_rows(int m, int w, const float* src, long long lds, float* X,
 }
 
 unsigned long long* g_leaf_dbg = nullptr;
+unsigned long long* g_leaf_trace = nullptr;
 
 size_t leaf_tag_words() { return (size_t)kTgWords; }
 
@@ -1043,6 +1056,7 @@ cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long 
   a.status = status;
   a.col0 = col0;
   a.dbg = g_leaf_dbg;
+  a.trace = g_leaf_trace;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nb);
   cfg.blockDim = dim3(kNT);

@@ -64,9 +64,13 @@ struct Context {
   cudaStream_t user_stream = nullptr;  // the caller's stream (may be the legacy NULL stream)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // copy streams of the streamed host factor
-  // K1 cast of a split node's A2 runs on s_side beside the node's left recursion (it reads only
-  // A2, which the left subtree never touches); fork / join events per recursion depth
-  cudaStream_t s_side = nullptr;
+  // K1 cast of a split node's A2 runs on a side stream beside the node's left recursion (it reads
+  // only A2, which the left subtree never touches); fork / join events per recursion depth.  One
+  // side stream per class of node width (w <= 2 cutoff, 4 cutoff, 16 cutoff, wider), the narrower
+  // the more urgent: a leaf-level node's cast is needed one leaf later and must not queue behind
+  // an ancestor's wide cast (measured at config 3: 470 us gaps after the first leaf otherwise)
+  static constexpr int kSide = 4;
+  cudaStream_t s_side[kSide] = {};
   cudaEvent_t ev_fork[64] = {}, ev_join[64] = {};
   int cast_overlap = 1;  // env TCQR_CAST_OVERLAP=0 turns it off
   // Look-ahead (one rank, device path): a split node of width w <= la_max_w updates only the
@@ -980,22 +984,25 @@ static int rgs(FactorJob& J, int c0, int w, bool need_h) {
     // K1 of this node's A2 does not depend on the left recursion (Alg. 2 line 7 writes only
     // columns [c0, c0+h)): fork it onto the side stream, join before the TN product
     const bool side = tc && !J.sp && c.cast_overlap && !g_prof && J.depth < 64;
+    cudaStream_t s_side = nullptr;
     if (side) {
+      const int cut = c.cfg.cutoff;
+      s_side = c.s_side[w <= 2 * cut ? 3 : w <= 4 * cut ? 2 : w <= 16 * cut ? 1 : 0];
       const int p0 = c0 + h;
       float* A2p = J.Q + (long long)p0 * J.ldq;
       __half* A2h = ws.Qh + (long long)p0 * ws.ldh;
       CK(cudaEventRecord(c.ev_fork[J.depth], c.stream));
-      CK(cudaStreamWaitEvent(c.s_side, c.ev_fork[J.depth], 0));
-      CKR(la_wait(J, p0, p0 + w2, c.s_side));  // ancestors' deferred updates of A2
+      CK(cudaStreamWaitEvent(s_side, c.ev_fork[J.depth], 0));
+      CKR(la_wait(J, p0, p0 + w2, s_side));  // ancestors' deferred updates of A2
       const bool first = J.untouched >= p0 + w2;  // A2 never touched: copy-cast from the input
       CK(cast_scale(m, w2, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, c.cfg.col_scaling, c.d_status,
-                    p0, ws.cmax + p0, c.s_side, first ? J.src + (long long)p0 * J.lds : nullptr,
+                    p0, ws.cmax + p0, s_side, first ? J.src + (long long)p0 * J.lds : nullptr,
                     J.lds));
       if (first) J.untouched = p0;
       if (c.cfg.fp16_split && ws.Ql)
         CK(cast_lo(m, w2, A2p, J.ldq, A2h, ws.ldh, ws.inv_s + p0, ws.Ql + (long long)p0 * ws.ldh,
-                   ws.ldh, c.s_side));
-      CK(cudaEventRecord(c.ev_join[J.depth], c.s_side));
+                   ws.ldh, s_side));
+      CK(cudaEventRecord(c.ev_join[J.depth], s_side));
     }
     ++J.depth;
     const int lrc = rgs(J, c0, h, tc || need_h);  // Alg. 2 line 7
@@ -1428,8 +1435,10 @@ static int finalize_ctx() {
   if (c.ev_in) cudaEventDestroy(c.ev_in);
   if (c.ev_out) cudaEventDestroy(c.ev_out);
   if (c.stream) cudaStreamDestroy(c.stream);
-  if (c.s_side) cudaStreamDestroy(c.s_side);
-  c.s_side = nullptr;
+  for (int i = 0; i < Context::kSide; ++i) {
+    if (c.s_side[i]) cudaStreamDestroy(c.s_side[i]);
+    c.s_side[i] = nullptr;
+  }
   if (c.s_la) cudaStreamDestroy(c.s_la);
   c.s_la = nullptr;
   if (c.s_comm) cudaStreamDestroy(c.s_comm);
@@ -1490,12 +1499,17 @@ static int init_ctx(int device, void* cuda_stream, const void* nccl_unique_id, i
   cudaEventCreateWithFlags(&c.ev_in, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c.ev_out, cudaEventDisableTiming);
   if (cudaStreamCreateWithFlags(&c.s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c.s_d2h, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c.s_side, cudaStreamNonBlocking) != cudaSuccess)
+      cudaStreamCreateWithFlags(&c.s_d2h, cudaStreamNonBlocking) != cudaSuccess)
     return TCQR_ERR_CUDA;
   {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo: the least urgent
+    // side streams: the narrowest nodes' casts most urgent (priorities between lo and hi)
+    for (int i = 0; i < Context::kSide; ++i) {
+      const int pr = lo + (hi < lo ? -1 : 1) * std::min(i, std::abs(hi - lo));
+      if (cudaStreamCreateWithPriority(&c.s_side[i], cudaStreamNonBlocking, pr) != cudaSuccess)
+        return TCQR_ERR_CUDA;
+    }
     if (cudaStreamCreateWithPriority(&c.s_la, cudaStreamNonBlocking, lo) != cudaSuccess)
       return TCQR_ERR_CUDA;
     if (cudaStreamCreateWithPriority(&c.s_comm, cudaStreamNonBlocking, hi) != cudaSuccess)
@@ -2187,6 +2201,12 @@ int tcqr_debug_panel_timestamps(void* dptr) {
 }
 int tcqr_debug_leaf_timestamps(void* dptr) {
   g_leaf_dbg = static_cast<unsigned long long*>(dptr);
+  return 0;
+}
+// Debug: 8192 device uint64 slots (zeroed): [0] counts leaf launches, then (start, end) globaltimer
+// pairs of CTA 0 of each launch (or NULL).  Read at launch time (graphs keep the captured value).
+int tcqr_debug_leaf_trace(void* dptr) {
+  g_leaf_trace = static_cast<unsigned long long*>(dptr);
   return 0;
 }
 int tcqr_debug_proj_timestamps(void* dptr) {
