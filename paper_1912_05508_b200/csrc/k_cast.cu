@@ -14,6 +14,11 @@
 
 namespace tcqr {
 
+// streaming (evict-first) loads and stores of the cast (env TCQR_L2_EF=0: plain): see g_l2_ef in
+// k_gemm_tc.cu -- the casts stream GBs beside the leaves and must not evict the leaf's code
+__constant__ int g_cast_ef = 1;
+
+
 constexpr int kCastThreads = 256;
 
 __device__ __forceinline__ float block_max(float v, float* red) {
@@ -129,7 +134,10 @@ __global__ void __launch_bounds__(256) cast_pass2_kernel(int m, const float* __r
       uint2 pk;
       pk.x = *reinterpret_cast<uint32_t*>(&lo);
       pk.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(xh + q) = pk;
+      if (g_cast_ef)
+        __stcs(reinterpret_cast<uint2*>(xh + q), pk);
+      else
+        *reinterpret_cast<uint2*>(xh + q) = pk;
     }
     i = r0 + ((r1 - r0) & ~3LL);
   }
@@ -171,7 +179,8 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* X
   for (int u = 0; u < V; ++u) {
     const long long q = r0 + 4LL * (threadIdx.x + 256 * u);
     if (q + 3 < m) {
-      v[u] = *reinterpret_cast<const float4*>(x + q);
+      v[u] = g_cast_ef ? __ldcs(reinterpret_cast<const float4*>(x + q))
+                       : *reinterpret_cast<const float4*>(x + q);
     } else {
       v[u].x = q < m ? x[q] : 0.f;
       v[u].y = q + 1 < m ? x[q + 1] : 0.f;
@@ -184,7 +193,10 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* X
     for (int u = 0; u < V; ++u) {
       const long long q = r0 + 4LL * (threadIdx.x + 256 * u);
       if (q + 3 < m) {
-        *reinterpret_cast<float4*>(xc + q) = v[u];
+        if (g_cast_ef)
+          __stcs(reinterpret_cast<float4*>(xc + q), v[u]);
+        else
+          *reinterpret_cast<float4*>(xc + q) = v[u];
       } else {
         if (q < m) xc[q] = v[u].x;
         if (q + 1 < m) xc[q + 1] = v[u].y;
@@ -223,7 +235,10 @@ __global__ void __launch_bounds__(256) cast_cluster_kernel(int m, const float* X
       uint2 pk;
       pk.x = *reinterpret_cast<uint32_t*>(&lo);
       pk.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(xh + q) = pk;
+      if (g_cast_ef)
+        __stcs(reinterpret_cast<uint2*>(xh + q), pk);
+      else
+        *reinterpret_cast<uint2*>(xh + q) = pk;
     } else {
       if (q < m) xh[q] = __float2half_rn(v[u].x * s);
       if (q + 1 < m) xh[q + 1] = __float2half_rn(v[u].y * s);
@@ -270,6 +285,13 @@ cudaError_t cast_scale(int m, int w, const float* X, long long ldx, __half* Xh, 
   const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
                    ((ldh & 3) == 0) && ((reinterpret_cast<uintptr_t>(Xh) & 7) == 0) &&
                    (!src || (((lds & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)));
+  static bool ef_done = false;
+  if (!ef_done) {
+    ef_done = true;
+    const char* e = getenv("TCQR_L2_EF");
+    const int v = (e ? atoi(e) : 1) & 1;
+    if (v != 1) cudaMemcpyToSymbol(g_cast_ef, &v, sizeof(int));
+  }
   if (use_cluster && vec && (scaling || status) && m <= 8 * 8192) {
     // 8192-row CTAs (8 float4 loads in flight per thread) by default: at config 3 K1 3.03 ->
     // 2.76 ms against 4096-row CTAs (profiles/r01_bench_cfg3_v19_*); env TCQR_CAST_V8=0 for those

@@ -60,13 +60,34 @@ __device__ __forceinline__ void tile_of(int w, int tiles_m, int tiles_n, int& mb
 }
 
 __constant__ int nn_pre_all = 1;
+// L2 policy of the streamed operands and C tiles: evict_first for what one launch reads once (an
+// operand whose other dimension fits one tile, the C tiles of the update), so the streams between
+// two leaves do not push the whole-leaf kernel's 190 KB of code (and the next leaf's columns) out
+// of L2 (measured: a leaf whose code comes from HBM runs 10-20 us longer,
+// tools/leaf_phases_insitu.py); operands re-read across tiles keep evict_normal (their L2 reuse).
+// The first kKeepCols columns of an update -- the right subtree's first leaf, read next -- keep
+// evict_normal.  Bits of the per-launch ef argument:
+constexpr int kEfA = 1, kEfB = 2, kEfC = 4;
+// host mask (env TCQR_L2_EF): 1 the K1 casts (k_cast.cu), 2 the C tiles, 4 read-once operands,
+// 8 every operand.  Default 5 (config 3, interleaved benches: 0 -> 44.50 ms, 5 -> 44.02, 7 -> 44.12,
+// 6 -> 44.09; 15 -> +1.2 ms of gaps: the wide levels' operands need their L2 reuse)
+constexpr int kL2EfDefault = 5;
+constexpr int kKeepCols = 128;
+// direct-epilogue C accesses: streaming (evict-first) loads, stores past the kept columns
+__device__ __forceinline__ float c_load(int ef, const float* p) { return (ef & kEfC) ? __ldcs(p) : *p; }
+__device__ __forceinline__ void c_store(float* p, float v, int col, int ef) {
+  if ((ef & kEfC) && col >= kKeepCols)
+    __stcs(p, v);
+  else
+    *p = v;
+}
 
 template <int BN, int MODE, int NBUF>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int splits,
                    float* __restrict__ C, long long ldc, long long split_stride,
-                   const float* __restrict__ col_mult) {
+                   const float* __restrict__ col_mult, int ef) {
   using Cfg = TcCfg<BN, MODE, NBUF>;
   constexpr bool TMAC = NBUF > 0;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, ST = Cfg::ST, STAGE = Cfg::STAGE;
@@ -109,6 +130,7 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
+      const uint64_t pol_a = l2_policy(ef & kEfA), pol_b = l2_policy(ef & kEfB);
       int stage = 0;
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -121,12 +143,12 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* sa = smem + stage * STAGE;
           uint8_t* sb = sa + Cfg::A_BYTES;
           if (MODE == kModeTN) {
-            tma_load_2d(sa, &tmA, &full[stage], kb * BK, mb * BM);
+            tma_load_2d_hint(sa, &tmA, &full[stage], kb * BK, mb * BM, pol_a);
           } else {
-            tma_load_2d(sa, &tmA, &full[stage], mb * BM, kb * BK);
-            tma_load_2d(sa + 8192, &tmA, &full[stage], mb * BM + 64, kb * BK);
+            tma_load_2d_hint(sa, &tmA, &full[stage], mb * BM, kb * BK, pol_a);
+            tma_load_2d_hint(sa + 8192, &tmA, &full[stage], mb * BM + 64, kb * BK, pol_a);
           }
-          tma_load_2d(sb, &tmB, &full[stage], kb * BK, nb * BN);
+          tma_load_2d_hint(sb, &tmB, &full[stage], kb * BK, nb * BN, pol_b);
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
@@ -180,6 +202,7 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     const int rt = q * 32 + lane;  // row within the tile (= TMEM lane)
     const bool issuer = (warp == 2 && lane == 0);
+    const uint64_t pol_ef = l2_policy(ef & kEfC), pol_n = l2_policy(0);
     uint32_t cph = 0;
     int it = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
@@ -195,7 +218,7 @@ __global__ void __launch_bounds__(192, 1)
         bulk_wait_read<0>();  // the previous tile's stores have read their buffers
         for (int c = 0; c < pre && c < nch; ++c) {
           mbar_arrive_expect_tx(&cfull[c], 16384);
-          tma_load_2d(cbuf + c * 4096, &tmC, &cfull[c], mb * BM, nb * BN + 32 * c);
+          tma_load_2d_hint(cbuf + c * 4096, &tmC, &cfull[c], mb * BM, nb * BN + 32 * c, pol_ef);
         }
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -220,7 +243,7 @@ __global__ void __launch_bounds__(192, 1)
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA store
         named_bar_sync(1, 128);
         if (issuer) {
-          tma_store_2d(&tmC, cb, mb * BM, col0);
+          tma_store_2d_hint(&tmC, cb, mb * BM, col0, col0 >= kKeepCols ? pol_ef : pol_n);
           bulk_commit();
           if (c + pre < nch) {
             // the buffer of chunk c + pre was last used by chunk c + pre - NBUF (c or c - 1),
@@ -231,7 +254,8 @@ __global__ void __launch_bounds__(192, 1)
             else
               bulk_wait_read<1>();
             mbar_arrive_expect_tx(&cfull[nbuf], 16384);
-            tma_load_2d(cbuf + nbuf * 4096, &tmC, &cfull[nbuf], mb * BM, nb * BN + 32 * (c + pre));
+            tma_load_2d_hint(cbuf + nbuf * 4096, &tmC, &cfull[nbuf], mb * BM, nb * BN + 32 * (c + pre),
+                             pol_ef);
           }
         }
       }
@@ -257,7 +281,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int col = nb * BN + j;
-          cv[j] = (rok && col < N) ? C[row + (long long)col * ldc] : 0.f;
+          cv[j] = (rok && col < N) ? c_load(ef, C + row + (long long)col * ldc) : 0.f;
         }
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -287,7 +311,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int col = col0 + 32 + j;
-            cn[j] = (rok && c + 32 < BN && col < N) ? C[row + (long long)col * ldc] : 0.f;
+            cn[j] = (rok && c + 32 < BN && col < N) ? c_load(ef, C + row + (long long)col * ldc) : 0.f;
           }
           tmem_ld_wait();
           if (rok) {
@@ -297,7 +321,7 @@ __global__ void __launch_bounds__(192, 1)
               const int col = col0 + j;
               if (col < N) {
                 const float mlt = col_mult ? __ldg(col_mult + col) : 1.f;
-                out[(long long)col * ldc] = cv[j] - __uint_as_float(r[j]) * mlt;
+                c_store(out + (long long)col * ldc, cv[j] - __uint_as_float(r[j]) * mlt, col, ef);
               }
             }
           }
@@ -355,7 +379,7 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K, int splits,
                        float* __restrict__ C, long long ldc, long long split_stride,
-                       const float* __restrict__ col_mult) {
+                       const float* __restrict__ col_mult, int ef) {
   using Cfg = Tc2Cfg;
   constexpr int BK = Cfg::BK, ST = Cfg::ST, STAGE = Cfg::STAGE;
   extern __shared__ uint8_t smem_raw[];
@@ -404,6 +428,7 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
+      const uint64_t pol_a = l2_policy(ef & kEfA), pol_b = l2_policy(ef & kEfB);
       int stage = 0;
       uint32_t phase = 0;
       for (int w = pair; w < total; w += npairs) {
@@ -418,26 +443,29 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
           const uint32_t bar = leader_addr(&full[stage]);
           if (MODE == kModeTN) {
             asm volatile(
-                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sa)),
+                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(sa)),
                 "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(bar), "r"(kb * BK),
                 "r"(mb * 256 + (int)rank * 128)
+                , "l"(pol_a)
                 : "memory");
           } else {  // A = Q1 MN-major: two 64 (M) x 64 (K) boxes of this CTA's 128 rows
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh)
               asm volatile(
-                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                  " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sa + hh * 8192)),
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                  " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(sa + hh * 8192)),
                   "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(bar),
                   "r"(mb * 256 + (int)rank * 128 + hh * 64), "r"(kb * BK)
-                  : "memory");
+                  , "l"(pol_a)
+                : "memory");
           }
           asm volatile(
-              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-              " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sb)),
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+              " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(sb)),
               "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(bar), "r"(kb * BK),
               "r"(nb * 256 + (int)rank * 128)
+              , "l"(pol_b)
               : "memory");
           if (++stage == ST) {
             stage = 0;
@@ -514,7 +542,7 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int col = nb * Cfg::BN + j;
-          cv[j] = (rok && col < N) ? C[row + (long long)col * ldc] : 0.f;
+          cv[j] = (rok && col < N) ? c_load(ef, C + row + (long long)col * ldc) : 0.f;
         }
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -544,7 +572,7 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int col = col0 + 32 + j;
-            cn[j] = (rok && c + 32 < Cfg::BN && col < N) ? C[row + (long long)col * ldc] : 0.f;
+            cn[j] = (rok && c + 32 < Cfg::BN && col < N) ? c_load(ef, C + row + (long long)col * ldc) : 0.f;
           }
           tmem_ld_wait();
           if (rok) {
@@ -554,7 +582,7 @@ __global__ void __launch_bounds__(192, 1) __cluster_dims__(2, 1, 1)
               const int col = col0 + j;
               if (col < N) {
                 const float mlt = col_mult ? __ldg(col_mult + col) : 1.f;
-                out[(long long)col * ldc] = cv[j] - __uint_as_float(r[j]) * mlt;
+                c_store(out + (long long)col * ldc, cv[j] - __uint_as_float(r[j]) * mlt, col, ef);
               }
             }
           }
@@ -672,6 +700,24 @@ static bool make_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uin
   return r == CUDA_SUCCESS;
 }
 
+static int l2_ef_mask() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TCQR_L2_EF");
+    v = e ? atoi(e) : kL2EfDefault;
+  }
+  return v;
+}
+// per-launch ef bits: an operand is read once when the output's other dimension is one tile
+static int launch_ef(int mode, int M, int N, int tile_m, int tile_n) {
+  const int g = l2_ef_mask();
+  int ef = (g & 2) ? kEfC : 0;
+  const bool all = (g & 8) != 0, once = (g & 4) != 0;
+  if (all || (once && N <= tile_n)) ef |= kEfA;
+  if (mode == kModeTN && (all || (once && M <= tile_m))) ef |= kEfB;
+  return ef;
+}
+
 template <int BN, int MODE, int NBUF = 0>
 static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
                              int M, int N, int K, int splits, float* C, long long ldc,
@@ -688,7 +734,8 @@ static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const C
   const int slots = Cfg::OCC * num_sms;
   const int grid = tiles < slots ? tiles : slots;
   tc_gemm_kernel<BN, MODE, NBUF><<<grid, 192, Cfg::SMEM, st>>>(a, b, cm, M, N, K, splits, C, ldc,
-                                                               sstride, mult);
+                                                               sstride, mult,
+                                                               launch_ef(MODE, M, N, 128, BN));
   return cudaGetLastError();
 }
 
@@ -708,7 +755,8 @@ static cudaError_t launch_tc2(const CUtensorMap& ma, const CUtensorMap& mb, int 
   const int units = ((M + 255) / 256) * ((N + 255) / 256) * splits;
   const int npairs = std::min(units, num_sms / 2);
   tc_gemm2_kernel<MODE><<<2 * npairs, 192, Cfg::SMEM, st>>>(ma, mb, M, N, K, splits, C, ldc,
-                                                             sstride, mult);
+                                                             sstride, mult,
+                                                             launch_ef(MODE, M, N, 256, 256));
   return cudaGetLastError();
 }
 

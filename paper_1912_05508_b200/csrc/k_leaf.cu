@@ -1016,6 +1016,8 @@ cudaError_t unpack_rows(int m, int w, const float* src, long long lds, float* X,
 
 unsigned long long* g_leaf_dbg = nullptr;
 unsigned long long* g_leaf_trace = nullptr;
+unsigned long long* g_leaf_dbg_multi = nullptr;
+unsigned g_leaf_dbg_idx = 0;
 
 size_t leaf_tag_words() { return (size_t)kTgWords; }
 
@@ -1055,7 +1057,7 @@ cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long 
   a.tag0 = tag_seq[0];
   a.status = status;
   a.col0 = col0;
-  a.dbg = g_leaf_dbg;
+  a.dbg = g_leaf_dbg_multi ? g_leaf_dbg_multi + 128 * (g_leaf_dbg_idx++ & 127) : g_leaf_dbg;
   a.trace = g_leaf_trace;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nb);

@@ -96,6 +96,8 @@ extern unsigned long long* g_proj_dbg;  // debug: phase timestamps of the FP32 p
 // cudaErrorNotSupported when the blocks do not fit the co-resident grid.
 size_t leaf_tag_words();
 extern unsigned long long* g_leaf_dbg;  // debug: CTA-0 phase timestamps of the leaf kernel
+extern unsigned long long* g_leaf_dbg_multi;  // debug: 128 launches x 128 phase slots
+extern unsigned g_leaf_dbg_idx;
 extern unsigned long long* g_leaf_trace;  // debug: per-launch (start, end) of every leaf launch
 cudaError_t leaf_fused(int m, int wl, float* X, long long ldx, __half* Xh, long long ldh, float* R,
                        long long ldr, int col0, int* status, unsigned long long* tg,

@@ -2205,6 +2205,13 @@ int tcqr_debug_leaf_timestamps(void* dptr) {
 }
 // Debug: 8192 device uint64 slots (zeroed): [0] counts leaf launches, then (start, end) globaltimer
 // pairs of CTA 0 of each launch (or NULL).  Read at launch time (graphs keep the captured value).
+// Debug: 128 x 128 device uint64 slots: launch i (mod 128, counted from this call) writes its
+// CTA-0 phase timestamps to slots [128 i, 128 i + 128) (or NULL).
+int tcqr_debug_leaf_timestamps_multi(void* dptr) {
+  g_leaf_dbg_multi = static_cast<unsigned long long*>(dptr);
+  g_leaf_dbg_idx = 0;
+  return 0;
+}
 int tcqr_debug_leaf_trace(void* dptr) {
   g_leaf_trace = static_cast<unsigned long long*>(dptr);
   return 0;
@@ -2243,3 +2250,26 @@ int tcqr_gemv(int trans, int64_t m, int64_t n, const float* A, int64_t lda, cons
 }
 
 }  // extern "C"
+
+// Debug: overwrite n floats at p with zeros (evict_first != 0: stores carry an L2 evict_first
+// policy) -- a cache polluter for the leaf's instruction-fetch experiments.
+namespace {
+__global__ void debug_pollute_kernel(float4* p, long long n4, int evict_first) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (evict_first)
+      asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p + i),
+                   "f"(z.x), "f"(z.y), "f"(z.z), "f"(z.w), "l"(pol)
+                   : "memory");
+    else
+      p[i] = z;
+  }
+}
+}  // namespace
+extern "C" int tcqr_debug_pollute(void* p, int64_t n, int evict_first) {
+  debug_pollute_kernel<<<4 * 148, 256, 0, g_ctx.stream>>>(static_cast<float4*>(p), n / 4, evict_first);
+  return cudaStreamSynchronize(g_ctx.stream) == cudaSuccess ? 0 : TCQR_ERR_CUDA;
+}

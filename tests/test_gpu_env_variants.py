@@ -5,10 +5,12 @@ each group runs in its own Python process and must pass the same oracle gates as
 
   group "fallbacks": TCQR_CAST_CLUSTER=0 (one-CTA-per-column / split-row casts), TCQR_TC2=0 (no
       CTA-pair GEMMs), TCQR_LOOKAHEAD_W=0 (no look-ahead), TCQR_CAST_OVERLAP=0 (casts in line),
-      TCQR_NN_PRE_ALL=0 (NN epilogue with NBUF - 1 C chunks in flight)
+      TCQR_NN_PRE_ALL=0 (NN epilogue with NBUF - 1 C chunks in flight), TCQR_L2_EF=0 (no L2
+      evict-first hints)
   group "variants":  TCQR_CAST_V8=0 (4096-row cluster CTAs), TCQR_TC2_NN_MINK=256 (CTA-pair NN
       from K = 256), TCQR_TN_MINKB=1 (finest split-K), TCQR_NN_SHORTK=0 (no short-K NN),
-      TCQR_LOOKAHEAD_W=1024 with TCQR_LA_SMS=2 (leaf-wide deferred look-ahead blocks)
+      TCQR_LOOKAHEAD_W=1024 with TCQR_LA_SMS=2 (leaf-wide deferred look-ahead blocks),
+      TCQR_L2_EF=15 (evict-first hints on every operand and C tile)
   group "host":      TCQR_CAST_COL_MIN=1 (per-column cast kernel at every width), TCQR_STREAM_DIV=4
       (coarse chunks of the streamed host factorization)
 """
@@ -52,9 +54,10 @@ print("ok")
 
 GROUPS = {
     "fallbacks": {"TCQR_CAST_CLUSTER": "0", "TCQR_TC2": "0", "TCQR_LOOKAHEAD_W": "0",
-                  "TCQR_CAST_OVERLAP": "0", "TCQR_NN_PRE_ALL": "0"},
+                  "TCQR_CAST_OVERLAP": "0", "TCQR_NN_PRE_ALL": "0", "TCQR_L2_EF": "0"},
     "variants": {"TCQR_CAST_V8": "0", "TCQR_TC2_NN_MINK": "256", "TCQR_TN_MINKB": "1",
-                 "TCQR_NN_SHORTK": "0", "TCQR_LOOKAHEAD_W": "1024", "TCQR_LA_SMS": "2"},
+                 "TCQR_NN_SHORTK": "0", "TCQR_LOOKAHEAD_W": "1024", "TCQR_LA_SMS": "2",
+                 "TCQR_L2_EF": "15"},
     "host": {"TCQR_CAST_COL_MIN": "1", "TCQR_STREAM_DIV": "4"},
 }
 
