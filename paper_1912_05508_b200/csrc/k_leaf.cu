@@ -87,7 +87,6 @@ struct Smem {
   double Rd[32 * 34 + 34];     // the panel's R in FP64, row-major (ld 34; one row of slack)
   double rowb[kMW][2][64];     // Cholesky: row k of R twice over, per chain warp (step parity)
   float colbuf[kMW][kBR];      // MGS: the pivot column of each block
-  float qbuf[kMW][kBR];        // MGS: q_k of each block
   double Gs[528];              // PANEL: the stack's Gram (packed upper triangle), from the owners
   float wsum[kNW * 32];        // per-warp partial sums of the cross-CTA reductions (FP32)
   double wsumd[kNW * 32];      //   (FP64)
@@ -309,15 +308,14 @@ __device__ __forceinline__ void tagged_gather(const LeafArgs& a, const unsigned 
 // Step k: the pivot column x_k (published in colbuf by lane k) is broadcast to every lane; lane j
 // forms a_k' a_j over the block's 64 rows (lane k: the norm^2); R(k, k) = sqrt, one correctly
 // rounded reciprocal (reading R-B2); R(k, j) = (a_k' a_j) / R(k, k) (R-A7); q_k = x_k / R(k, k)
-// (line 6) is formed once per row (lane r: rows r, r + 32), broadcast through qbuf and written to
-// L as the block's final Q column k; lines 7-8 update every lane's column by FFMA2.  A locally
+// (line 6) is formed by every lane from its copy of x_k (lane r writes rows r, r + 32 to L as the
+// block's final Q column k); lines 7-8 update every lane's column by FFMA2.  A locally
 // zero norm gives q = 0, r = 0 (R-A8; only the stack's Cholesky reports breakdowns).  Afterwards
 // the warp forms the block's Gram R_b' R_b (FP64, packed upper triangle) for the stack.
 __device__ __forceinline__ void mgs_warp(Smem& s, int blk, int c0, int pw) {
   const int lane = threadIdx.x & 31;
   const int r0 = blk * kBR;
   float* colb = s.colbuf[blk];
-  float* qb = s.qbuf[blk];
   double* Rb = s.Rbd[blk];
   float2 x[kBR / 2];  // x[i] = rows (r0 + 2i, r0 + 2i + 1) of column c0 + lane
 #pragma unroll
@@ -354,18 +352,15 @@ __device__ __forceinline__ void mgs_warp(Smem& s, int blk, int c0, int pw) {
     const float rkj = zero ? 0.f : (lane == k ? rkk : tot * inv);
     if (lane >= k && lane < pw) Rb[k * kLdR + lane] = (double)rkj;
     const float q0 = colb[lane] * inv, q1 = colb[lane + 32] * inv;
-    __syncwarp();  // every lane has read colb before lane k + 1 republishes it below
-    qb[lane] = q0;
-    qb[lane + 32] = q1;
     s.L[(r0 + lane) * kLd + c0 + k] = q0;
     s.L[(r0 + lane + 32) * kLd + c0 + k] = q1;
-    __syncwarp();
+    // q_k in every lane's registers: its copy of the pivot column times 1/R(k,k) (x * inv + -0 is
+    // x * inv exactly: the same bits as q0 / q1), no shared-memory round trip on the chain
+    // (tools/micro/mgs_warp_bench.cu V9: 815 -> 794 cycles per step)
+    const float2 iv = make_float2(inv, inv), nz = make_float2(-0.f, -0.f);
 #pragma unroll
-    for (int i = 0; i < kBR / 4; ++i) {
-      const float4 q4 = *reinterpret_cast<const float4*>(qb + 4 * i);
-      v[2 * i] = make_float2(q4.x, q4.y);
-      v[2 * i + 1] = make_float2(q4.z, q4.w);
-    }
+    for (int i = 0; i < kBR / 2; ++i) v[i] = ffma2(v[i], iv, nz);
+    __syncwarp();  // every lane has read colb before lane k + 1 republishes it below
     const float2 nr = make_float2(-rkj, -rkj);
 #pragma unroll
     for (int i = 0; i < kBR / 2; ++i) x[i] = ffma2(v[i], nr, x[i]);  // x_j - q_k R(k, j)

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(128, 1) bench(const float* A, float* Q, float*
   float2 v[BR / 2];
   __syncwarp();
   long long t0 = clock64();
-  if (V <= 1) {
+  if (V <= 1 || V == 9) {
     if (lane == 0)
 #pragma unroll
       for (int i = 0; i < BR / 4; ++i)
@@ -73,6 +73,14 @@ __global__ void __launch_bounds__(128, 1) bench(const float* A, float* Q, float*
       const float rkj = zero ? 0.f : (lane == k ? rkk : tot * inv);
       Rrow[k] = rkj;
       const float q0 = colb[lane] * inv, q1 = colb[lane + 32] * inv;
+      if (V == 9) {  // q_k formed in every lane from its copy of the pivot column (same bits)
+        L[w][k * LD + lane] = q0;
+        L[w][k * LD + lane + 32] = q1;
+        const float2 iv = make_float2(inv, inv), nz = make_float2(-0.f, -0.f);
+#pragma unroll
+        for (int i = 0; i < BR / 2; ++i) v[i] = ffma2(v[i], iv, nz);
+        __syncwarp();  // every lane has read colb before lane k + 1 republishes it
+      } else {
       __syncwarp();
       qb[lane] = q0;
       qb[lane + 32] = q1;
@@ -84,6 +92,7 @@ __global__ void __launch_bounds__(128, 1) bench(const float* A, float* Q, float*
         const float4 q4 = *reinterpret_cast<const float4*>(qb + 4 * i);
         v[2 * i] = make_float2(q4.x, q4.y);
         v[2 * i + 1] = make_float2(q4.z, q4.w);
+      }
       }
       const float2 nr = make_float2(-rkj, -rkj);
 #pragma unroll
@@ -288,7 +297,7 @@ int main() {
   float* ref = (float*)malloc(ne * 4);
   float* out = (float*)malloc(ne * 4);
   auto run = [&](auto kern, const char* name, int v) {
-    for (int r = 0; r < 3; ++r) kern<<<148, v >= 4 ? 256 : 128>>>(A, Q, R, cyc);
+    for (int r = 0; r < 3; ++r) kern<<<148, (v >= 4 && v <= 8) ? 256 : 128>>>(A, Q, R, cyc);
     cudaDeviceSynchronize();
     long long c;
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
@@ -301,6 +310,7 @@ int main() {
   };
   run(bench<0>, "V0 colbuf publish + qbuf, sqrtf + __frcp_rn", 0);
   run(bench<1>, "V1 = V0 with 1.0f / rkk", 1);
+  run(bench<9>, "V9 = V1 with q in registers (every lane scales its pivot copy)", 9);
   run(bench<2>, "V2 pre-update publish + recompute, q in regs, sqrtf + 1/x", 2);
   run(bench<3>, "V3 = V2 with one FP64 rsqrt", 3);
   run(bench2<4>, "V4 two warps per block (row halves), q via qbuf, sqrtf + 1/x", 4);
