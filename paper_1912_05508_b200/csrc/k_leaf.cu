@@ -616,6 +616,15 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
   leaf_ts(a, slot);
 }
 
+// column of entry c (0..7) of column tile tj in the projection's partial R12 (see leaf_proj)
+template <int W2P>
+__device__ __forceinline__ int tile_col(int tj, int c) {
+  if constexpr (W2P == 64)
+    return (c < 4 ? 4 * tj : 32 + 4 * tj) + (c & 3);
+  else
+    return 8 * tj + c;
+}
+
 // ---- PROJ: R12 = Q1' A2, R block <- R12, A2 -= Q1 R12 (FP32) ------------------------------------
 // H = h (32 or 64), W2P = w2 rounded up to 32 (the columns past the leaf are zero in shared memory
 // and stay zero).
@@ -641,13 +650,18 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
     for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
   {
     const float* q1 = s.L + c0 + 8 * ti;
-    const float* a2 = s.L + c0 + H + 8 * tj;
+    // the tile's 8 A2 columns: 8 tj .. 8 tj + 7, or for 8 column tiles (W2P = 64: 4 row groups per
+    // tile, so a quarter-warp holds 2 tiles x 4 rows) the quads 4 tj and 32 + 4 tj, which keeps
+    // the quarter-warp's 16-byte loads on distinct banks (8 tj would put tiles tj and tj + 4 on
+    // the same banks: a 2-way conflict on half the loads)
+    const int ca0 = tile_col<W2P>(tj, 0), ca4 = tile_col<W2P>(tj, 4);
+    const float* a2 = s.L + c0 + H;
 #pragma unroll 2
     for (int r = grp; r < nrows; r += G) {
       const float4 q0 = *reinterpret_cast<const float4*>(q1 + r * kLd);
       const float4 q4 = *reinterpret_cast<const float4*>(q1 + r * kLd + 4);
-      const float4 a0 = *reinterpret_cast<const float4*>(a2 + r * kLd);
-      const float4 a4 = *reinterpret_cast<const float4*>(a2 + r * kLd + 4);
+      const float4 a0 = *reinterpret_cast<const float4*>(a2 + r * kLd + ca0);
+      const float4 a4 = *reinterpret_cast<const float4*>(a2 + r * kLd + ca4);
       const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q4.x, q4.y, q4.z, q4.w};
       const float2 av[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w),
                             make_float2(a4.x, a4.y), make_float2(a4.z, a4.w)};
@@ -683,7 +697,7 @@ __device__ __noinline__ void leaf_proj(const LeafArgs& a, Smem& s, int nrows, in
 #pragma unroll
   for (int k = 0; k < KEEP; ++k) {
     const int idx = grp * KEEP + k;
-    TagWords<float>::put(pp + (8 * ti + idx / 8) * W2P + 8 * tj + idx % 8, v[k], tag);
+    TagWords<float>::put(pp + (8 * ti + idx / 8) * W2P + tile_col<W2P>(tj, idx % 8), v[k], tag);
   }
   leaf_ts(a, slot);
   tagged_sum<float>(a, a.tg + kTgPP, 4096, H * W2P, tag, a.tg + kTgPS, s.wsum, H, w2, W2P, c0,
