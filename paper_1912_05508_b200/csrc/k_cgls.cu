@@ -610,6 +610,70 @@ __global__ void __launch_bounds__(kTriBlk) tri_n_part_kernel(int n, const TM* __
   part[(long long)cb * n + i] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
+// The FP32 M with 16-byte row quads (n, ldm multiples of 4, M 16-byte aligned): the same blocks
+// and partials, thread = (row quad q, column slice cs): rows 4q..4q+3 of the block over the
+// slice's 64 columns, one 16-byte load per column (8 in flight: 128 bytes per thread, where one
+// 4-byte row per thread kept too few bytes in flight for HBM), the four slices added in order
+// through shared memory.
+__global__ void __launch_bounds__(kTriBlk) tri_n_part_f32v_kernel(int n, const float* __restrict__ M,
+                                                                  long long ldm,
+                                                                  const double* __restrict__ p,
+                                                                  double* __restrict__ part,
+                                                                  const int* __restrict__ done) {
+  if (done && *done) return;
+  const int nch = (n + kTriBlk - 1) / kTriBlk;
+  int rb = 0, rest = blockIdx.x;
+  while (rest >= nch - rb) {
+    rest -= nch - rb;
+    ++rb;
+  }
+  const int cb = rb + rest;
+  __shared__ double ps[kTriBlk];
+  __shared__ double sl[3][kTriBlk];
+  const int j0 = cb * kTriBlk;
+  const int nc = min(kTriBlk, n - j0);
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) ps[j] = p[j0 + j];
+  __syncthreads();
+  const int q = threadIdx.x & 63, cs = threadIdx.x >> 6;
+  const int i0 = rb * kTriBlk + 4 * q;  // n % 4 == 0: the quad is entirely in or out
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int js = cs * 64, je = min(nc, js + 64);
+  if (i0 < n) {
+    const float* mm = M + i0 + (long long)j0 * ldm;
+    int j = js;
+    for (; j + 8 <= je; j += 8) {
+      float4 mv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        mv[u] = __ldg(reinterpret_cast<const float4*>(mm + (long long)(j + u) * ldm));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double pj = ps[j + u];
+        acc[0] = fma((double)mv[u].x, pj, acc[0]);
+        acc[1] = fma((double)mv[u].y, pj, acc[1]);
+        acc[2] = fma((double)mv[u].z, pj, acc[2]);
+        acc[3] = fma((double)mv[u].w, pj, acc[3]);
+      }
+    }
+    for (; j < je; ++j) {
+      const float4 mv = __ldg(reinterpret_cast<const float4*>(mm + (long long)j * ldm));
+      const double pj = ps[j];
+      acc[0] = fma((double)mv.x, pj, acc[0]);
+      acc[1] = fma((double)mv.y, pj, acc[1]);
+      acc[2] = fma((double)mv.z, pj, acc[2]);
+      acc[3] = fma((double)mv.w, pj, acc[3]);
+    }
+  }
+  if (cs > 0)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) sl[cs - 1][4 * q + r] = acc[r];
+  __syncthreads();
+  if (cs == 0 && i0 < n)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      part[(long long)cb * n + i0 + r] = ((acc[r] + sl[0][4 * q + r]) + sl[1][4 * q + r]) + sl[2][4 * q + r];
+}
+
 __global__ void tri_n_reduce_kernel(int n, int nch, const double* __restrict__ part,
                                     double* __restrict__ t, const int* __restrict__ done) {
   if (done && *done) return;
@@ -931,7 +995,15 @@ cudaError_t cg_launch_tri_n(int n, const double* M, long long ldm, const double*
 cudaError_t cg_launch_tri_n(int n, const float* M, long long ldm, const double* p, double* t,
                             double* part, const int* done, cudaStream_t st) {
   const int nch = cg_tri_chunks(n);
-  tri_n_part_kernel<float><<<nch * (nch + 1) / 2, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
+  static int v4 = -1;  // env TCQR_TRI_N_V4=0: one row per thread
+  if (v4 < 0) {
+    const char* e = getenv("TCQR_TRI_N_V4");
+    v4 = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (v4 && n % 4 == 0 && ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(M) & 15) == 0)
+    tri_n_part_f32v_kernel<<<nch * (nch + 1) / 2, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
+  else
+    tri_n_part_kernel<float><<<nch * (nch + 1) / 2, kTriBlk, 0, st>>>(n, M, ldm, p, part, done);
   tri_n_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, nch, part, t, done);
   return cudaGetLastError();
 }

@@ -6,7 +6,8 @@ each group runs in its own Python process and must pass the same oracle gates as
   group "fallbacks": TCQR_CAST_CLUSTER=0 (one-CTA-per-column / split-row casts), TCQR_TC2=0 (no
       CTA-pair GEMMs), TCQR_LOOKAHEAD_W=0 (no look-ahead), TCQR_CAST_OVERLAP=0 (casts in line),
       TCQR_NN_PRE_ALL=0 (NN epilogue with NBUF - 1 C chunks in flight), TCQR_L2_EF=0 (no L2
-      evict-first hints)
+      evict-first hints), TCQR_TRI_N_V4=0 (one row per thread in the CGLS M p partials); every
+      group also solves a small LLS
   group "variants":  TCQR_CAST_V8=0 (4096-row cluster CTAs), TCQR_TC2_NN_MINK=256 (CTA-pair NN
       from K = 256), TCQR_TN_MINKB=1 (finest split-K), TCQR_NN_SHORTK=0 (no short-K NN),
       TCQR_LOOKAHEAD_W=1024 with TCQR_LA_SMS=2 (leaf-wide deferred look-ahead blocks),
@@ -49,12 +50,20 @@ for cutoff in (128, 32):
 tq.set_config()
 qh, rh = tq.factor_host(a)
 assert r_rel_error(rh.astype(np.float64), r_o) <= 1e-2
+# LLS (the CGLS GEMVs and triangular products of the variant): x within 1e-10 of x_true
+al = W.gaussian(4096, 512, seed=72)
+xt = np.random.default_rng(73).standard_normal(512)
+Ad = tq.to_device_colmajor(al)
+b = torch.from_numpy(al.astype(np.float64) @ xt).cuda()
+x, info = tq.lls_solve(Ad, b, tol=1e-10, maxit=400)
+assert np.linalg.norm(x.cpu().numpy() - xt) <= 1e-10 * np.linalg.norm(xt), info
 print("ok")
 """
 
 GROUPS = {
     "fallbacks": {"TCQR_CAST_CLUSTER": "0", "TCQR_TC2": "0", "TCQR_LOOKAHEAD_W": "0",
-                  "TCQR_CAST_OVERLAP": "0", "TCQR_NN_PRE_ALL": "0", "TCQR_L2_EF": "0"},
+                  "TCQR_CAST_OVERLAP": "0", "TCQR_NN_PRE_ALL": "0", "TCQR_L2_EF": "0",
+                  "TCQR_TRI_N_V4": "0"},
     "variants": {"TCQR_CAST_V8": "0", "TCQR_TC2_NN_MINK": "256", "TCQR_TN_MINKB": "1",
                  "TCQR_NN_SHORTK": "0", "TCQR_LOOKAHEAD_W": "1024", "TCQR_LA_SMS": "2",
                  "TCQR_L2_EF": "15"},
