@@ -372,14 +372,20 @@ __device__ __forceinline__ void mgs_warp(Smem& s, int blk, int c0, int pw) {
     }
     __syncwarp();
   }
-  // the block's Gram G_b(i, j) = sum_{l <= i} R_b(l, i) R_b(l, j), i <= j (lane j: column j of
-  // R_b in registers, R_b(l, i) broadcast), packed upper triangle into u.Gp[blk]
+}
+
+// The block's Gram G_b(i, j) = sum_{l <= i} R_b(l, i) R_b(l, j), i <= j (lane j: column j of R_b in
+// registers, R_b(l, i) broadcast), packed upper triangle into u.Gp[blk]; rows i of parity `half`
+// (two warps per block after the MGS: warps b and b + 4, the same entries and order as one warp)
+__device__ __forceinline__ void block_gram(Smem& s, int blk, int half, int step) {
+  const int lane = threadIdx.x & 31;
+  const double* Rb = s.Rbd[blk];
   double rj[32];
 #pragma unroll
   for (int l = 0; l < 32; ++l) rj[l] = Rb[l * kLdR + lane];
   double* gp = s.u.Gp[blk];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
+  for (int i = half; i < 32; i += step) {
     double g = 0.0;
 #pragma unroll
     for (int l = 0; l <= i; ++l) g = fma(Rb[l * kLdR + i], rj[l], g);
@@ -487,10 +493,19 @@ __device__ __noinline__ void leaf_panel(const LeafArgs& a, Smem& s, int nrows, i
     } else {
 #pragma unroll 4
       for (int k = 0; k < 32; ++k) s.Rbd[warp][k * kLdR + lane] = 0.0;
-      for (int e = lane; e < 528; e += 32) s.u.Gp[warp][e] = 0.0;
+    }
+    // zero R_b (blocks past the rows): zero Gram.  First panel: the upper warps are still issuing
+    // the leaf's later columns, so each MGS warp takes its whole Gram before the barrier
+    if (first) {
+      __syncwarp();
+      block_gram(s, warp, 0, 1);
     }
   }
   __syncthreads();
+  if (!first) {  // later panels: warps b and b + 4 split block b's Gram
+    block_gram(s, warp & (kMW - 1), warp / kMW, 2);
+    __syncthreads();
+  }
   leaf_ts(a, slot);
   // (2) the CTA's part of the stack's Gram: G = (G_0 + G_1) + (G_2 + G_3) (FP64, fixed order;
   // packed upper triangle, zero past the panel), stored tagged; the owners sum the nb partials
