@@ -2270,6 +2270,8 @@ __global__ void debug_pollute_kernel(float4* p, long long n4, int evict_first) {
 }
 }  // namespace
 extern "C" int tcqr_debug_pollute(void* p, int64_t n, int evict_first) {
+  if (!g_ctx.inited) return TCQR_ERR_NOT_INIT;
+  if (!p || n < 4) return -1;
   debug_pollute_kernel<<<4 * 148, 256, 0, g_ctx.stream>>>(static_cast<float4*>(p), n / 4, evict_first);
   return cudaStreamSynchronize(g_ctx.stream) == cudaSuccess ? 0 : TCQR_ERR_CUDA;
 }
