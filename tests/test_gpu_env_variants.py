@@ -11,7 +11,8 @@ each group runs in its own Python process and must pass the same oracle gates as
   group "variants":  TCQR_CAST_V8=0 (4096-row cluster CTAs), TCQR_TC2_NN_MINK=256 (CTA-pair NN
       from K = 256), TCQR_TN_MINKB=1 (finest split-K), TCQR_NN_SHORTK=0 (no short-K NN),
       TCQR_LOOKAHEAD_W=1024 with TCQR_LA_SMS=2 (leaf-wide deferred look-ahead blocks),
-      TCQR_L2_EF=15 (evict-first hints on every operand and C tile)
+      TCQR_L2_EF=15 (evict-first hints on every operand and C tile), TCQR_LEAF_RESERVE=0 (the leaf
+      beside a look-ahead block takes every SM)
   group "host":      TCQR_CAST_COL_MIN=1 (per-column cast kernel at every width), TCQR_STREAM_DIV=4
       (coarse chunks of the streamed host factorization)
 """
@@ -66,7 +67,7 @@ GROUPS = {
                   "TCQR_TRI_N_V4": "0"},
     "variants": {"TCQR_CAST_V8": "0", "TCQR_TC2_NN_MINK": "256", "TCQR_TN_MINKB": "1",
                  "TCQR_NN_SHORTK": "0", "TCQR_LOOKAHEAD_W": "1024", "TCQR_LA_SMS": "2",
-                 "TCQR_L2_EF": "15"},
+                 "TCQR_L2_EF": "15", "TCQR_LEAF_RESERVE": "0"},
     "host": {"TCQR_CAST_COL_MIN": "1", "TCQR_STREAM_DIV": "4"},
 }
 
