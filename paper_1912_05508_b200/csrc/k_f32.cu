@@ -11,6 +11,15 @@ namespace tcqr {
 
 constexpr int kTnRows = 64;   // rows per shared-memory chunk
 constexpr int kTnPad = 68;    // row stride (floats) of the staged tiles, 16-byte aligned
+#ifndef TCQR_PROJ_OCC
+#define TCQR_PROJ_OCC 2
+#endif
+#ifndef TCQR_PROJ_SLICE
+#define TCQR_PROJ_SLICE 16
+#endif
+// streaming projection: CTAs per SM and the update's column slice (registers: two CTAs per SM
+// need <= 128 per thread)
+constexpr int kProjOcc = TCQR_PROJ_OCC, kProjSlice = TCQR_PROJ_SLICE;
 constexpr int kResSmemMax = 220 * 1024;  // dynamic shared memory cap of the resident projection
 
 // P_s (h x w2, ld h) = sum over rows [r0_s, r1_s) of Q1(r, :)' A2(r, :).  h, w2 <= 64.
@@ -295,7 +304,7 @@ __device__ __forceinline__ void proj_phase2(const float* P, float* T, float* Rbl
 }
 
 template <int TD>  // TD = 32 or 64: h, w2 <= TD
-__global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w2,
+__global__ void __launch_bounds__(256, kProjOcc) f32_project_kernel(int m, int h, int w2,
                                                              const float* __restrict__ Q1,
                                                              long long ldq, float* A2,
                                                              long long lda, float* Rblk,
@@ -422,19 +431,19 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
 #pragma unroll
       for (int i = 0; i < TD; ++i) qrow[i] = (i < h) ? __ldg(Q1 + row + (long long)i * ldq) : 0.f;
 #pragma unroll 1
-      for (int jh = 0; jh < TD; jh += 32) {  // 32-column halves keep registers bounded
-        float cold[32];
+      for (int jh = 0; jh < TD; jh += kProjSlice) {  // column slices keep registers bounded
+        float cold[kProjSlice];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) cold[j] = (jh + j < w2) ? A2[row + (long long)(jh + j) * lda] : 0.f;
-        float acc[32];
+        for (int j = 0; j < kProjSlice; ++j) cold[j] = (jh + j < w2) ? A2[row + (long long)(jh + j) * lda] : 0.f;
+        float acc[kProjSlice];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        for (int j = 0; j < kProjSlice; ++j) acc[j] = 0.f;
 #pragma unroll
         for (int i = 0; i < TD; ++i) {
           if (i < h) {
             const float2 qi = make_float2(qrow[i], qrow[i]);
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {  // FFMA2: the same fmaf sequence per entry
+            for (int j = 0; j < kProjSlice; j += 4) {  // FFMA2: the same fmaf sequence per entry
               const float4 tv = *reinterpret_cast<const float4*>(&Ts[i * TD + jh + j]);
               const float2 c01 = ffma2(qi, make_float2(tv.x, tv.y), make_float2(acc[j], acc[j + 1]));
               const float2 c23 = ffma2(qi, make_float2(tv.z, tv.w),
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(256, 1) f32_project_kernel(int m, int h, int w
           }
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
+        for (int j = 0; j < kProjSlice; ++j)
           if (jh + j < w2) A2[row + (long long)(jh + j) * lda] = cold[j] - acc[j];
       }
     }
