@@ -32,7 +32,7 @@ struct TcCfg {
   // NBUF = 0: direct-load epilogue; 2 / 4: TMA epilogue with that many 16 KB C-chunk buffers (4
   // buffers prefetch three chunks ahead for short-K updates at the cost of one mainloop stage; 2
   // keep the full mainloop depth for long K, where the epilogue hides behind the next tile)
-  // NBUF = 2 is the short-K update (K = h <= 512, BN = 128): two mainloop stages, 97 KB of
+  // NBUF = 2 is the short-K update (K = h <= 1024, BN = 128): two mainloop stages, 97 KB of
   // shared memory and 256 TMEM columns, so TWO CTAs share an SM and one CTA's C loads overlap the
   // other's epilogue (the deep levels are HBM-bound on the C read-modify-write)
   static constexpr int CBUF = NBUF * 16384;
@@ -879,7 +879,7 @@ static int nn_short_k() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("TCQR_NN_SHORTK");
-    v = e ? atoi(e) : 512;
+    v = e ? atoi(e) : 1024;  // config 3: 1024 -> w = 2048 gaps 221 -> 204 us (2048: w = 4096 worse)
   }
   return v;
 }

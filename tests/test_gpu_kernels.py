@@ -96,6 +96,8 @@ def test_gemm_tn_envelope(tq, m, h, w2):
                                     # K = h <= 256: the two-CTAs-per-SM short-K variant, with more
                                     # tiles than CTA slots (persistent loop) and ragged rows/columns
                                     (40000, 128, 256), (33000, 200, 130), (70000, 256, 128),
+                                    # K = h in (512, 1024]: the short-K variant with a long K loop
+                                    (20000, 1000, 200), (8192, 1024, 1024),
                                     # h > 2048, w2 >= 256: the CTA-pair kernel (ragged tiles)
                                     (4104, 2304, 320), (704, 4096, 256)])
 def test_gemm_nn_update_envelope(tq, m, h, w2):
